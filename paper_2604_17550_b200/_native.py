@@ -1,0 +1,126 @@
+"""Build and load ``libflint_b200.so`` (the CUDA engine behind include/flint_b200.h).
+
+The library is compiled in-tree for sm_100a only
+(``-gencode arch=compute_100a,code=sm_100a``) and loaded with ctypes.  There
+is no fallback: if the library is missing or no GPU is visible, every engine
+entry point raises :class:`~paper_2604_17550_b200.errors.EngineError`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+from .errors import EngineError
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+BUILD = PKG / "_build"
+LIB = BUILD / "libflint_b200.so"
+SOURCES = [PKG / "csrc" / "engine.cu", PKG / "csrc" / "capi.cu"]
+HEADERS = [ROOT / "include" / "flint_b200.h", PKG / "csrc" / "engine_internal.h"]
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-fmad=false",                 # no FMA contraction: bit-exact fp64 cost model
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (Path(cand).exists() or cand == "nvcc"):
+            return cand
+    return "nvcc"
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    BUILD.mkdir(exist_ok=True)
+    newest = max(p.stat().st_mtime for p in SOURCES + HEADERS)
+    if not force and LIB.exists() and LIB.stat().st_mtime >= newest:
+        return LIB
+    cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-I", str(PKG / "csrc"),
+           *map(str, SOURCES), "-o", str(LIB) + ".tmp"]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise EngineError("nvcc failed:\n" + res.stderr[-4000:])
+    os.replace(str(LIB) + ".tmp", LIB)
+    return LIB
+
+
+P64 = C.POINTER(C.c_int64)
+P32 = C.POINTER(C.c_int32)
+PU8 = C.POINTER(C.c_uint8)
+PF64 = C.POINTER(C.c_double)
+
+
+class GraphDesc(C.Structure):
+    _fields_ = [
+        ("n_ranks", C.c_int32), ("rank_struct", P32), ("rank_graph_pos", P32),
+        ("n_structs", C.c_int32), ("s_node_off", P32), ("s_tens_off", P32), ("s_init_off", P32),
+        ("s_init_alloc", P64), ("s_ncoll", P32),
+        ("node_kind", PU8), ("node_flags", PU8), ("node_id", P64), ("node_dur", P64),
+        ("node_flops", P64), ("node_alloc", P64), ("node_coll_ord", P32),
+        ("pred_off", P32), ("pred_idx", P32), ("succ_off", P32), ("succ_idx", P32),
+        ("free_off", P32), ("free_tens", P32), ("init_list", P32),
+        ("tens_bytes", P64), ("tens_cons_off", P32), ("tens_cons", P32),
+        ("n_inst", C.c_int32), ("inst_kind", PU8), ("inst_n", P32), ("inst_bytes", P64),
+        ("inst_lead_id", P64), ("inst_init_key", P64), ("inst_mem_off", P64),
+        ("inst_mem_rank", P32), ("inst_mem_node", P32),
+        ("coll_stride", C.c_int32), ("rank_coll_inst", P32),
+    ]
+
+
+class Points(C.Structure):
+    _fields_ = [
+        ("n_points", C.c_int32), ("algo", PU8), ("topo_kind", PU8), ("bw", PF64),
+        ("latency", P64), ("rows", P32), ("cols", P32), ("peak_flops", PF64),
+        ("efficiency", PF64), ("compute_streams", C.c_int32),
+    ]
+
+
+class Outputs(C.Structure):
+    _fields_ = [("status", P32), ("rows", P64), ("rank_stats", P64),
+                ("ev_start", P64), ("ev_end", P64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load the engine (building it first if this is a source checkout)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB.exists():
+        try:
+            build()
+        except (OSError, EngineError) as e:
+            raise EngineError(f"CUDA engine library {LIB} is missing and could not be built: {e}") from e
+    L = C.CDLL(str(LIB))
+    L.fl_version.restype = C.c_int
+    L.fl_last_error.restype = C.c_char_p
+    L.fl_device_count.argtypes = [P32]
+    L.fl_graph_create.argtypes = [C.POINTER(GraphDesc), C.c_int32, C.POINTER(C.c_void_p)]
+    L.fl_graph_destroy.argtypes = [C.c_void_p]
+    L.fl_graph_max_nodes.argtypes = [C.c_void_p]
+    L.fl_graph_max_nodes.restype = C.c_int32
+    L.fl_sweep_run.argtypes = [C.c_void_p, C.POINTER(Points), C.POINTER(Outputs)]
+    L.fl_sweep_run_device.argtypes = [C.c_void_p, C.POINTER(Points), C.POINTER(Outputs), C.c_void_p, P32]
+    L.fl_cost_only.argtypes = [C.c_int32, PU8, P64, P64, PU8, PF64, PF64, P32, P32, P64, P32,
+                               C.c_int32, P64, PF64, PF64, P64]
+    _lib = L
+    return L
+
+
+def last_error() -> str:
+    return lib().fl_last_error().decode(errors="replace")
+
+
+EXPORTED = ["fl_version", "fl_last_error", "fl_device_count", "fl_graph_create", "fl_graph_destroy",
+            "fl_graph_max_nodes", "fl_sweep_run", "fl_sweep_run_device", "fl_cost_only"]

@@ -1,0 +1,366 @@
+// capi.cu -- the extern "C" boundary declared in include/flint_b200.h.
+//
+// Owns device memory for compiled graph sets (fl_graph) and their per-CTA
+// scratch, validates descriptors, launches the engine kernels.  No torch
+// types cross this boundary; the Python layer binds it with ctypes.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "flint_b200.h"
+#include "engine_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(expr)                                                                      \
+    do {                                                                              \
+        cudaError_t e_ = (expr);                                                      \
+        if (e_ != cudaSuccess)                                                        \
+            return fail(FL_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct fl_graph {
+    int device;
+    fl::DevGraph dg;
+    std::vector<void *> allocs;
+    // scratch, grown on demand
+    unsigned char *scratch = nullptr;
+    size_t scratch_bytes = 0;
+    fl::DevScratch sc{};
+    int grid_cap = 0;
+    int block = 32;
+    size_t smem = 0;
+};
+
+namespace {
+
+template <typename T>
+int upload(fl_graph *g, const T *host, size_t n, const T **dev) {
+    if (n == 0) n = 1;   // keep a valid pointer for empty tables
+    void *p = nullptr;
+    CK(cudaMalloc(&p, n * sizeof(T)));
+    g->allocs.push_back(p);
+    if (host) CK(cudaMemcpy(p, host, n * sizeof(T), cudaMemcpyHostToDevice));
+    else CK(cudaMemset(p, 0, n * sizeof(T)));
+    *dev = static_cast<const T *>(p);
+    return FL_OK;
+}
+
+#define UP(field, n)                                                   \
+    do {                                                               \
+        int rc_ = upload(g, d->field, (size_t)(n), &g->dg.field);      \
+        if (rc_) return rc_;                                           \
+    } while (0)
+
+int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
+    if (!d || d->n_ranks < 1 || d->n_structs < 1) return fail(FL_ERR_INVALID, "empty graph set");
+    if (d->n_ranks > FL_MAX_RANKS)
+        return fail(FL_ERR_CAPACITY, "this build evaluates at most " + std::to_string(FL_MAX_RANKS) + " ranks per design point");
+    const int R = d->n_ranks, S = d->n_structs;
+    int max_nodes = 0;
+    for (int s = 0; s < S; s++) {
+        int n = d->s_node_off[s + 1] - d->s_node_off[s];
+        if (n > FL_MAX_NODES_PER_RANK)
+            return fail(FL_ERR_CAPACITY, "a rank graph has more than " + std::to_string(FL_MAX_NODES_PER_RANK) + " nodes");
+        max_nodes = n > max_nodes ? n : max_nodes;
+    }
+    for (int r = 0; r < R; r++)
+        if (d->rank_struct[r] < 0 || d->rank_struct[r] >= S) return fail(FL_ERR_INVALID, "rank_struct out of range");
+    const int total = d->s_node_off[S], total_t = d->s_tens_off[S];
+    for (int i = 0; i < total; i++) {
+        int k = d->node_kind[i];
+        if (k == FL_SEND || k == FL_RECV)
+            return fail(FL_ERR_CAPACITY, "SEND/RECV (expanded comm mode) is not supported by this build");
+        if (k > FL_RECV) return fail(FL_ERR_INVALID, "bad node kind");
+        if (d->succ_off[i + 1] - d->succ_off[i] >= 4096) return fail(FL_ERR_CAPACITY, "node fan-out >= 4096");
+    }
+    CK(cudaSetDevice(device));
+    g->device = device;
+    fl::DevGraph &dg = g->dg;
+    dg.R = R;
+    dg.S = S;
+    dg.n_inst = d->n_inst;
+    dg.coll_stride = d->coll_stride > 0 ? d->coll_stride : 1;
+    dg.max_nodes = max_nodes > 0 ? max_nodes : 1;
+    dg.max_words = (dg.max_nodes + 63) / 64;
+    dg.total_nodes = total;
+    dg.total_tens = total_t;
+    const int ne_pred = d->pred_off[total], ne_succ = d->succ_off[total], ne_free = d->free_off[total];
+    const int ne_cons = d->tens_cons_off[total_t], ne_init = d->s_init_off[S];
+    const int64_t ne_mem = d->inst_mem_off[d->n_inst];
+    UP(rank_struct, R);
+    UP(s_node_off, S + 1);
+    UP(s_tens_off, S + 1);
+    UP(s_init_off, S + 1);
+    UP(s_ncoll, S);
+    UP(s_init_alloc, S);
+    UP(node_kind, total);
+    UP(node_flags, total);
+    UP(node_dur, total);
+    UP(node_flops, total);
+    UP(node_alloc, total);
+    UP(node_coll_ord, total);
+    UP(pred_off, total + 1);
+    UP(pred_idx, ne_pred);
+    UP(succ_off, total + 1);
+    UP(succ_idx, ne_succ);
+    UP(free_off, total + 1);
+    UP(free_tens, ne_free);
+    UP(init_list, ne_init);
+    UP(tens_bytes, total_t);
+    UP(tens_cons_off, total_t + 1);
+    UP(tens_cons, ne_cons);
+    UP(inst_kind, d->n_inst);
+    UP(inst_n, d->n_inst);
+    UP(inst_bytes, d->n_inst);
+    UP(inst_lead_id, d->n_inst);
+    UP(inst_init_key, d->n_inst);
+    UP(inst_mem_off, d->n_inst + 1);
+    UP(inst_mem_rank, ne_mem);
+    UP(inst_mem_node, ne_mem);
+    {
+        int rc = upload(g, d->rank_coll_inst, (size_t)R * dg.coll_stride, &dg.rank_coll_inst);
+        if (rc) return rc;
+    }
+
+    // launch geometry: one thread per rank, one CTA per design point
+    g->block = (R + 31) / 32 * 32;
+    g->smem = sizeof(uint64_t) * 64 + sizeof(int64_t) * 64 + 64 + (size_t)R * 12 + 64;
+    int sms = 0, occ = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    CK(fl::sweep_occupancy(g->block, g->smem, &occ));
+    if (occ < 1) occ = 1;
+    g->grid_cap = sms * occ;
+
+    // per-CTA scratch layout
+    fl::DevScratch &sc = g->sc;
+    size_t off = 0;
+    sc.off_bits = off; off = align_up(off + 4 * (size_t)dg.max_words * R * 8, 256);
+    sc.off_cp = off;   off = align_up(off + (size_t)dg.max_nodes * R * 8, 256);
+    sc.off_ring = off; off = align_up(off + 2 * (size_t)dg.coll_stride * R * 4, 256);
+    sc.off_dur = off;  off = align_up(off + (size_t)(total > 0 ? total : 1) * 8, 256);
+    sc.off_inst = off; off = align_up(off + (size_t)(d->n_inst > 0 ? d->n_inst : 1) * (5 * 8 + 2 * 4), 256);
+    sc.slot_bytes = off;
+    return FL_OK;
+}
+
+int ensure_scratch(fl_graph *g, int grid) {
+    size_t need = g->sc.slot_bytes * (size_t)grid;
+    if (need <= g->scratch_bytes) return FL_OK;
+    if (g->scratch) cudaFree(g->scratch);
+    g->scratch = nullptr;
+    g->scratch_bytes = 0;
+    CK(cudaMalloc(&g->scratch, need));
+    g->scratch_bytes = need;
+    g->sc.base = g->scratch;
+    return FL_OK;
+}
+
+int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stream) {
+    if (pts->n_points <= 0) return FL_OK;
+    int cs = pts->compute_streams;
+    if (cs < 1 || cs > 4) return fail(FL_ERR_CAPACITY, "compute_streams must be 1..4 in this build");
+    int grid = pts->n_points < g->grid_cap ? pts->n_points : g->grid_cap;
+    int rc = ensure_scratch(g, grid);
+    if (rc) return rc;
+    fl::DevPoints dp;
+    dp.n = pts->n_points;
+    dp.algo = pts->algo;
+    dp.topo_kind = pts->topo_kind;
+    dp.bw = pts->bw;
+    dp.latency = pts->latency;
+    dp.rows = pts->rows;
+    dp.cols = pts->cols;
+    dp.peak_flops = pts->peak_flops;
+    dp.efficiency = pts->efficiency;
+    dp.compute_streams = cs;
+    fl::DevOut dout;
+    dout.status = out->status;
+    dout.rows = out->rows;
+    dout.rank_stats = out->rank_stats;
+    dout.ev_start = out->ev_start;
+    dout.ev_end = out->ev_end;
+    CK(fl::launch_sweep(cs == 3 ? 4 : cs, grid, g->block, g->smem, stream, g->dg, dp, dout, g->sc));
+    return FL_OK;
+}
+
+template <typename T>
+int to_dev(const T *host, size_t n, T **dev, std::vector<void *> &tmp) {
+    *dev = nullptr;
+    if (!host) return FL_OK;
+    void *p = nullptr;
+    CK(cudaMalloc(&p, (n ? n : 1) * sizeof(T)));
+    tmp.push_back(p);
+    if (n) CK(cudaMemcpy(p, host, n * sizeof(T), cudaMemcpyHostToDevice));
+    *dev = static_cast<T *>(p);
+    return FL_OK;
+}
+
+void free_all(std::vector<void *> &v) {
+    for (void *p : v) cudaFree(p);
+    v.clear();
+}
+
+}  // namespace
+
+extern "C" {
+
+int fl_version(void) { return FL_ABI_VERSION; }
+
+const char *fl_last_error(void) { return g_err.c_str(); }
+
+int fl_device_count(int32_t *count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    *count = e == cudaSuccess ? n : 0;
+    if (e != cudaSuccess) return fail(FL_ERR_CUDA, cudaGetErrorString(e));
+    return FL_OK;
+}
+
+int fl_graph_create(const fl_graph_desc *desc, int32_t device, fl_graph **out) {
+    *out = nullptr;
+    fl_graph *g = new fl_graph();
+    int rc = create(desc, device, g);
+    if (rc) {
+        fl_graph_destroy(g);
+        return rc;
+    }
+    *out = g;
+    return FL_OK;
+}
+
+int fl_graph_destroy(fl_graph *g) {
+    if (!g) return FL_OK;
+    cudaSetDevice(g->device);
+    for (void *p : g->allocs) cudaFree(p);
+    if (g->scratch) cudaFree(g->scratch);
+    delete g;
+    return FL_OK;
+}
+
+int32_t fl_graph_max_nodes(const fl_graph *g) { return g ? g->dg.max_nodes : 0; }
+
+int fl_sweep_run_device(fl_graph *g, const fl_points *dev_points, fl_outputs *dev_out, void *stream,
+                        int32_t *launches) {
+    if (!g || !dev_points || !dev_out) return fail(FL_ERR_INVALID, "null argument");
+    CK(cudaSetDevice(g->device));
+    int rc = launch(g, dev_points, dev_out, static_cast<cudaStream_t>(stream));
+    if (launches) *launches = rc == FL_OK && dev_points->n_points > 0 ? 1 : 0;
+    return rc;
+}
+
+int fl_sweep_run(fl_graph *g, const fl_points *hp, fl_outputs *ho) {
+    if (!g || !hp || !ho) return fail(FL_ERR_INVALID, "null argument");
+    CK(cudaSetDevice(g->device));
+    const size_t n = (size_t)hp->n_points;
+    if (n == 0) return FL_OK;
+    std::vector<void *> tmp;
+    fl_points dp = *hp;
+    fl_outputs dout{};
+    int rc = FL_OK;
+    uint8_t *algo, *topo;
+    double *bw, *peak = nullptr, *eff = nullptr;
+    int64_t *lat;
+    int32_t *rows, *cols, *status;
+    int64_t *orows, *rs = nullptr, *es = nullptr, *ee = nullptr;
+    const size_t R = (size_t)g->dg.R, MN = (size_t)g->dg.max_nodes;
+    if ((rc = to_dev(hp->algo, n, &algo, tmp)) || (rc = to_dev(hp->topo_kind, n, &topo, tmp)) ||
+        (rc = to_dev(hp->bw, n, &bw, tmp)) || (rc = to_dev(hp->latency, n, &lat, tmp)) ||
+        (rc = to_dev(hp->rows, n, &rows, tmp)) || (rc = to_dev(hp->cols, n, &cols, tmp)) ||
+        (rc = to_dev(hp->peak_flops, n, &peak, tmp)) || (rc = to_dev(hp->efficiency, n, &eff, tmp))) {
+        free_all(tmp);
+        return rc;
+    }
+    auto dalloc = [&](size_t bytes, void **p) -> int {
+        cudaError_t e = cudaMalloc(p, bytes ? bytes : 1);
+        if (e != cudaSuccess) return fail(FL_ERR_CUDA, cudaGetErrorString(e));
+        tmp.push_back(*p);
+        return FL_OK;
+    };
+    if ((rc = dalloc(n * 4, (void **)&status)) || (rc = dalloc(n * 6 * 8, (void **)&orows)) ||
+        (ho->rank_stats && (rc = dalloc(n * R * 5 * 8, (void **)&rs))) ||
+        (ho->ev_start && (rc = dalloc(n * R * MN * 8, (void **)&es))) ||
+        (ho->ev_start && (rc = dalloc(n * R * MN * 8, (void **)&ee)))) {
+        free_all(tmp);
+        return rc;
+    }
+    dp.algo = algo; dp.topo_kind = topo; dp.bw = bw; dp.latency = lat; dp.rows = rows; dp.cols = cols;
+    dp.peak_flops = peak; dp.efficiency = eff;
+    dout.status = status; dout.rows = orows; dout.rank_stats = rs; dout.ev_start = es; dout.ev_end = ee;
+    rc = launch(g, &dp, &dout, 0);
+    if (rc == FL_OK) {
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) rc = fail(FL_ERR_CUDA, std::string("engine kernel: ") + cudaGetErrorString(e));
+    }
+    if (rc == FL_OK) {
+        cudaMemcpy(ho->status, status, n * 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(ho->rows, orows, n * 6 * 8, cudaMemcpyDeviceToHost);
+        if (rs) cudaMemcpy(ho->rank_stats, rs, n * R * 5 * 8, cudaMemcpyDeviceToHost);
+        if (es) {
+            cudaMemcpy(ho->ev_start, es, n * R * MN * 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(ho->ev_end, ee, n * R * MN * 8, cudaMemcpyDeviceToHost);
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = fail(FL_ERR_CUDA, cudaGetErrorString(e));
+    }
+    free_all(tmp);
+    return rc;
+}
+
+int fl_cost_only(int32_t n, const uint8_t *kind, const int64_t *size_bytes, const int64_t *group_n,
+                 const uint8_t *algo, const double *alpha, const double *beta, const int32_t *rows,
+                 const int32_t *cols, int64_t *out_ns, int32_t *out_status, int32_t m,
+                 const int64_t *flops, const double *peak, const double *eff, int64_t *out_comp_ns) {
+    std::vector<void *> tmp;
+    uint8_t *dk = nullptr, *da = nullptr;
+    int64_t *ds = nullptr, *dn = nullptr, *dout = nullptr, *dfl = nullptr, *dcomp = nullptr;
+    double *dal = nullptr, *dbe = nullptr, *dpk = nullptr, *def = nullptr;
+    int32_t *dr = nullptr, *dc = nullptr, *dst = nullptr;
+    int rc;
+    const size_t N = n > 0 ? n : 0, M = m > 0 ? m : 0;
+    if ((rc = to_dev(kind, N, &dk, tmp)) || (rc = to_dev(size_bytes, N, &ds, tmp)) ||
+        (rc = to_dev(group_n, N, &dn, tmp)) || (rc = to_dev(algo, N, &da, tmp)) ||
+        (rc = to_dev(alpha, N, &dal, tmp)) || (rc = to_dev(beta, N, &dbe, tmp)) ||
+        (rc = to_dev(rows, N, &dr, tmp)) || (rc = to_dev(cols, N, &dc, tmp)) ||
+        (rc = to_dev(flops, M, &dfl, tmp)) || (rc = to_dev(peak, M, &dpk, tmp)) ||
+        (rc = to_dev(eff, M, &def, tmp)) || (rc = to_dev(out_ns, N, &dout, tmp)) ||
+        (rc = to_dev(out_status, N, &dst, tmp)) || (rc = to_dev(out_comp_ns, M, &dcomp, tmp))) {
+        free_all(tmp);
+        return rc;
+    }
+    int total = (int)(N > M ? N : M);
+    if (total > 0) {
+        cudaError_t e = fl::launch_cost_only((int)N, dk, ds, dn, da, dal, dbe, dr, dc, dout, dst, (int)M, dfl,
+                                             dpk, def, dcomp);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+            free_all(tmp);
+            return fail(FL_ERR_CUDA, cudaGetErrorString(e));
+        }
+        if (N) {
+            cudaMemcpy(out_ns, dout, N * 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(out_status, dst, N * 4, cudaMemcpyDeviceToHost);
+        }
+        if (M) cudaMemcpy(out_comp_ns, dcomp, M * 8, cudaMemcpyDeviceToHost);
+    }
+    free_all(tmp);
+    return FL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,55 @@
+// engine_internal.h -- device-side views shared by engine.cu and capi.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fl {
+
+// Device copy of fl_graph_desc (pointers are device pointers).
+struct DevGraph {
+    int R, S, n_inst, coll_stride, max_nodes, max_words, total_nodes, total_tens;
+    const int32_t *rank_struct;
+    const int32_t *s_node_off, *s_tens_off, *s_init_off, *s_ncoll;
+    const int64_t *s_init_alloc;
+    const uint8_t *node_kind, *node_flags;
+    const int64_t *node_dur, *node_flops, *node_alloc;
+    const int32_t *node_coll_ord, *pred_off, *pred_idx, *succ_off, *succ_idx, *free_off, *free_tens, *init_list;
+    const int64_t *tens_bytes;
+    const int32_t *tens_cons_off, *tens_cons;
+    const uint8_t *inst_kind;
+    const int32_t *inst_n;
+    const int64_t *inst_bytes, *inst_lead_id, *inst_init_key, *inst_mem_off;
+    const int32_t *inst_mem_rank, *inst_mem_node, *rank_coll_inst;
+};
+
+struct DevPoints {
+    int n;
+    const uint8_t *algo, *topo_kind;
+    const double *bw;
+    const int64_t *latency;
+    const int32_t *rows, *cols;
+    const double *peak_flops, *efficiency;
+    int compute_streams;
+};
+
+struct DevOut {
+    int32_t *status;
+    int64_t *rows, *rank_stats, *ev_start, *ev_end;
+};
+
+// Per-CTA scratch: slot_bytes each, laid out at the given byte offsets.
+struct DevScratch {
+    unsigned char *base;
+    size_t slot_bytes, off_bits, off_cp, off_ring, off_dur, off_inst;
+};
+
+cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t st, const DevGraph &g,
+                         const DevPoints &p, const DevOut &o, const DevScratch &sc);
+cudaError_t sweep_occupancy(int block, size_t smem, int *occ);
+cudaError_t launch_cost_only(int n, const uint8_t *kind, const int64_t *size, const int64_t *gn,
+                             const uint8_t *algo, const double *alpha, const double *beta,
+                             const int32_t *rows, const int32_t *cols, int64_t *out, int32_t *status,
+                             int m, const int64_t *flops, const double *peak, const double *eff,
+                             int64_t *out_comp);
+
+}  // namespace fl

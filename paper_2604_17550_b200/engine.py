@@ -1,0 +1,320 @@
+"""Reference-facing API over the CUDA engine.
+
+Drop-in replacements for the reference's hot-path functions, same names,
+argument meaning and exceptions:
+
+* :func:`simulate` -- ``trainsim.simulate`` (pkg/src/trainsim/simulator.py:203-367)
+* :func:`critical_path` -- ``trainsim.critical_path`` (simulator.py:400-460)
+
+plus the batched entry point the reference lacks, :func:`simulate_batch`
+(one compiled graph set x N design points -> N sweep rows), and
+:class:`Engine`, a graph set resident on one GPU.
+
+Every call runs on the GPU through ``libflint_b200.so``; there is no CPU
+path.  Results are bit-identical to the reference (tests/test_gpu_parity.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _native
+from .costs import CollectiveAlgo
+from .errors import (EngineError, FL_ERR_NOT_RUN, FL_OK, raise_for_status)
+from .store import GraphSet, check_supported, compile_graphs, desc_arrays
+
+ALGO = {"ring": 0, "tree": 1, "mesh-hier": 2}
+ROW_FIELDS = ("makespan_ns", "critical_path_ns", "compute_busy_ns", "comm_busy_ns",
+              "exposed_comm_ns", "peak_mem_bytes")
+
+
+def _ev(x):
+    return x.value if hasattr(x, "value") else x
+
+
+# ------------------------------------------------------------ report types
+# (simulator.py:45-106)
+
+
+@dataclass
+class SimOptions:
+    algo: CollectiveAlgo = CollectiveAlgo.RING
+    compute_streams: int = 1
+    comm_streams: int = 1
+    record_events: bool = True
+
+
+@dataclass
+class TraceEvent:
+    rank: int
+    node_id: int
+    stream: str
+    op_name: str
+    start_ns: int
+    end_ns: int
+
+
+@dataclass
+class RankStats:
+    finish_ns: int = 0
+    compute_busy_ns: int = 0
+    comm_busy_ns: int = 0
+    exposed_comm_ns: int = 0
+    peak_mem_bytes: int = 0
+
+
+@dataclass
+class SimReport:
+    makespan_ns: int
+    ranks: dict
+    link_busy_ns: dict = field(default_factory=dict)
+    events: list = field(default_factory=list)
+
+    @property
+    def exposed_comm_ns(self) -> int:
+        return max((s.exposed_comm_ns for s in self.ranks.values()), default=0)
+
+    @property
+    def peak_mem_bytes(self) -> int:
+        return max((s.peak_mem_bytes for s in self.ranks.values()), default=0)
+
+    def to_doc(self) -> dict:
+        return {
+            "format_version": "sim-trace/1",
+            "makespan_ns": self.makespan_ns,
+            "ranks": {str(r): {"finish_ns": s.finish_ns, "compute_busy_ns": s.compute_busy_ns,
+                               "comm_busy_ns": s.comm_busy_ns, "exposed_comm_ns": s.exposed_comm_ns,
+                               "peak_mem_bytes": s.peak_mem_bytes}
+                      for r, s in sorted(self.ranks.items())},
+            "links": dict(sorted(self.link_busy_ns.items())),
+            "events": [{"rank": e.rank, "node_id": e.node_id, "stream": e.stream, "op": e.op_name,
+                        "start_ns": e.start_ns, "end_ns": e.end_ns} for e in self.events],
+        }
+
+
+# ------------------------------------------------------------ design points
+
+
+@dataclass
+class DesignPoints:
+    """Structure-of-arrays design points (fl_points)."""
+    algo: np.ndarray          # uint8 (ring=0, tree=1, mesh-hier=2)
+    topo_kind: np.ndarray     # uint8 (switch=0, mesh=1)
+    bw: np.ndarray            # float64 bytes/s
+    latency: np.ndarray       # int64 ns
+    rows: np.ndarray          # int32
+    cols: np.ndarray          # int32
+    peak_flops: Optional[np.ndarray] = None   # float64; None keeps each node's duration_ns
+    efficiency: Optional[np.ndarray] = None
+    compute_streams: int = 1
+
+    def __len__(self) -> int:
+        return len(self.bw)
+
+    @classmethod
+    def from_topologies(cls, topos, algos, devices=None, compute_streams: int = 1) -> "DesignPoints":
+        n = len(topos)
+        algos = list(algos) if not isinstance(algos, (str, CollectiveAlgo)) else [algos] * n
+        pts = cls(algo=np.asarray([ALGO[_ev(a)] for a in algos], np.uint8),
+                  topo_kind=np.asarray([0 if _ev(t.kind) == "switch" else 1 for t in topos], np.uint8),
+                  bw=np.asarray([float(t.bw_bytes_per_s) for t in topos], np.float64),
+                  latency=np.asarray([int(t.latency_ns) for t in topos], np.int64),
+                  rows=np.asarray([int(getattr(t, "rows", 0)) for t in topos], np.int32),
+                  cols=np.asarray([int(getattr(t, "cols", 0)) for t in topos], np.int32),
+                  compute_streams=compute_streams)
+        if devices is not None:
+            pts.peak_flops = np.asarray([d.peak_flops for d in devices], np.float64)
+            pts.efficiency = np.asarray([d.efficiency for d in devices], np.float64)
+        return pts
+
+    def slice(self, a: int, b: int) -> "DesignPoints":
+        f = lambda x: None if x is None else np.ascontiguousarray(x[a:b])
+        return DesignPoints(f(self.algo), f(self.topo_kind), f(self.bw), f(self.latency), f(self.rows),
+                            f(self.cols), f(self.peak_flops), f(self.efficiency), self.compute_streams)
+
+
+def _ptr(a, typ):
+    return None if a is None else a.ctypes.data_as(typ)
+
+
+# ------------------------------------------------------------ engine handle
+
+
+class Engine:
+    """A compiled graph set resident on one GPU (an ``fl_graph`` handle)."""
+
+    def __init__(self, graphs_or_set, device: int = 0):
+        self.gs = graphs_or_set if isinstance(graphs_or_set, GraphSet) else compile_graphs(graphs_or_set)
+        check_supported(self.gs)
+        L = _native.lib()
+        arrs = desc_arrays(self.gs)
+        d = _native.GraphDesc()
+        keep = []
+        for name, typ in _native.GraphDesc._fields_:
+            v = arrs[name]
+            if isinstance(v, np.ndarray):
+                if v.size == 0:
+                    v = np.zeros(1, v.dtype)
+                v = np.ascontiguousarray(v)
+                keep.append(v)
+                setattr(d, name, v.ctypes.data_as(typ))
+            else:
+                setattr(d, name, v)
+        h = C.c_void_p()
+        rc = L.fl_graph_create(C.byref(d), device, C.byref(h))
+        if rc:
+            raise EngineError(f"fl_graph_create: {_native.last_error()} (status {rc})")
+        self._h = h
+        self.device = device
+        self.max_nodes = int(L.fl_graph_max_nodes(h))
+        self.units_per_point = self.gs.units()
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _native.lib().fl_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def run(self, pts: DesignPoints, rank_stats: bool = False, events: bool = False) -> dict:
+        """Evaluate design points from host buffers (copies included)."""
+        n = len(pts)
+        R = self.gs.n_ranks
+        out = {"status": np.zeros(n, np.int32), "rows": np.zeros((n, 6), np.int64)}
+        if rank_stats:
+            out["rank_stats"] = np.zeros((n, R, 5), np.int64)
+        if events:
+            out["ev_start"] = np.zeros((n, R, self.max_nodes), np.int64)
+            out["ev_end"] = np.zeros((n, R, self.max_nodes), np.int64)
+        p = _native.Points(n, _ptr(pts.algo, _native.PU8), _ptr(pts.topo_kind, _native.PU8),
+                           _ptr(pts.bw, _native.PF64), _ptr(pts.latency, _native.P64),
+                           _ptr(pts.rows, _native.P32), _ptr(pts.cols, _native.P32),
+                           _ptr(pts.peak_flops, _native.PF64), _ptr(pts.efficiency, _native.PF64),
+                           pts.compute_streams)
+        o = _native.Outputs(_ptr(out["status"], _native.P32), _ptr(out["rows"], _native.P64),
+                            _ptr(out.get("rank_stats"), _native.P64), _ptr(out.get("ev_start"), _native.P64),
+                            _ptr(out.get("ev_end"), _native.P64))
+        rc = _native.lib().fl_sweep_run(self._h, C.byref(p), C.byref(o))
+        if rc:
+            raise EngineError(f"fl_sweep_run: {_native.last_error()} (status {rc})")
+        return out
+
+    def run_device(self, dev: dict, stream_ptr: int, n: int, compute_streams: int = 1) -> int:
+        """Evaluate design points already resident in device memory.
+
+        ``dev`` maps fl_points / fl_outputs field names to raw device pointers
+        (ints, e.g. ``tensor.data_ptr()``).  Asynchronous on ``stream_ptr``.
+        Returns the number of kernels enqueued.
+        """
+        v = lambda k, t: C.cast(C.c_void_p(dev[k]), t) if dev.get(k) else None
+        p = _native.Points(n, v("algo", _native.PU8), v("topo_kind", _native.PU8), v("bw", _native.PF64),
+                           v("latency", _native.P64), v("rows", _native.P32), v("cols", _native.P32),
+                           v("peak_flops", _native.PF64), v("efficiency", _native.PF64), compute_streams)
+        o = _native.Outputs(v("status", _native.P32), v("rows", _native.P64), v("rank_stats", _native.P64),
+                            v("ev_start", _native.P64), v("ev_end", _native.P64))
+        launches = C.c_int32(0)
+        rc = _native.lib().fl_sweep_run_device(self._h, C.byref(p), C.byref(o), C.c_void_p(stream_ptr),
+                                               C.byref(launches))
+        if rc:
+            raise EngineError(f"fl_sweep_run_device: {_native.last_error()} (status {rc})")
+        return int(launches.value)
+
+
+# ------------------------------------------------------------ drop-in API
+
+
+def _single_point(topo, algo, compute_streams=1) -> DesignPoints:
+    return DesignPoints.from_topologies([topo], [algo], compute_streams=compute_streams)
+
+
+def simulate(graphs, topo, opts: Optional[SimOptions] = None, device: int = 0) -> SimReport:
+    """Drop-in ``trainsim.simulate`` (simulator.py:203) evaluated on the GPU."""
+    opts = opts or SimOptions()
+    if opts.compute_streams < 1 or opts.comm_streams < 1:
+        raise ValueError("stream counts must be >= 1")
+    gs = compile_graphs(graphs)
+    eng = Engine(gs, device)
+    try:
+        out = eng.run(_single_point(topo, opts.algo, opts.compute_streams), rank_stats=True,
+                      events=opts.record_events)
+    finally:
+        eng.close()
+    raise_for_status(int(out["status"][0]), "simulation stalled with work remaining"
+                     if out["status"][0] == 3 else "")
+    ranks = {}
+    for r in range(gs.n_ranks):
+        s = out["rank_stats"][0, r]
+        ranks[int(gs.rank_values[r])] = RankStats(*map(int, s))
+    rep = SimReport(makespan_ns=int(out["rows"][0, 0]), ranks=ranks)
+    if opts.record_events:
+        stream_of = {0: "host", 1: "compute", 2: "comm", 3: "comm", 4: "comm"}
+        evs = []
+        for r in range(gs.n_ranks):
+            st = gs.structs[gs.rank_struct[r]]
+            rv = int(gs.rank_values[r])
+            s0, e0 = out["ev_start"][0, r], out["ev_end"][0, r]
+            for k, node in enumerate(st.nodes):
+                evs.append(TraceEvent(rv, node.node_id, stream_of[int(st.kind[k])], node.op_name,
+                                      int(s0[k]), int(e0[k])))
+        evs.sort(key=lambda e: (e.start_ns, e.rank, e.node_id))
+        rep.events = evs
+    # ranks must be reported in the caller's order (dict insertion order of the reference)
+    rep.ranks = {int(g.rank): rep.ranks[int(g.rank)] for g in graphs}
+    return rep
+
+
+def critical_path(graphs, topo, algo=CollectiveAlgo.RING, device: int = 0) -> int:
+    """Drop-in ``trainsim.critical_path`` (simulator.py:400): contention-free bound."""
+    eng = Engine(graphs, device)
+    try:
+        out = eng.run(_single_point(topo, algo))
+    finally:
+        eng.close()
+    raise_for_status(int(out["status"][0]), "cyclic cross-rank wait in critical path"
+                     if out["status"][0] == 3 else "")
+    return int(out["rows"][0, 1])
+
+
+def simulate_batch(graphs, points: DesignPoints, device: int = 0, engine: Optional[Engine] = None) -> dict:
+    """One graph set x N design points -> sweep rows (cli.py:319-342, batched).
+
+    Returns ``{"status": int32[N], field: int64[N] for field in ROW_FIELDS}``;
+    rows whose status is not FL_OK carry zeros (see errors.raise_for_status).
+    """
+    eng = engine or Engine(graphs, device)
+    out = eng.run(points)
+    res = {"status": out["status"]}
+    for k, name in enumerate(ROW_FIELDS):
+        res[name] = out["rows"][:, k]
+    return res
+
+
+def cost_only(kind, size_bytes, group_n, algo, alpha, beta, rows, cols, flops=None, peak=None, eff=None):
+    """K1 on the device: alpha-beta times (collectives.py:251-293) and flops->ns
+    (traceio.py:184) for arrays of inputs.  Returns (ns, status, comp_ns)."""
+    c = lambda a, t: np.ascontiguousarray(np.asarray(a, dtype=t))
+    kind, size_bytes, group_n, algo = c(kind, np.uint8), c(size_bytes, np.int64), c(group_n, np.int64), c(algo, np.uint8)
+    alpha, beta, rows, cols = c(alpha, np.float64), c(beta, np.float64), c(rows, np.int32), c(cols, np.int32)
+    n = len(kind)
+    m = 0 if flops is None else len(flops)
+    flops = c(flops if flops is not None else [0], np.int64)
+    peak = c(peak if peak is not None else [1.0], np.float64)
+    eff = c(eff if eff is not None else [1.0], np.float64)
+    out, st, comp = np.zeros(max(n, 1), np.int64), np.zeros(max(n, 1), np.int32), np.zeros(max(m, 1), np.int64)
+    rc = _native.lib().fl_cost_only(n, _ptr(kind, _native.PU8), _ptr(size_bytes, _native.P64),
+                                    _ptr(group_n, _native.P64), _ptr(algo, _native.PU8),
+                                    _ptr(alpha, _native.PF64), _ptr(beta, _native.PF64),
+                                    _ptr(rows, _native.P32), _ptr(cols, _native.P32), _ptr(out, _native.P64),
+                                    _ptr(st, _native.P32), m, _ptr(flops, _native.P64), _ptr(peak, _native.PF64),
+                                    _ptr(eff, _native.PF64), _ptr(comp, _native.P64))
+    if rc:
+        raise EngineError(f"fl_cost_only: {_native.last_error()} (status {rc})")
+    return out[:n], st[:n], comp[:m]

@@ -1,0 +1,192 @@
+"""CUDA engine vs the reference's outputs (golden fixtures) and vs the oracle.
+
+All comparisons are bit-exact on integer nanoseconds and bytes.  Every call
+goes through libflint_b200.so's C-ABI (fl_graph_create / fl_sweep_run).
+"""
+
+import numpy as np
+import pytest
+
+from golden_io import corpus, decode_graphs, decode_topo, has_p2p, synth_fixtures
+from oracle import pyoracle as O
+from paper_2604_17550_b200 import engine as E
+from paper_2604_17550_b200 import synth
+from paper_2604_17550_b200.errors import EngineError
+from paper_2604_17550_b200.topology import Topology, parse_topology
+from randgraphs import random_graphs
+
+pytestmark = pytest.mark.gpu
+
+CASES = [c for c in corpus() if not has_p2p(c)]
+P2P_CASES = [c for c in corpus() if has_p2p(c)]
+
+
+def engine_result(graphs, topo, algo, cs, events):
+    res = {}
+    try:
+        rep = E.simulate(graphs, topo, E.SimOptions(algo=algo, compute_streams=cs, record_events=events))
+        doc = rep.to_doc()
+        res["sim"] = {"makespan_ns": doc["makespan_ns"], "ranks": doc["ranks"], "links": doc["links"]}
+        if events:
+            res["events"] = [[e["rank"], e["node_id"], e["start_ns"], e["end_ns"]] for e in doc["events"]]
+    except (ValueError, EngineError) as e:
+        if isinstance(e, EngineError):
+            raise
+        res["sim"] = {"error": "ValueError"}
+    except Exception as e:  # trainsim-compatible error classes
+        res["sim"] = {"error": type(e).__name__}
+    try:
+        res["cp"] = E.critical_path(graphs, topo, algo)
+    except EngineError:
+        raise
+    except Exception as e:
+        res["cp"] = {"error": type(e).__name__}
+    return res
+
+
+@pytest.mark.parametrize("idx", range(len(CASES)), ids=[c["name"] for c in CASES])
+def test_engine_matches_reference(idx):
+    case = CASES[idx]
+    got = engine_result(decode_graphs(case), decode_topo(case["topo"]), case["algo"],
+                        case["compute_streams"], "events" in case)
+    assert got["sim"] == case["sim"]
+    assert got["cp"] == case["cp"]
+    if "events" in case:
+        assert got["events"] == case["events"]
+
+
+def test_p2p_graphs_fail_loudly():
+    """Expanded comm mode is not in this build: the engine must refuse, not guess."""
+    with pytest.raises(EngineError):
+        E.simulate(decode_graphs(P2P_CASES[0]), decode_topo(P2P_CASES[0]["topo"]))
+
+
+def _family(preset, par, mode):
+    p = synth.parse_parallel(par)
+    p.fsdp_mode = synth.FsdpMode(mode)
+    return synth.synth_transformer(synth.PRESETS[preset], p, p.degree)
+
+
+@pytest.mark.parametrize("fx", synth_fixtures()["families"],
+                         ids=lambda f: f"{f['parallel']}-{f['fsdp_mode']}-{f['topo_spec']}-{f['algo']}")
+def test_engine_synth_families(fx):
+    gs = _family(fx["preset"], fx["parallel"], fx["fsdp_mode"])
+    got = engine_result(gs, parse_topology(fx["topo_spec"]), fx["algo"], 1, False)
+    assert got["sim"] == fx["sim"]
+    assert got["cp"] == fx["cp"]
+
+
+ROW_KEYS = E.ROW_FIELDS
+
+
+def _batch(gs, specs_algos):
+    topos = [parse_topology(s) for s, _ in specs_algos]
+    pts = E.DesignPoints.from_topologies(topos, [a for _, a in specs_algos])
+    return E.simulate_batch(gs, pts)
+
+
+def test_engine_sweep_rows_batched():
+    rows = synth_fixtures()["rows"]
+    groups = {}
+    for r in rows:
+        groups.setdefault((r["model"], r["parallel"]), []).append(r)
+    for (model, par), rs in groups.items():
+        p = synth.parse_parallel(par)
+        m = synth.GPT2_SMALL if model == "gpt2-small" else synth.PRESETS[model]
+        gs = synth.synth_transformer(m, p, p.degree)
+        out = _batch(gs, [(r["topo_spec"], r["algo"]) for r in rs])
+        assert (out["status"] == 0).all()
+        for i, r in enumerate(rs):
+            assert {k: int(out[k][i]) for k in ROW_KEYS} == {k: r[k] for k in ROW_KEYS}, (model, par, r["topo_spec"])
+
+
+def test_engine_c3_north_star_points():
+    """llama-8b-like fsdp:1024 -- rows measured with the reference (15 min each on CPU)."""
+    rows = synth_fixtures()["c3_r1024"]
+    gs = synth.synth_transformer(synth.PRESETS["llama-8b-like"], synth.ParallelConfig(synth.Strategy.FSDP, 1024), 1024)
+    out = _batch(gs, [(r["spec"], r["algo"]) for r in rows])
+    for i, r in enumerate(rows):
+        assert {k: int(out[k][i]) for k in ROW_KEYS} == {k: r[k] for k in ROW_KEYS}
+
+
+@pytest.mark.parametrize("seed", range(400))
+def test_engine_random_race_graphs_vs_oracle(seed):
+    gs, topo = random_graphs(seed)
+    for algo, cs in (("ring", 1), ("ring", 2), ("tree", 1), ("ring", 3)):
+        try:
+            ref = O.simulate(gs, topo, algo, cs, 1, record_events=True)
+            st, en = ref.pop("events")
+            ref.pop("links")
+            evs, k = [], 0
+            for g in gs:
+                for n in g.nodes:
+                    evs.append((int(st[k]), g.rank, n.node_id, int(en[k])))
+                    k += 1
+            want = (ref["makespan_ns"], ref["ranks"], sorted(evs))
+        except O.OracleError as e:
+            want = e.kind
+        try:
+            rep = E.simulate(gs, topo, E.SimOptions(algo=algo, compute_streams=cs))
+            got = (rep.makespan_ns, {k: vars(v) for k, v in rep.ranks.items()},
+                   sorted((e.start_ns, e.rank, e.node_id, e.end_ns) for e in rep.events))
+        except EngineError:
+            raise
+        except Exception as e:
+            got = "ValueError" if isinstance(e, ValueError) else type(e).__name__
+        assert got == want, (seed, algo, cs)
+        try:
+            want_cp = O.critical_path(gs, topo, algo)
+        except O.OracleError as e:
+            want_cp = e.kind
+        try:
+            got_cp = E.critical_path(gs, topo, algo)
+        except EngineError:
+            raise
+        except Exception as e:
+            got_cp = type(e).__name__
+        assert got_cp == want_cp, (seed, algo)
+
+
+def test_engine_c3_grid_sample_vs_oracle():
+    """A spread of BASELINE config-3 design points (switch ring + mesh-hier) at R=1024."""
+    gs = synth.synth_transformer(synth.PRESETS["llama-8b-like"], synth.ParallelConfig(synth.Strategy.FSDP, 1024), 1024)
+    flat = O.flatten(gs)
+    specs = [("switch:1024:10GB:100ns", "ring"), ("switch:1024:1800GB:20us", "ring"),
+             ("mesh:32x32:37GB:1us", "mesh-hier"), ("mesh:32x32:640GB:150ns", "mesh-hier")]
+    out = _batch(gs, specs)
+    for i, (spec, algo) in enumerate(specs):
+        want = O.sweep_row(gs, parse_topology(spec), algo, flat=flat)
+        assert {k: int(out[k][i]) for k in ROW_KEYS} == want, spec
+
+
+def test_cost_stage_matches_oracle_exhaustively():
+    """K1: alpha-beta forms and flops->ns on the device vs the C restatement."""
+    from paper_2604_17550_b200 import costs
+    rng = np.random.default_rng(7)
+    n = 20000
+    kind = rng.integers(0, 3, n).astype(np.uint8)
+    algo = rng.integers(0, 3, n).astype(np.uint8)
+    gn = rng.integers(1, 9000, n).astype(np.int64)
+    size = rng.integers(0, 1 << 40, n).astype(np.int64)
+    alpha = rng.integers(0, 20000, n).astype(np.float64)
+    beta = 1e9 / np.exp(rng.uniform(np.log(1e9), np.log(2e12), n))
+    rows = np.ones(n, np.int32)
+    cols = gn.astype(np.int32)
+    sq = rng.random(n) < 0.5
+    rows[sq] = 2
+    cols[sq] = (gn[sq] // 2).astype(np.int32)
+    gn[sq] = rows[sq] * cols[sq]
+    flops = rng.integers(0, 1 << 50, n).astype(np.int64)
+    peak = np.exp(rng.uniform(np.log(1e11), np.log(5e15), n))
+    eff = rng.uniform(0.05, 1.0, n)
+    got, st, comp = E.cost_only(kind, size, gn, algo, alpha, beta, rows, cols, flops, peak, eff)
+    names = {0: "ALL_REDUCE", 1: "ALL_GATHER", 2: "REDUCE_SCATTER"}
+    anames = {0: "ring", 1: "tree", 2: "mesh-hier"}
+    for i in range(n):
+        try:
+            want = O.analytical_time(names[int(kind[i])], int(size[i]), int(gn[i]), anames[int(algo[i])],
+                                     float(alpha[i]), float(beta[i]), int(rows[i]), int(cols[i]))
+            assert st[i] == 0 and got[i] == want, i
+        except O.OracleError:
+            assert st[i] == 4, i
+        assert comp[i] == O.duration_from_flops(int(flops[i]), float(peak[i]), float(eff[i])), i

@@ -43,6 +43,9 @@ struct fl_graph {
     unsigned char *scratch = nullptr;
     size_t scratch_bytes = 0;
     fl::DevScratch sc{};
+    // staging for fl_sweep_run (host-buffer entry point), grown on demand
+    unsigned char *stage = nullptr;
+    size_t stage_bytes = 0;
     int grid_cap = 0;
     int block = 32;
     size_t smem = 0;
@@ -250,6 +253,7 @@ int fl_graph_destroy(fl_graph *g) {
     cudaSetDevice(g->device);
     for (void *p : g->allocs) cudaFree(p);
     if (g->scratch) cudaFree(g->scratch);
+    if (g->stage) cudaFree(g->stage);
     delete g;
     return FL_OK;
 }
@@ -270,57 +274,56 @@ int fl_sweep_run(fl_graph *g, const fl_points *hp, fl_outputs *ho) {
     CK(cudaSetDevice(g->device));
     const size_t n = (size_t)hp->n_points;
     if (n == 0) return FL_OK;
-    std::vector<void *> tmp;
-    fl_points dp = *hp;
-    fl_outputs dout{};
-    int rc = FL_OK;
-    uint8_t *algo, *topo;
-    double *bw, *peak = nullptr, *eff = nullptr;
-    int64_t *lat;
-    int32_t *rows, *cols, *status;
-    int64_t *orows, *rs = nullptr, *es = nullptr, *ee = nullptr;
     const size_t R = (size_t)g->dg.R, MN = (size_t)g->dg.max_nodes;
-    if ((rc = to_dev(hp->algo, n, &algo, tmp)) || (rc = to_dev(hp->topo_kind, n, &topo, tmp)) ||
-        (rc = to_dev(hp->bw, n, &bw, tmp)) || (rc = to_dev(hp->latency, n, &lat, tmp)) ||
-        (rc = to_dev(hp->rows, n, &rows, tmp)) || (rc = to_dev(hp->cols, n, &cols, tmp)) ||
-        (rc = to_dev(hp->peak_flops, n, &peak, tmp)) || (rc = to_dev(hp->efficiency, n, &eff, tmp))) {
-        free_all(tmp);
-        return rc;
+    // one staging block: inputs then outputs, 256-byte aligned sub-buffers
+    struct Part { const void *src; size_t bytes; size_t off; };
+    Part in[8] = {{hp->algo, n, 0}, {hp->topo_kind, n, 0}, {hp->bw, 8 * n, 0}, {hp->latency, 8 * n, 0},
+                  {hp->rows, 4 * n, 0}, {hp->cols, 4 * n, 0},
+                  {hp->peak_flops, hp->peak_flops ? 8 * n : 0, 0}, {hp->efficiency, hp->efficiency ? 8 * n : 0, 0}};
+    size_t off = 0;
+    for (auto &p : in) { p.off = off; off = align_up(off + p.bytes, 256); }
+    const size_t o_status = off; off = align_up(off + 4 * n, 256);
+    const size_t o_rows = off; off = align_up(off + 48 * n, 256);
+    const size_t o_rs = off; off = align_up(off + (ho->rank_stats ? 40 * n * R : 0), 256);
+    const size_t o_es = off; off = align_up(off + (ho->ev_start ? 8 * n * R * MN : 0), 256);
+    const size_t o_ee = off; off = align_up(off + (ho->ev_start ? 8 * n * R * MN : 0), 256);
+    if (off > g->stage_bytes) {
+        if (g->stage) cudaFree(g->stage);
+        g->stage = nullptr;
+        g->stage_bytes = 0;
+        CK(cudaMalloc(&g->stage, off));
+        g->stage_bytes = off;
     }
-    auto dalloc = [&](size_t bytes, void **p) -> int {
-        cudaError_t e = cudaMalloc(p, bytes ? bytes : 1);
-        if (e != cudaSuccess) return fail(FL_ERR_CUDA, cudaGetErrorString(e));
-        tmp.push_back(*p);
-        return FL_OK;
-    };
-    if ((rc = dalloc(n * 4, (void **)&status)) || (rc = dalloc(n * 6 * 8, (void **)&orows)) ||
-        (ho->rank_stats && (rc = dalloc(n * R * 5 * 8, (void **)&rs))) ||
-        (ho->ev_start && (rc = dalloc(n * R * MN * 8, (void **)&es))) ||
-        (ho->ev_start && (rc = dalloc(n * R * MN * 8, (void **)&ee)))) {
-        free_all(tmp);
-        return rc;
+    unsigned char *S = g->stage;
+    for (auto &p : in)
+        if (p.bytes) CK(cudaMemcpyAsync(S + p.off, p.src, p.bytes, cudaMemcpyHostToDevice, 0));
+    fl_points dp = *hp;
+    dp.algo = S + in[0].off;
+    dp.topo_kind = S + in[1].off;
+    dp.bw = reinterpret_cast<const double *>(S + in[2].off);
+    dp.latency = reinterpret_cast<const int64_t *>(S + in[3].off);
+    dp.rows = reinterpret_cast<const int32_t *>(S + in[4].off);
+    dp.cols = reinterpret_cast<const int32_t *>(S + in[5].off);
+    dp.peak_flops = hp->peak_flops ? reinterpret_cast<const double *>(S + in[6].off) : nullptr;
+    dp.efficiency = hp->efficiency ? reinterpret_cast<const double *>(S + in[7].off) : nullptr;
+    fl_outputs dout{};
+    dout.status = reinterpret_cast<int32_t *>(S + o_status);
+    dout.rows = reinterpret_cast<int64_t *>(S + o_rows);
+    dout.rank_stats = ho->rank_stats ? reinterpret_cast<int64_t *>(S + o_rs) : nullptr;
+    dout.ev_start = ho->ev_start ? reinterpret_cast<int64_t *>(S + o_es) : nullptr;
+    dout.ev_end = ho->ev_start ? reinterpret_cast<int64_t *>(S + o_ee) : nullptr;
+    int rc = launch(g, &dp, &dout, 0);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(ho->status, dout.status, 4 * n, cudaMemcpyDeviceToHost, 0));
+    CK(cudaMemcpyAsync(ho->rows, dout.rows, 48 * n, cudaMemcpyDeviceToHost, 0));
+    if (ho->rank_stats) CK(cudaMemcpyAsync(ho->rank_stats, dout.rank_stats, 40 * n * R, cudaMemcpyDeviceToHost, 0));
+    if (ho->ev_start) {
+        CK(cudaMemcpyAsync(ho->ev_start, dout.ev_start, 8 * n * R * MN, cudaMemcpyDeviceToHost, 0));
+        CK(cudaMemcpyAsync(ho->ev_end, dout.ev_end, 8 * n * R * MN, cudaMemcpyDeviceToHost, 0));
     }
-    dp.algo = algo; dp.topo_kind = topo; dp.bw = bw; dp.latency = lat; dp.rows = rows; dp.cols = cols;
-    dp.peak_flops = peak; dp.efficiency = eff;
-    dout.status = status; dout.rows = orows; dout.rank_stats = rs; dout.ev_start = es; dout.ev_end = ee;
-    rc = launch(g, &dp, &dout, 0);
-    if (rc == FL_OK) {
-        cudaError_t e = cudaDeviceSynchronize();
-        if (e != cudaSuccess) rc = fail(FL_ERR_CUDA, std::string("engine kernel: ") + cudaGetErrorString(e));
-    }
-    if (rc == FL_OK) {
-        cudaMemcpy(ho->status, status, n * 4, cudaMemcpyDeviceToHost);
-        cudaMemcpy(ho->rows, orows, n * 6 * 8, cudaMemcpyDeviceToHost);
-        if (rs) cudaMemcpy(ho->rank_stats, rs, n * R * 5 * 8, cudaMemcpyDeviceToHost);
-        if (es) {
-            cudaMemcpy(ho->ev_start, es, n * R * MN * 8, cudaMemcpyDeviceToHost);
-            cudaMemcpy(ho->ev_end, ee, n * R * MN * 8, cudaMemcpyDeviceToHost);
-        }
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) rc = fail(FL_ERR_CUDA, cudaGetErrorString(e));
-    }
-    free_all(tmp);
-    return rc;
+    cudaError_t e = cudaStreamSynchronize(0);
+    if (e != cudaSuccess) return fail(FL_ERR_CUDA, std::string("engine kernel: ") + cudaGetErrorString(e));
+    return FL_OK;
 }
 
 int fl_cost_only(int32_t n, const uint8_t *kind, const int64_t *size_bytes, const int64_t *group_n,

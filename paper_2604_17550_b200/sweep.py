@@ -1,0 +1,203 @@
+"""Design-space sweeps: design-point grids, the batched sweep driver, GPU sharding.
+
+The reference's driver (``cmd_sweep``/``_sweep_row``, pkg/src/trainsim/cli.py:314-377)
+re-synthesizes the graph and runs ``simulate`` + ``critical_path`` for every
+design point, optionally across a process pool.  Here one graph structure per
+parallel token is compiled once and *all* its design points are evaluated by
+one engine launch; rows come back in the reference's product order
+(parallel x topology x algo, cli.py:352-353) with the same fields, the same
+``speedup_vs_base`` normalization and the same CSV bytes.
+
+Multi-GPU: design points are share-nothing.  Each process
+(one per GPU, torchrun) evaluates a contiguous slice of every graph group and
+the rows are collected with one ``all_gather_into_tensor`` (NCCL over NVLink on
+the GPU box; gloo in the CPU tests) -- the only collective of the path.
+"""
+
+from __future__ import annotations
+
+import csv
+import dataclasses
+import itertools
+import math
+import time
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .costs import CollectiveAlgo, load_profile
+from .engine import ROW_FIELDS, DesignPoints, Engine
+from .errors import (EngineError, FL_OK, TrainsimError, UnsupportedAlgoTopologyError,
+                     UnsupportedComboError, raise_for_status)
+from .synth import PRESETS, FsdpMode, parse_parallel, synth_transformer
+from .topology import parse_topology
+
+SWEEP_FIELDS = ["model", "parallel", "fsdp_mode", "algo", "comm_mode", "topology", "world_size",
+                "makespan_ns", "critical_path_ns", "compute_busy_ns", "comm_busy_ns",
+                "exposed_comm_ns", "peak_mem_bytes", "speedup_vs_base"]     # cli.py:314-316
+
+
+# ------------------------------------------------------------------ grids
+
+
+def log_grid(lo: float, hi: float, n: int) -> np.ndarray:
+    if n == 1:
+        return np.asarray([lo], np.float64)
+    return np.exp(np.linspace(math.log(lo), math.log(hi), n))
+
+
+def latency_grid(lo_ns: float, hi_ns: float, n: int) -> np.ndarray:
+    return np.rint(log_grid(lo_ns, hi_ns, n)).astype(np.int64)
+
+
+@dataclass
+class Workload:
+    """A named BASELINE configuration: one graph family x a design-point grid."""
+    name: str
+    model: str
+    parallel: str
+    points: DesignPoints
+    labels: list               # (topology kind, algo) per point, for reporting
+
+
+def _grid(pairs, bws, lats, rows_cols) -> DesignPoints:
+    algo, topo, bw, lat, rows, cols = [], [], [], [], [], []
+    amap = {"ring": 0, "tree": 1, "mesh-hier": 2}
+    for kind, a in pairs:
+        for b in bws:
+            for l in lats:
+                algo.append(amap[a]); topo.append(0 if kind == "switch" else 1)
+                bw.append(float(b)); lat.append(int(l))
+                r, c = rows_cols if kind == "mesh" else (0, 0)
+                rows.append(r); cols.append(c)
+    return DesignPoints(np.asarray(algo, np.uint8), np.asarray(topo, np.uint8), np.asarray(bw, np.float64),
+                        np.asarray(lat, np.int64), np.asarray(rows, np.int32), np.asarray(cols, np.int32))
+
+
+def c3_workload() -> Workload:
+    """BASELINE config 3: llama-8b-like fsdp:1024, 4096 points =
+    {switch:1024 + ring, mesh:32x32 + mesh-hier} x 64 bandwidths in
+    [10 GB/s, 1.8 TB/s] x 32 latencies in [100 ns, 20 us] (log-spaced)."""
+    pairs = [("switch", "ring"), ("mesh", "mesh-hier")]
+    pts = _grid(pairs, log_grid(10e9, 1.8e12, 64), latency_grid(100, 20000, 32), (32, 32))
+    return Workload("c3", "llama-8b-like", "fsdp:1024", pts, [p for p in pairs for _ in range(64 * 32)])
+
+
+def c2_workload() -> Workload:
+    """BASELINE config 2: GPT-2 small dp:64, 256 points = {ring, tree} x 16
+    bandwidths in [10 GB/s, 1.8 TB/s] x 8 latencies in [100 ns, 10 us]."""
+    pairs = [("switch", "ring"), ("switch", "tree")]
+    pts = _grid(pairs, log_grid(10e9, 1.8e12, 16), latency_grid(100, 10000, 8), (0, 0))
+    return Workload("c2", "gpt2-small", "dp:64", pts, [p for p in pairs for _ in range(16 * 8)])
+
+
+def workload_graphs(w: Workload):
+    from .synth import GPT2_SMALL
+    m = GPT2_SMALL if w.model == "gpt2-small" else PRESETS[w.model]
+    p = parse_parallel(w.parallel)
+    return synth_transformer(m, p, p.degree)
+
+
+# ------------------------------------------------------------- sharding
+
+
+def shard(n: int, world: int, rank: int) -> tuple:
+    """Contiguous, balanced slice [a, b) of n design points for one GPU."""
+    base, rem = divmod(n, world)
+    a = rank * base + min(rank, rem)
+    return a, a + base + (1 if rank < rem else 0)
+
+
+def gather_rows(local_status, local_rows, n_total: int, world: int, rank: int, device=None):
+    """All-gather per-slice results into full [n_total] arrays on every rank.
+
+    Slices are padded to the largest slice so one all_gather_into_tensor moves
+    everything (status is packed into column 6 of an int64 [n, 7] block)."""
+    import torch
+    import torch.distributed as dist
+    per = -(-n_total // world)
+    block = torch.full((per, 7), -1, dtype=torch.int64, device=device)
+    m = len(local_status)
+    if m:
+        block[:m, :6] = torch.as_tensor(np.asarray(local_rows), dtype=torch.int64, device=device)
+        block[:m, 6] = torch.as_tensor(np.asarray(local_status), dtype=torch.int64, device=device)
+    out = torch.empty((per * world, 7), dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(out, block)
+    out = out.cpu().numpy()
+    rows = np.zeros((n_total, 6), np.int64)
+    status = np.zeros(n_total, np.int32)
+    for r in range(world):
+        a, b = shard(n_total, world, r)
+        rows[a:b] = out[r * per: r * per + (b - a), :6]
+        status[a:b] = out[r * per: r * per + (b - a), 6]
+    return status, rows
+
+
+# --------------------------------------------------------- sweep driver
+
+
+def sweep_rows(preset: str, parallels, topos, algos, comm_mode: str = "analytical",
+               fsdp_mode: str = "delayed", profile_path: Optional[str] = None, device: int = 0) -> list:
+    """Rows of ``trainsim sweep`` (cli.py:345-358) computed on the GPU."""
+    if comm_mode != "analytical":
+        raise EngineError("expanded comm mode is not supported by this engine build")
+    if not parallels or not topos or not algos:
+        raise UnsupportedComboError("sweep lists must be non-empty")
+    profile = load_profile(profile_path) if profile_path else None
+    tasks = list(itertools.product(parallels, topos, algos))
+    by_par: dict = {}
+    for i, (par, topo, algo) in enumerate(tasks):
+        by_par.setdefault(par, []).append(i)
+    results = [None] * len(tasks)
+    first_error = None
+    for par, idxs in by_par.items():
+        m = PRESETS[preset]
+        p = dataclasses.replace(parse_parallel(par), fsdp_mode=FsdpMode(fsdp_mode))
+        try:
+            graphs = synth_transformer(m, p, p.degree, profile=profile)
+            topo_objs = [parse_topology(tasks[i][1]) for i in idxs]
+            algo_objs = [CollectiveAlgo(tasks[i][2]) for i in idxs]
+        except TrainsimError as e:
+            first_error = first_error or (idxs[0], e)
+            continue
+        eng = Engine(graphs, device)
+        try:
+            out = eng.run(DesignPoints.from_topologies(topo_objs, algo_objs))
+        finally:
+            eng.close()
+        for j, i in enumerate(idxs):
+            results[i] = (int(out["status"][j]), out["rows"][j], p.degree)
+    rows = []
+    for i, (par, topo, algo) in enumerate(tasks):
+        if first_error and first_error[0] == i:
+            raise first_error[1]
+        st, vals, deg = results[i] if results[i] is not None else (None, None, None)
+        if results[i] is None:
+            continue
+        if st != FL_OK:
+            raise_for_status(st, f"design point {par} {topo} {algo}")
+        row = {"model": preset, "parallel": par, "fsdp_mode": fsdp_mode, "algo": algo,
+               "comm_mode": comm_mode, "topology": topo, "world_size": deg}
+        row.update({k: int(v) for k, v in zip(ROW_FIELDS, vals)})
+        rows.append(row)
+    return rows
+
+
+def normalize(rows: list, normalize_to: Optional[str]) -> None:
+    """speedup_vs_base exactly as cli.py:360-369."""
+    base = {}
+    if normalize_to:
+        for row in rows:
+            if row["parallel"] == normalize_to:
+                base[(row["model"], row["topology"], row["algo"], row["comm_mode"])] = row["makespan_ns"]
+    for row in rows:
+        b = base.get((row["model"], row["topology"], row["algo"], row["comm_mode"]))
+        row["speedup_vs_base"] = f"{b / row['makespan_ns']:.6f}" if b and row["makespan_ns"] else "1.000000"
+
+
+def write_csv(rows: list, path: str) -> None:
+    with open(path, "w", newline="") as f:
+        w = csv.DictWriter(f, fieldnames=SWEEP_FIELDS, lineterminator="\n")
+        w.writeheader()
+        w.writerows(rows)

@@ -313,5 +313,24 @@ def main():
     print("synth cases:", len(synth), "rows:", len(rows), "c3:", len(c3))
 
 
+SWEEPS = {
+    "sweep_tiny_dp_tp.csv": ["--preset", "tiny", "--parallel", "dp:4,dp:8,tp:4",
+                             "--topo", "switch:8:25GB:2us,switch:8:100GB:500ns",
+                             "--algo", "ring,tree", "--normalize-to", "dp:4"],
+    "sweep_tiny_fsdp_mesh.csv": ["--preset", "tiny", "--parallel", "fsdp:8",
+                                 "--topo", "mesh:2x4:50GB:1us,mesh:2x4:400GB:100ns",
+                                 "--algo", "ring,mesh-hier", "--fsdp-mode", "none"],
+}
+
+
+def sweeps():
+    """Reference CLI sweeps (cli.py:345-377), kept byte-for-byte."""
+    from trainsim.cli import main as ref_main
+    for name, args in SWEEPS.items():
+        assert ref_main(["sweep", *args, "--out", str(OUT / name)]) == 0
+    (OUT / "sweeps.json").write_text(json.dumps(SWEEPS, indent=1) + "\n")
+
+
 if __name__ == "__main__":
     main()
+    sweeps()

@@ -190,3 +190,29 @@ def test_cost_stage_matches_oracle_exhaustively():
         except O.OracleError:
             assert st[i] == 4, i
         assert comp[i] == O.duration_from_flops(int(flops[i]), float(peak[i]), float(eff[i])), i
+
+
+@pytest.mark.parametrize("name", ["sweep_tiny_dp_tp.csv", "sweep_tiny_fsdp_mesh.csv"])
+def test_sweep_cli_csv_byte_identical(name, tmp_path):
+    """`python -m paper_2604_17550_b200 sweep` == reference `trainsim sweep` byte for byte."""
+    import json
+    from golden_io import GOLDEN
+    from paper_2604_17550_b200.cli import main
+    args = json.loads((GOLDEN / "sweeps.json").read_text())[name]
+    out = tmp_path / name
+    assert main(["sweep", *args, "--out", str(out)]) == 0
+    assert out.read_bytes() == (GOLDEN / name).read_bytes()
+
+
+def test_sweep_cli_exit_codes(tmp_path):
+    from paper_2604_17550_b200.cli import main
+    out = str(tmp_path / "x.csv")
+    # mesh-hier on a switch: UnsupportedAlgoTopologyError -> exit 1 (cli.py:395-397)
+    assert main(["sweep", "--preset", "tiny", "--parallel", "dp:4", "--topo", "switch:4:1GB:1us",
+                 "--algo", "mesh-hier", "--out", out]) == 1
+    # tree on FSDP gathers
+    assert main(["sweep", "--preset", "tiny", "--parallel", "fsdp:4", "--topo", "switch:4:1GB:1us",
+                 "--algo", "tree", "--out", out]) == 1
+    # bad topology spec: FormatError -> exit 2
+    assert main(["sweep", "--preset", "tiny", "--parallel", "dp:4", "--topo", "ring:4",
+                 "--algo", "ring", "--out", out]) == 2

@@ -255,7 +255,7 @@ def run_ours(args):
     d_status = torch.zeros(n, dtype=torch.int32, device=dev)
     d_rows = torch.zeros((n, 6), dtype=torch.int64, device=dev)
     ptrs = {k: t.data_ptr() for k, t in d_in.items()}
-    ptrs.update(status=d_status.data_ptr(), rows=d_rows.data_ptr())
+    ptrs.update(out_status=d_status.data_ptr(), out_rows=d_rows.data_ptr())
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)       # > L2 (126 MB)
     per = -(-n * world // world)

@@ -210,16 +210,20 @@ class Engine:
     def run_device(self, dev: dict, stream_ptr: int, n: int, compute_streams: int = 1) -> int:
         """Evaluate design points already resident in device memory.
 
-        ``dev`` maps fl_points / fl_outputs field names to raw device pointers
-        (ints, e.g. ``tensor.data_ptr()``).  Asynchronous on ``stream_ptr``.
+        ``dev`` maps fl_points field names, and fl_outputs field names prefixed
+        with ``out_`` (``out_status``, ``out_rows``, ...), to raw device
+        pointers (ints, e.g. ``tensor.data_ptr()``).  Asynchronous on ``stream_ptr``.
         Returns the number of kernels enqueued.
         """
         v = lambda k, t: C.cast(C.c_void_p(dev[k]), t) if dev.get(k) else None
         p = _native.Points(n, v("algo", _native.PU8), v("topo_kind", _native.PU8), v("bw", _native.PF64),
                            v("latency", _native.P64), v("rows", _native.P32), v("cols", _native.P32),
                            v("peak_flops", _native.PF64), v("efficiency", _native.PF64), compute_streams)
-        o = _native.Outputs(v("status", _native.P32), v("rows", _native.P64), v("rank_stats", _native.P64),
-                            v("ev_start", _native.P64), v("ev_end", _native.P64))
+        o = _native.Outputs(v("out_status", _native.P32), v("out_rows", _native.P64),
+                            v("out_rank_stats", _native.P64), v("out_ev_start", _native.P64),
+                            v("out_ev_end", _native.P64))
+        if not dev.get("out_status") or not dev.get("out_rows"):
+            raise EngineError("run_device needs out_status and out_rows device buffers")
         launches = C.c_int32(0)
         rc = _native.lib().fl_sweep_run_device(self._h, C.byref(p), C.byref(o), C.c_void_p(stream_ptr),
                                                C.byref(launches))

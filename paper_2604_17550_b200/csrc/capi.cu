@@ -124,7 +124,6 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     UP(succ_off, total + 1);
     UP(succ_idx, ne_succ);
     UP(free_off, total + 1);
-    UP(free_tens, ne_free);
     UP(init_list, ne_init);
     UP(tens_bytes, total_t);
     UP(tens_cons_off, total_t + 1);
@@ -142,24 +141,128 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
         if (rc) return rc;
     }
 
-    // launch geometry: one thread per rank, one CTA per design point
-    g->block = (R + 31) / 32 * 32;
-    g->smem = sizeof(uint64_t) * 64 + sizeof(int64_t) * 64 + 64 + (size_t)R * 12 + 64;
-    int sms = 0, occ = 0;
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    CK(fl::sweep_occupancy(g->block, g->smem, &occ));
-    if (occ < 1) occ = 1;
-    g->grid_cap = sms * occ;
+    // packed node records and tensor consumer ranges (engine.cu node record layout)
+    {
+        std::vector<uint4> rec(3 * (size_t)(total > 0 ? total : 1));
+        std::vector<int32_t> mfree;
+        mfree.reserve((size_t)ne_free + 1);
+        // static hosts: zero in-degree, zero duration, no tensors (all start and end at t=0)
+        std::vector<char> is_static((size_t)total + 1, 0);
+        std::vector<int32_t> s_nstatic(S, 0), s_fold(S, 1), trig_off(S + 1, 0), static_off(S + 1, 0), static_list;
+        std::vector<int4> trig;
+        for (int s = 0; s < S; s++) {
+            for (int i = d->s_node_off[s]; i < d->s_node_off[s + 1]; i++) {
+                const bool zero_in = d->pred_off[i + 1] == d->pred_off[i] && !(d->node_flags[i] & 1);
+                if (d->node_kind[i] == FL_HOST && zero_in && d->node_dur[i] == 0) {
+                    is_static[i] = 1;
+                    s_nstatic[s]++;
+                    static_list.push_back(i - d->s_node_off[s]);
+                    if (d->free_off[i + 1] != d->free_off[i] || d->node_alloc[i] != 0) s_fold[s] = 0;
+                }
+            }
+            static_off[s + 1] = (int32_t)static_list.size();
+        }
+        int s_of = 0;
+        for (int i = 0; i < total; i++) {
+            while (s_of + 1 < S && i >= d->s_node_off[s_of + 1]) s_of++;
+            const int nb = d->s_node_off[s_of], tb = d->s_tens_off[s_of];
+            const int indeg = d->pred_off[i + 1] - d->pred_off[i];
+            if (indeg > 1023) return fail(FL_ERR_CAPACITY, "node in-degree > 1023");
+            int indeg_nh = 0;
+            for (int q = d->pred_off[i]; q < d->pred_off[i + 1]; q++) indeg_nh += !is_static[nb + d->pred_idx[q]];
+            uint64_t ufree = 0;
+            const uint32_t m0 = (uint32_t)mfree.size();
+            for (int q = d->free_off[i]; q < d->free_off[i + 1]; q++) {
+                const int t = d->free_tens[q];
+                const int nc = d->tens_cons_off[tb + t + 1] - d->tens_cons_off[tb + t];
+                if (nc == 1) ufree += (uint64_t)d->tens_bytes[tb + t];   // sole consumer: freed when it completes
+                else mfree.push_back(t);
+            }
+            const uint64_t alloc = (uint64_t)d->node_alloc[i];
+            const unsigned meta = (unsigned)d->node_kind[i] | ((unsigned)(d->node_flags[i] & 1) << 4) |
+                                  ((unsigned)is_static[i] << 5) | ((unsigned)indeg_nh << 6) | ((unsigned)indeg << 16);
+            rec[3 * i] = make_uint4((unsigned)d->succ_off[i], (unsigned)d->succ_off[i + 1], m0, (uint32_t)mfree.size());
+            rec[3 * i + 1] = make_uint4(meta, (unsigned)(d->node_coll_ord[i] < 0 ? 0 : d->node_coll_ord[i]),
+                                        (uint32_t)alloc, (uint32_t)(alloc >> 32));
+            rec[3 * i + 2] = make_uint4((uint32_t)ufree, (uint32_t)(ufree >> 32), 0u, 0u);
+        }
+        // nodes whose every dependency is a static host become ready during the t=0 pops of
+        // those hosts, right after the highest-id one (the trigger); listed by (trigger, position)
+        for (int s = 0; s < S; s++) {
+            const int nb = d->s_node_off[s];
+            for (int h = nb; h < d->s_node_off[s + 1]; h++) {
+                if (!is_static[h]) continue;
+                int seq = 0;
+                for (int q = d->succ_off[h]; q < d->succ_off[h + 1]; q++, seq++) {
+                    const int v = nb + d->succ_idx[q];
+                    if (d->node_flags[v] & 1) continue;
+                    bool host_only = true;
+                    int last = -1;
+                    for (int u = d->pred_off[v]; u < d->pred_off[v + 1]; u++) {
+                        host_only &= is_static[nb + d->pred_idx[u]] != 0;
+                        last = d->pred_idx[u] > last ? d->pred_idx[u] : last;
+                    }
+                    if (host_only && last == h - nb) trig.push_back(make_int4(h - nb, v - nb, seq, 0));
+                }
+            }
+            trig_off[s + 1] = (int32_t)trig.size();
+        }
+        int fold_ok = 1;
+        for (int s = 0; s < S; s++) fold_ok &= s_fold[s];
+        dg.fold_ok = fold_ok;
+        std::vector<int2> tc((size_t)(total_t > 0 ? total_t : 1));
+        for (int i = 0; i < total_t; i++) tc[i] = make_int2(d->tens_cons_off[i], d->tens_cons_off[i + 1]);
+        if (mfree.empty()) mfree.push_back(0);
+        if (trig.empty()) trig.push_back(make_int4(0, 0, 0, 0));
+        if (static_list.empty()) static_list.push_back(0);
+        int rc = upload(g, rec.data(), rec.size(), &dg.node_rec);
+        if (!rc) rc = upload(g, tc.data(), tc.size(), &dg.tens_rng);
+        if (!rc) rc = upload(g, mfree.data(), mfree.size(), &dg.free_tens);
+        if (!rc) rc = upload(g, s_nstatic.data(), s_nstatic.size(), &dg.s_nstatic);
+        if (!rc) rc = upload(g, trig_off.data(), trig_off.size(), &dg.trig_off);
+        if (!rc) rc = upload(g, trig.data(), trig.size(), &dg.trig);
+        if (!rc) rc = upload(g, static_off.data(), static_off.size(), &dg.static_off);
+        if (!rc) rc = upload(g, static_list.data(), static_list.size(), &dg.static_list);
+        if (rc) return rc;
+    }
 
-    // per-CTA scratch layout
+    // launch geometry: one thread per rank, one CTA per design point at a time
+    g->block = (R + 31) / 32 * 32;
+    int sms = 0, optin = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+
+    // per-CTA scratch (global) layout
     fl::DevScratch &sc = g->sc;
+    const size_t inst_bytes = (size_t)(d->n_inst > 0 ? d->n_inst : 1) * (5 * 8 + 2 * 4);
+    const size_t dur_bytes = (size_t)(total > 0 ? total : 1) * 8;
+    const size_t done_bytes = (size_t)dg.max_words * R * 8;
     size_t off = 0;
-    sc.off_bits = off; off = align_up(off + 4 * (size_t)dg.max_words * R * 8, 256);
+    sc.off_bits = off; off = align_up(off + 4 * done_bytes, 256);
     sc.off_cp = off;   off = align_up(off + (size_t)dg.max_nodes * R * 8, 256);
     sc.off_ring = off; off = align_up(off + 2 * (size_t)dg.coll_stride * R * 4, 256);
-    sc.off_dur = off;  off = align_up(off + (size_t)(total > 0 ? total : 1) * 8, 256);
-    sc.off_inst = off; off = align_up(off + (size_t)(d->n_inst > 0 ? d->n_inst : 1) * (5 * 8 + 2 * 4), 256);
+    sc.off_dur = off;  off = align_up(off + dur_bytes, 256);
+    sc.off_inst = off; off = align_up(off + inst_bytes, 256);
     sc.slot_bytes = off;
+
+    // shared memory: header | comm_end, stats, ring tails | [instances] | [durations] | [done bitmap]
+    size_t sm = fl::sweep_shared_header_bytes();
+    sc.sm_off_dyn = (unsigned)sm;
+    sm = align_up(sm + (size_t)R * (8 + 6 * 8 + 4), 16);
+    const size_t budget = (size_t)optin;
+    sc.inst_in_smem = sm + inst_bytes <= budget;
+    if (sc.inst_in_smem) { sc.sm_off_inst = (unsigned)sm; sm = align_up(sm + inst_bytes, 16); }
+    sc.dur_in_smem = sm + dur_bytes <= budget;
+    if (sc.dur_in_smem) { sc.sm_off_dur = (unsigned)sm; sm = align_up(sm + dur_bytes, 16); }
+    sc.done_in_smem = sm + done_bytes <= budget;
+    if (sc.done_in_smem) { sc.sm_off_done = (unsigned)sm; sm = align_up(sm + done_bytes, 16); }
+    if (sm > budget) return fail(FL_ERR_CAPACITY, "per-rank state exceeds shared memory");
+    g->smem = sm;
+    CK(fl::sweep_set_smem(sm));
+    int occ = 0;
+    CK(fl::sweep_occupancy(g->block, g->smem, &occ));
+    if (occ < 1) return fail(FL_ERR_CAPACITY, "engine kernel cannot be resident with this shared-memory footprint");
+    g->grid_cap = sms * occ;
     return FL_OK;
 }
 

@@ -133,18 +133,25 @@ struct Shared {
     int flag;
 };
 
-__device__ __forceinline__ uint64_t block_min_u64(uint64_t v, Shared &sh, int &par) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+// Warp min of keys (time << 14 | rank).  Ranks step in lockstep most of the
+// time: when every lane holds the same time, lane 0 (lowest rank) has the min.
+__device__ __forceinline__ uint64_t warp_min_key(uint64_t v) {
+    const uint64_t v0 = __shfl_sync(FULL, v, 0);
+    if (__all_sync(FULL, (v >> 14) == (v0 >> 14))) return v0;
 #pragma unroll
     for (int o = 16; o; o >>= 1) { uint64_t w = __shfl_xor_sync(FULL, v, o); v = w < v ? w : v; }
+    return v;
+}
+
+__device__ __forceinline__ uint64_t block_min_u64(uint64_t v, Shared &sh, int &par) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = warp_min_key(v);
     uint64_t *b = sh.red[par];
     par ^= 1;
     if (lane == 0) b[warp] = v;
     __syncthreads();
-    v = lane < nw ? b[lane] : KINF;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) { uint64_t w = __shfl_xor_sync(FULL, v, o); v = w < v ? w : v; }
-    return v;
+    v = lane < nw ? b[lane] : b[0];
+    return warp_min_key(v);
 }
 
 __device__ __forceinline__ int64_t block_max_i64(int64_t v, Shared &sh, int &par) {
@@ -163,288 +170,369 @@ __device__ __forceinline__ int64_t block_max_i64(int64_t v, Shared &sh, int &par
 
 // ---------------------------------------------------------- rank state
 
-// Bitmaps are stored word-major, rank-minor ([word][rank]) so the 32 ranks of
-// a warp that step in lockstep touch one contiguous 256-byte segment.
-struct Bits {
-    uint64_t *p;
+// Node record built by capi.cu, three 16-byte words per node so that one
+// broadcast load per word serves the 32 ranks of a warp visiting the node:
+//   a = {succ_off, succ_end, mfree_off, mfree_end}  dependents; tensors with >1 consumer
+//   b = {meta, coll_ord, alloc_lo, alloc_hi}        bytes allocated when the node starts
+//   c = {ufree_lo, ufree_hi, -, -}                  bytes of tensors it is the only consumer of
+//   meta bits: 0-3 kind, 4 never-ready (waits on a missing node), 8-19 in-degree
+//   meta bits: 0-3 kind, 4 never-ready, 5 static host, 6-15 in-degree from
+//   non-static nodes, 16-25 in-degree
+__device__ __forceinline__ int rec_kind(const uint4 &b) { return (int)(b.x & 15u); }
+__device__ __forceinline__ bool rec_never(const uint4 &b) { return (b.x >> 4) & 1u; }
+__device__ __forceinline__ bool rec_static(const uint4 &b) { return (b.x >> 5) & 1u; }
+__device__ __forceinline__ uint64_t rec_indeg(const uint4 &b, bool fold) { return (b.x >> (fold ? 6 : 16)) & 0x3ffu; }
+__device__ __forceinline__ int64_t rec_u64(uint32_t lo, uint32_t hi) { return (int64_t)(((uint64_t)hi << 32) | lo); }
+__device__ __forceinline__ uint4 rec_a(const DevGraph &g, int gn) { return g.node_rec[3 * gn]; }
+__device__ __forceinline__ uint4 rec_b(const DevGraph &g, int gn) { return g.node_rec[3 * gn + 1]; }
+__device__ __forceinline__ uint4 rec_c(const DevGraph &g, int gn) { return g.node_rec[3 * gn + 2]; }
+
+// Per-(node, rank) accumulator word, one int64 in global memory ([node][rank]):
+//   bits 58-63  epoch of the design point that wrote it (stale words read as empty)
+//   bits 48-57  dependencies still outstanding (in-degree <= 1023)
+//   bits  0-47  max critical-path finish over the completed dependencies; once the
+//               node is dispatched, its own critical-path finish
+// so a dependency's completion is one read-modify-write that both counts it
+// down (simulator.py:337-340) and relaxes the contention-free longest path
+// (simulator.py:449-453) -- no per-rank in-degree table to initialize.
+constexpr uint64_t VAL48 = (1ull << 48) - 1;
+
+enum { ST_COMP = 0, ST_COMM, ST_OVL, ST_CUR, ST_PEAK, ST_FIN, ST_N };
+
+// Per-CTA (block-uniform) state pointers.  Bitmaps are word-major,
+// rank-minor ([word][rank]) so a warp's 32 ranks touch one 256-byte segment;
+// `done` lives in shared memory when it fits.
+struct Ctx {
     int R;
-    __device__ __forceinline__ uint64_t &w(int word, int r) const { return p[(size_t)word * R + r]; }
+    uint64_t *done, *rdyc, *rdyh, *due;
+    int64_t *cp;                    // [max_nodes][R]
+    int32_t *ring_inst, *ring_node; // [coll_stride][R] per-rank comm FIFO
+    int64_t *dur;                   // [total_nodes] this design point's durations
+    int64_t *inst_dur, *inst_s, *inst_e, *inst_cpmax;
+    unsigned long long *inst_ckey;
+    int32_t *inst_wait, *complist;
+    int64_t *comm_end;              // shared [R]
+    int32_t *ring_tail;             // shared [R]
+    int *ncomp;                     // shared
+    int64_t *stat;                  // shared [ST_N][R]
+};
+
+// Per-thread rank identity: element w of rank r in a [w][R] array is at w * R + r.
+struct Lane {
+    int r, nb, tb;
+};
+
+// A node set with its minimum cached in a register and the rest in a global
+// bitmap (+ register summary of non-empty words).  Invariant: head < every
+// bitmap member, head < 0 iff the set is empty.  The due / ready sets rarely
+// hold more than one node, so most inserts and pops never touch memory.
+struct MinSet {
+    int head;
+    uint64_t sum;
 };
 
 template <int K>
 struct Rank {
-    int r, nb, N, tb;            // rank, global node base, node count, global tensor base
-    uint64_t due_s, rc_s, rh_s;  // non-empty-word summaries of the due / ready-comp / ready-host sets
+    MinSet due, rc, rh;             // due events at t / ready compute nodes / ready host nodes
     int64_t host_slot, host_e;
-    int host_n;
     int64_t slot[K], occ_e[K];
+    int64_t head_s, head_e;         // comm-FIFO head (valid iff ring_head < ring_seen)
+    int64_t alloc_t, free_t, cpmax;
+    int host_n;
     int occ_n[K];
-    int ring_head, ring_acur;
-    int64_t comp_busy, comm_busy, overlap, finish, cur, peak, alloc_t, free_t, cpmax;
+    int head_node, head_alloc;
+    int ring_head, ring_seen;
     int done_cnt, pop_seq;
 };
 
-struct Cfg {                      // per design point, uniform over the CTA
-    int64_t *dur;                 // per node duration for this point
-    int serial;
+struct Step {                       // block-uniform per-step context
     uint64_t step;
+    uint64_t epoch;                 // design-point epoch << 58 (accumulator tag)
     int init;
+    int fold;                       // static hosts folded (see "t = 0 host pops")
 };
 
-__device__ __forceinline__ void bm_insert(const Bits &b, uint64_t &sum, int r, int idx) {
-    int w = idx >> 6;
-    b.w(w, r) |= 1ull << (idx & 63);
+__device__ __forceinline__ void bm_set(uint64_t *b, int R, int r, uint64_t &sum, int idx) {
+    const int w = idx >> 6;
+    b[w * R + r] |= 1ull << (idx & 63);
     sum |= 1ull << w;
 }
 
-__device__ __forceinline__ int bm_pop(const Bits &b, uint64_t &sum, int r) {
-    int w = __ffsll((long long)sum) - 1;
-    uint64_t word = b.w(w, r);
-    int bit = __ffsll((long long)word) - 1;
+__device__ __forceinline__ int bm_pop(uint64_t *b, int R, int r, uint64_t &sum) {
+    const int w = __ffsll((long long)sum) - 1;
+    uint64_t *p = b + (w * R + r);
+    uint64_t word = *p;
+    const int bit = __ffsll((long long)word) - 1;
     word &= word - 1;
-    b.w(w, r) = word;
+    *p = word;
     if (!word) sum &= sum - 1;
     return (w << 6) | bit;
 }
 
-__device__ __forceinline__ int bm_peek(const Bits &b, uint64_t sum, int r) {
-    int w = __ffsll((long long)sum) - 1;
-    return (w << 6) | (__ffsll((long long)b.w(w, r)) - 1);
+__device__ __forceinline__ int bm_peek(const uint64_t *b, int R, int r, uint64_t sum) {
+    const int w = __ffsll((long long)sum) - 1;
+    return (w << 6) | (__ffsll((long long)b[w * R + r]) - 1);
 }
 
-__device__ __forceinline__ bool bm_test(const Bits &b, int r, int idx) {
-    return (b.w(idx >> 6, r) >> (idx & 63)) & 1ull;
+__device__ __forceinline__ bool bm_has(const uint64_t *b, int R, int r, int idx) {
+    return (b[(idx >> 6) * R + r] >> (idx & 63)) & 1ull;
 }
 
-struct Ctx {
-    DevGraph g;
-    DevPoints p;
-    DevOut o;
-    Bits done, rdyc, rdyh, due;
-    int64_t *cp;                  // [max_nodes][R] critical-path finish per (node, rank)
-    int32_t *ring_inst, *ring_node;  // [coll_stride][R] per-rank comm FIFO
-    int64_t *dur;                 // [total_nodes]
-    int64_t *inst_dur, *inst_s, *inst_e, *inst_cpmax;
-    unsigned long long *inst_ckey;
-    int32_t *inst_wait, *complist;
-    int64_t *comm_end;            // shared: [R]
-    int32_t *ring_tail;           // shared: [R]
-    int *ncomp;                   // shared: instances completed in this step
-};
-
-template <int K>
-__device__ __forceinline__ void record(const Ctx &c, int cfg, const Rank<K> &s, int x, int64_t st, int64_t en) {
-    if (c.o.ev_start) {
-        size_t at = ((size_t)cfg * c.g.R + s.r) * c.g.max_nodes + x;
-        c.o.ev_start[at] = st;
-        c.o.ev_end[at] = en;
+__device__ __forceinline__ void ms_insert(MinSet &m, uint64_t *b, int R, int r, int idx) {
+    if (m.head < 0) {
+        m.head = idx;
+    } else if (idx < m.head) {
+        bm_set(b, R, r, m.sum, m.head);
+        m.head = idx;
+    } else {
+        bm_set(b, R, r, m.sum, idx);
     }
 }
 
-// One rank's start phase at time t (simulator.py:282-297 for this rank).
+__device__ __forceinline__ int ms_pop(MinSet &m, uint64_t *b, int R, int r) {
+    const int x = m.head;
+    m.head = m.sum ? bm_pop(b, R, r, m.sum) : -1;
+    return x;
+}
+
+__device__ __forceinline__ void record(const DevGraph &g, const DevOut &o, int cfg, int r, int x, int64_t st,
+                                       int64_t en) {
+    if (o.ev_start) {
+        size_t at = ((size_t)cfg * g.R + r) * g.max_nodes + x;
+        o.ev_start[at] = st;
+        o.ev_end[at] = en;
+    }
+}
+
+// One rank's start phase at time t (simulator.py:282-297 restricted to this rank).
 template <int K>
-__device__ void start_phase(const Ctx &c, const Cfg &f, Rank<K> &s, int64_t t, int cfg) {
-    const int r = s.r;
-    while (s.rh_s && s.host_slot <= t) {
-        int h = bm_pop(c.rdyh, s.rh_s, r);
-        int64_t e = t + f.dur[s.nb + h];
+__device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, const Ctx &c, const Lane &L,
+                                            Rank<K> &s, int64_t t, int cfg) {
+    const int R = c.R;
+    while (s.rh.head >= 0 && s.host_slot <= t) {
+        const int h = ms_pop(s.rh, c.rdyh, R, L.r);
+        const int64_t e = t + c.dur[L.nb + h];
         s.host_slot = e;
-        s.alloc_t += c.g.node_alloc[s.nb + h];
-        record(c, cfg, s, h, t, e);
-        if (e == t) bm_insert(c.due, s.due_s, r, h);
+        { const uint4 hb = rec_b(g, L.nb + h); s.alloc_t += rec_u64(hb.z, hb.w); }
+        record(g, o, cfg, L.r, h, t, e);
+        if (e == t) ms_insert(s.due, c.due, R, L.r, h);
         else { s.host_e = e; s.host_n = h; }
     }
-    while (s.rc_s) {
+    while (s.rc.head >= 0) {
         int k = 0;
 #pragma unroll
         for (int q = 1; q < K; q++) if (s.slot[q] < s.slot[k]) k = q;
-        if (s.slot[k] > t) break;
-        int x = bm_pop(c.rdyc, s.rc_s, r);
-        int64_t e = t + f.dur[s.nb + x];
-        s.alloc_t += c.g.node_alloc[s.nb + x];
-        record(c, cfg, s, x, t, e);
+        int64_t sk = s.slot[0];
+#pragma unroll
+        for (int q = 1; q < K; q++) if (q == k) sk = s.slot[q];
+        if (sk > t) break;
+        const int x = ms_pop(s.rc, c.rdyc, R, L.r);
+        const int64_t e = t + c.dur[L.nb + x];
+        { const uint4 xb = rec_b(g, L.nb + x); s.alloc_t += rec_u64(xb.z, xb.w); }
+        record(g, o, cfg, L.r, x, t, e);
 #pragma unroll
         for (int q = 0; q < K; q++) {
             if (q == k) {
                 s.slot[q] = e;
-                if (e == t) bm_insert(c.due, s.due_s, r, x);
+                if (e == t) ms_insert(s.due, c.due, R, L.r, x);
                 else { s.occ_e[q] = e; s.occ_n[q] = x; }
             }
         }
     }
 }
 
-// A node whose every dependency completed (simulator.py:247-268).
+// A node whose every dependency has completed (simulator.py:247-268); `cps`
+// is its contention-free critical-path start (simulator.py:449).
 template <int K>
-__device__ void dispatch(const Ctx &c, const Cfg &f, Rank<K> &s, int d, int seq) {
-    const int r = s.r, R = c.g.R;
-    const int gd = s.nb + d;
-    int64_t cps = 0;
-    for (int q = c.g.pred_off[gd]; q < c.g.pred_off[gd + 1]; q++) {
-        int64_t v = c.cp[(size_t)c.g.pred_idx[q] * R + r];
-        cps = v > cps ? v : cps;
-    }
-    int kind = c.g.node_kind[gd];
+__device__ __forceinline__ void dispatch(const DevGraph &g, const Ctx &c, const Lane &L, Rank<K> &s,
+                                         const Step &f, int d, const uint4 &rb, int64_t cps, int seq) {
+    const int R = c.R;
+    const int kind = rec_kind(rb);
     if (kind == FL_COLL) {
-        int i = c.g.rank_coll_inst[(size_t)r * c.g.coll_stride + c.g.node_coll_ord[gd]];
+        const int i = g.rank_coll_inst[L.r * g.coll_stride + (int)rb.y];
         atomicMax((unsigned long long *)&c.inst_cpmax[i], (unsigned long long)cps);
         if (!f.init) {
-            unsigned long long key = (f.step << 39) | ((unsigned long long)r << 25) |
-                                     ((unsigned long long)s.pop_seq << 12) | (unsigned long long)seq;
+            const unsigned long long key = (f.step << 39) | ((unsigned long long)L.r << 25) |
+                                           ((unsigned long long)s.pop_seq << 12) | (unsigned long long)seq;
             atomicMax(&c.inst_ckey[i], key);
         }
         if (atomicSub(&c.inst_wait[i], 1) == 1) c.complist[atomicAdd(c.ncomp, 1)] = i;
         return;
     }
-    int64_t fin = cps + f.dur[gd];
-    c.cp[(size_t)d * R + r] = fin;
+    const int64_t fin = cps + c.dur[L.nb + d];
+    c.cp[d * R + L.r] = (int64_t)(f.epoch | (uint64_t)fin);
     s.cpmax = fin > s.cpmax ? fin : s.cpmax;
-    if (kind == FL_COMP) bm_insert(c.rdyc, s.rc_s, r, d);
-    else bm_insert(c.rdyh, s.rh_s, r, d);
+    if (kind == FL_COMP) ms_insert(s.rc, c.rdyc, R, L.r, d);
+    else ms_insert(s.rh, c.rdyh, R, L.r, d);
 }
 
-// Pop one completion event (simulator.py:335-340) plus its tensor frees.
+// Pop one completion event (simulator.py:335-340) and free tensors whose last
+// consumer it was (simulator.py:384-388).
 template <int K>
-__device__ void pop_event(const Ctx &c, const Cfg &f, Rank<K> &s, int x, int64_t t) {
-    const int r = s.r;
-    const int gx = s.nb + x;
-    c.done.w(x >> 6, r) |= 1ull << (x & 63);
+__device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const Lane &L, Rank<K> &s,
+                                          const Step &f, int x, int64_t t) {
+    const int R = c.R;
+    const uint4 xa = rec_a(g, L.nb + x), xc = rec_c(g, L.nb + x);
+    c.done[(x >> 6) * R + L.r] |= 1ull << (x & 63);
     s.done_cnt++;
     s.pop_seq++;
-    s.finish = t;
-    // a tensor is freed when its last consumer completes (simulator.py:384-388)
-    for (int q = c.g.free_off[gx]; q < c.g.free_off[gx + 1]; q++) {
-        int tt = s.tb + c.g.free_tens[q];
+    c.stat[ST_FIN * R + L.r] = t;
+    s.free_t += rec_u64(xc.x, xc.y);
+    for (uint32_t q = xa.z; q < xa.w; q++) {
+        const int tt = L.tb + g.free_tens[q];
+        const int2 cr = g.tens_rng[tt];
         bool all = true;
-        for (int u = c.g.tens_cons_off[tt]; u < c.g.tens_cons_off[tt + 1] && all; u++)
-            all = bm_test(c.done, r, c.g.tens_cons[u]);
-        if (all) s.free_t += c.g.tens_bytes[tt];
+        for (int u = cr.x; u < cr.y && all; u++) all = bm_has(c.done, R, L.r, g.tens_cons[u]);
+        if (all) s.free_t += g.tens_bytes[tt];
     }
+    const uint64_t fx = (uint64_t)c.cp[x * R + L.r] & VAL48;    // this node's critical-path finish
     int seq = 0;
-    for (int q = c.g.succ_off[gx]; q < c.g.succ_off[gx + 1]; q++, seq++) {
-        int d = c.g.succ_idx[q];
-        int gd = s.nb + d;
-        if (c.g.node_flags[gd] & 1) continue;
-        bool ready = true;
-        for (int u = c.g.pred_off[gd]; u < c.g.pred_off[gd + 1] && ready; u++)
-            ready = bm_test(c.done, r, c.g.pred_idx[u]);
-        if (ready) dispatch(c, f, s, d, seq);
+    for (uint32_t q = xa.x; q < xa.y; q++, seq++) {
+        const int d = g.succ_idx[q];
+        const uint4 db = rec_b(g, L.nb + d);
+        if (rec_never(db)) continue;
+        int64_t *slot = c.cp + (d * R + L.r);
+        uint64_t a = (uint64_t)*slot;
+        if ((a >> 58) != (f.epoch >> 58)) a = f.epoch | (rec_indeg(db, f.fold) << 48);
+        const uint64_t v = (a & VAL48) > fx ? (a & VAL48) : fx;
+        const uint64_t left = ((a >> 48) & 0x3ff) - 1;
+        if (left == 0) dispatch(g, c, L, s, f, d, db, (int64_t)v, seq);
+        else *slot = (int64_t)(f.epoch | (left << 48) | v);
     }
 }
 
 template <int K>
-__device__ __forceinline__ int64_t next_time(const Ctx &c, const Rank<K> &s, int64_t tcur) {
-    if (s.due_s) return tcur;
-    int64_t nt = TINF;
-    if (s.host_n >= 0) nt = s.host_e;
+__device__ __forceinline__ void load_head(const Ctx &c, const Lane &L, Rank<K> &s) {
+    if (s.ring_head < s.ring_seen) {
+        const int i = c.ring_inst[s.ring_head * c.R + L.r];
+        s.head_node = c.ring_node[s.ring_head * c.R + L.r];
+        s.head_s = c.inst_s[i];
+        s.head_e = c.inst_e[i];
+        s.head_alloc = 0;
+    }
+}
+
+// After reservations: pick up comm-FIFO entries appended for this rank.
+template <int K>
+__device__ __forceinline__ void refresh_ring(const Ctx &c, const Lane &L, Rank<K> &s) {
+    const int tail = c.ring_tail[L.r];
+    if (tail != s.ring_seen) {
+        const bool was_empty = s.ring_head == s.ring_seen;
+        s.ring_seen = tail;
+        if (was_empty) load_head(c, L, s);
+    }
+}
+
+template <int K>
+__device__ __forceinline__ int64_t next_time(const Rank<K> &s, int64_t tcur) {
+    if (s.due.head >= 0) return tcur;
+    int64_t nt = s.host_n >= 0 ? s.host_e : TINF;
 #pragma unroll
     for (int q = 0; q < K; q++) if (s.occ_n[q] >= 0 && s.occ_e[q] < nt) nt = s.occ_e[q];
-    if (s.ring_head < c.ring_tail[s.r]) {
-        int64_t e = c.inst_e[c.ring_inst[(size_t)s.ring_head * c.g.R + s.r]];
-        nt = e < nt ? e : nt;
-    }
+    if (s.ring_head < s.ring_seen && s.head_e < nt) nt = s.head_e;
     return nt;
 }
 
 // Events already scheduled for exactly t join the due set.
 template <int K>
-__device__ __forceinline__ void gather_due(const Ctx &c, Rank<K> &s, int64_t t) {
-    const int r = s.r;
-    if (s.host_n >= 0 && s.host_e == t) { bm_insert(c.due, s.due_s, r, s.host_n); s.host_n = -1; }
+__device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, const Lane &L, Rank<K> &s,
+                                           int64_t t) {
+    const int R = c.R;
+    if (s.host_n >= 0 && s.host_e == t) { ms_insert(s.due, c.due, R, L.r, s.host_n); s.host_n = -1; }
 #pragma unroll
     for (int q = 0; q < K; q++)
-        if (s.occ_n[q] >= 0 && s.occ_e[q] == t) { bm_insert(c.due, s.due_s, r, s.occ_n[q]); s.occ_n[q] = -1; }
-    const int tail = c.ring_tail[r];
-    while (s.ring_head < tail) {
-        size_t at = (size_t)s.ring_head * c.g.R + r;
-        if (c.inst_e[c.ring_inst[at]] != t) break;
-        bm_insert(c.due, s.due_s, r, c.ring_node[at]);
+        if (s.occ_n[q] >= 0 && s.occ_e[q] == t) { ms_insert(s.due, c.due, R, L.r, s.occ_n[q]); s.occ_n[q] = -1; }
+    while (s.ring_head < s.ring_seen && s.head_e == t) {
+        if (!s.head_alloc) { const uint4 hb = rec_b(g, L.nb + s.head_node); s.alloc_t += rec_u64(hb.z, hb.w); }  // zero-length: starts now
+        ms_insert(s.due, c.due, R, L.r, s.head_node);
         s.ring_head++;
+        load_head(c, L, s);
     }
 }
 
-// Close the interval [tcur, tnew): busy/overlap integration and the
-// alloc-before-free memory high-water mark at tcur (simulator.py:381-393).
+// Close [tcur, tnew): busy/overlap integration (simulator.py:346-354 as a
+// timeline) and the alloc-before-free high-water mark at tcur (:381-393).
 template <int K>
-__device__ __forceinline__ void advance(const Ctx &c, Rank<K> &s, int64_t tcur, int64_t tnew) {
-    const int r = s.r;
-    const int tail = c.ring_tail[r];
-    while (s.ring_acur < tail) {   // collectives that started by tcur allocate their outputs then
-        size_t at = (size_t)s.ring_acur * c.g.R + r;
-        if (c.inst_s[c.ring_inst[at]] > tcur) break;
-        s.alloc_t += c.g.node_alloc[s.nb + c.ring_node[at]];
-        s.ring_acur++;
+__device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const Lane &L, Rank<K> &s,
+                                        int64_t tcur, int64_t tnew) {
+    const int R = c.R;
+    const bool head = s.ring_head < s.ring_seen;
+    if (head && !s.head_alloc && s.head_s <= tcur) {   // a collective that started by tcur
+        const uint4 hb = rec_b(g, L.nb + s.head_node);
+        s.alloc_t += rec_u64(hb.z, hb.w);
+        s.head_alloc = 1;
     }
-    s.cur += s.alloc_t;
-    s.peak = s.cur > s.peak ? s.cur : s.peak;
-    s.cur -= s.free_t;
-    s.alloc_t = s.free_t = 0;
+    if (s.alloc_t | s.free_t) {
+        int64_t cur = c.stat[ST_CUR * R + L.r] + s.alloc_t;
+        const int64_t pk = c.stat[ST_PEAK * R + L.r];
+        if (cur > pk) c.stat[ST_PEAK * R + L.r] = cur;
+        c.stat[ST_CUR * R + L.r] = cur - s.free_t;
+        s.alloc_t = s.free_t = 0;
+    }
     if (tnew == TINF) return;
-    int64_t dt = tnew - tcur;
+    const int64_t dt = tnew - tcur;
     bool comp_on = false;
 #pragma unroll
     for (int q = 0; q < K; q++) comp_on |= s.occ_n[q] >= 0;
-    bool comm_on = false;
-    if (s.ring_head < tail) comm_on = c.inst_s[c.ring_inst[(size_t)s.ring_head * c.g.R + r]] <= tcur;
-    if (comp_on) s.comp_busy += dt;
-    if (comm_on) s.comm_busy += dt;
-    if (comp_on && comm_on) s.overlap += dt;
+    const bool comm_on = head && s.head_s <= tcur;
+    if (comp_on) c.stat[ST_COMP * R + L.r] += dt;
+    if (comm_on) {
+        c.stat[ST_COMM * R + L.r] += dt;
+        if (comp_on) c.stat[ST_OVL * R + L.r] += dt;
+    }
 }
 
-__device__ __forceinline__ bool comp_before(const Ctx &c, int a, int b, bool init) {
-    // reservation order of instances that completed in the same step
-    int64_t la = c.g.inst_lead_id[a], lb = c.g.inst_lead_id[b];
+__device__ __forceinline__ bool comp_before(const DevGraph &g, const Ctx &c, int a, int b, bool init) {
+    // reservation order of instances completed in the same step
+    const int64_t la = g.inst_lead_id[a], lb = g.inst_lead_id[b];
     if (init) {
         if (la != lb) return la < lb;
-        return c.g.inst_init_key[a] < c.g.inst_init_key[b];
+        return g.inst_init_key[a] < g.inst_init_key[b];
     }
-    unsigned long long ka = c.inst_ckey[a] >> 12, kb = c.inst_ckey[b] >> 12;
+    const unsigned long long ka = c.inst_ckey[a] >> 12, kb = c.inst_ckey[b] >> 12;
     if (ka != kb) return ka < kb;
     if (la != lb) return la < lb;
     return (c.inst_ckey[a] & 0xfff) < (c.inst_ckey[b] & 0xfff);
 }
 
-// Reserve the comm streams for every instance completed in this step
-// (simulator.py:298-309); block-wide.  Returns max critical-path value seen.
-__device__ int64_t reserve(const Ctx &c, Shared &sh, int &par, int64_t t, bool init, int cfg) {
-    __syncthreads();
-    const int nc = sh.ncomp;
+// Reserve the comm streams of every instance completed in this step, in the
+// reference's order (simulator.py:298-309); block-wide.  Returns the largest
+// critical-path finish among them.
+__device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, const Ctx &c, Shared &sh, int &par,
+                                          int64_t t, bool init, int cfg, uint64_t epoch, int nc) {
     int64_t cpm = 0;
-    if (nc == 0) return 0;
     if (threadIdx.x == 0) {
         for (int a = 1; a < nc; a++) {
-            int x = c.complist[a], b = a - 1;
-            while (b >= 0 && comp_before(c, x, c.complist[b], init)) { c.complist[b + 1] = c.complist[b]; b--; }
+            const int x = c.complist[a];
+            int b = a - 1;
+            while (b >= 0 && comp_before(g, c, x, c.complist[b], init)) { c.complist[b + 1] = c.complist[b]; b--; }
             c.complist[b + 1] = x;
         }
     }
     __syncthreads();
+    const int R = c.R;
     for (int q = 0; q < nc; q++) {
         const int i = c.complist[q];
-        const int64_t m0 = c.g.inst_mem_off[i], nm = c.g.inst_mem_off[i + 1] - m0;
+        const int64_t m0 = g.inst_mem_off[i], nm = g.inst_mem_off[i + 1] - m0;
         int64_t local = t;
         for (int64_t j = threadIdx.x; j < nm; j += blockDim.x) {
-            int64_t ce = c.comm_end[c.g.inst_mem_rank[m0 + j]];
+            const int64_t ce = c.comm_end[g.inst_mem_rank[m0 + j]];
             local = ce > local ? ce : local;
         }
         const int64_t s = block_max_i64(local, sh, par);
         const int64_t e = s + c.inst_dur[i];
         const int64_t cpv = c.inst_cpmax[i] + c.inst_dur[i];
         cpm = cpv > cpm ? cpv : cpm;
-        for (int64_t j = threadIdx.x; j < nm; j += blockDim.x) {
-            int m = c.g.inst_mem_rank[m0 + j], node = c.g.inst_mem_node[m0 + j];
-            c.comm_end[m] = e;
-            int slot = c.ring_tail[m]++;
-            c.ring_inst[(size_t)slot * c.g.R + m] = i;
-            c.ring_node[(size_t)slot * c.g.R + m] = node;
-            c.cp[(size_t)node * c.g.R + m] = cpv;
-            if (c.o.ev_start) {
-                size_t at = ((size_t)cfg * c.g.R + m) * c.g.max_nodes + node;
-                c.o.ev_start[at] = s;
-                c.o.ev_end[at] = e;
-            }
-        }
         if (threadIdx.x == 0) { c.inst_s[i] = s; c.inst_e[i] = e; }
+        for (int64_t j = threadIdx.x; j < nm; j += blockDim.x) {
+            const int m = g.inst_mem_rank[m0 + j], node = g.inst_mem_node[m0 + j];
+            c.comm_end[m] = e;
+            const int slot = c.ring_tail[m]++;
+            c.ring_inst[slot * R + m] = i;
+            c.ring_node[slot * R + m] = node;
+            c.cp[node * R + m] = (int64_t)(epoch | (uint64_t)cpv);
+            record(g, o, cfg, m, node, s, e);
+        }
         __syncthreads();
     }
     if (threadIdx.x == 0) sh.ncomp = 0;
@@ -452,41 +540,81 @@ __device__ int64_t reserve(const Ctx &c, Shared &sh, int &par, int64_t t, bool i
     return cpm;
 }
 
+// Barrier, then reserve whatever completed since the last reservation.
+__device__ __forceinline__ int64_t reserve(const DevGraph &g, const DevOut &o, const Ctx &c, Shared &sh, int &par,
+                                           int64_t t, bool init, int cfg, uint64_t epoch) {
+    __syncthreads();
+    const int nc = sh.ncomp;
+    return nc ? reserve_n(g, o, c, sh, par, t, init, cfg, epoch, nc) : 0;
+}
+
 template <int K>
-__global__ void __launch_bounds__(1024, 1) sweep_kernel(DevGraph g, DevPoints p, DevOut o, DevScratch sc) {
+__global__ void __launch_bounds__(1024, 1)
+    sweep_kernel(const __grid_constant__ DevGraph g, const __grid_constant__ DevPoints p,
+                 const __grid_constant__ DevOut o, const __grid_constant__ DevScratch sc) {
     extern __shared__ __align__(16) unsigned char smem[];
     Shared &sh = *reinterpret_cast<Shared *>(smem);
-    int64_t *comm_end = reinterpret_cast<int64_t *>(smem + sizeof(Shared));
-    int32_t *ring_tail = reinterpret_cast<int32_t *>(comm_end + g.R);
-
-    // per-CTA scratch slot
-    unsigned char *base = sc.base + (size_t)blockIdx.x * sc.slot_bytes;
-    Ctx c;
-    c.g = g; c.p = p; c.o = o;
-    const size_t bw = (size_t)g.max_words * g.R;
-    uint64_t *bits = reinterpret_cast<uint64_t *>(base + sc.off_bits);
-    c.done = Bits{bits, g.R};
-    c.rdyc = Bits{bits + bw, g.R};
-    c.rdyh = Bits{bits + 2 * bw, g.R};
-    c.due = Bits{bits + 3 * bw, g.R};
-    c.cp = reinterpret_cast<int64_t *>(base + sc.off_cp);
-    c.ring_inst = reinterpret_cast<int32_t *>(base + sc.off_ring);
-    c.ring_node = c.ring_inst + (size_t)g.coll_stride * g.R;
-    c.dur = reinterpret_cast<int64_t *>(base + sc.off_dur);
-    c.inst_dur = reinterpret_cast<int64_t *>(base + sc.off_inst);
-    c.inst_s = c.inst_dur + g.n_inst;
-    c.inst_e = c.inst_s + g.n_inst;
-    c.inst_cpmax = c.inst_e + g.n_inst;
-    c.inst_ckey = reinterpret_cast<unsigned long long *>(c.inst_cpmax + g.n_inst);
-    c.inst_wait = reinterpret_cast<int32_t *>(c.inst_ckey + g.n_inst);
-    c.complist = c.inst_wait + g.n_inst;
-    c.comm_end = comm_end;
-    c.ring_tail = ring_tail;
-    c.ncomp = &sh.ncomp;
-
+    const int R = g.R;
     const int tid = threadIdx.x, bd = blockDim.x;
+
+    // ---- carve shared memory and this CTA's scratch slot ----
+    // (the pointer table lives in shared memory: it is block-uniform and would
+    // otherwise pin ~34 registers per thread)
+    __shared__ Ctx c_sh;
+    Ctx &c = c_sh;
+    if (tid == 0) {
+        c.R = R;
+        unsigned char *sp = smem + sc.sm_off_dyn;
+        c.comm_end = reinterpret_cast<int64_t *>(sp);
+        c.stat = c.comm_end + R;
+        c.ring_tail = reinterpret_cast<int32_t *>(c.stat + ST_N * R);
+        unsigned char *base = sc.base + (size_t)blockIdx.x * sc.slot_bytes;
+        const size_t words = (size_t)g.max_words * R;
+        uint64_t *gbits = reinterpret_cast<uint64_t *>(base + sc.off_bits);
+        c.rdyc = gbits;
+        c.rdyh = gbits + words;
+        c.due = gbits + 2 * words;
+        c.done = sc.done_in_smem ? reinterpret_cast<uint64_t *>(smem + sc.sm_off_done) : gbits + 3 * words;
+        c.cp = reinterpret_cast<int64_t *>(base + sc.off_cp);
+        c.ring_inst = reinterpret_cast<int32_t *>(base + sc.off_ring);
+        c.ring_node = c.ring_inst + (size_t)g.coll_stride * R;
+        c.dur = sc.dur_in_smem ? reinterpret_cast<int64_t *>(smem + sc.sm_off_dur)
+                               : reinterpret_cast<int64_t *>(base + sc.off_dur);
+        unsigned char *ib = sc.inst_in_smem ? smem + sc.sm_off_inst : base + sc.off_inst;
+        const int NI = g.n_inst;
+        c.inst_dur = reinterpret_cast<int64_t *>(ib);
+        c.inst_s = c.inst_dur + NI;
+        c.inst_e = c.inst_s + NI;
+        c.inst_cpmax = c.inst_e + NI;
+        c.inst_ckey = reinterpret_cast<unsigned long long *>(c.inst_cpmax + NI);
+        c.inst_wait = reinterpret_cast<int32_t *>(c.inst_ckey + NI);
+        c.complist = c.inst_wait + NI;
+        c.ncomp = &sh.ncomp;
+    }
+    __syncthreads();
+    uint64_t *gbits = c.rdyc;
+    const size_t words = (size_t)g.max_words * R;
+    const int NI = g.n_inst;
+
+    const bool active = tid < R;
+    Lane L;
+    L.r = active ? tid : 0;
+    {
+        const int st = g.rank_struct[L.r];
+        L.nb = g.s_node_off[st];
+        L.tb = g.s_tens_off[st];
+    }
+    const int my_n = active ? g.s_node_off[g.rank_struct[L.r] + 1] - L.nb : 0;
+
     int par = 0;
     if (tid == 0) { sh.parity = 0; sh.ncomp = 0; sh.flag = 0; }
+    // the three global bitmaps are all-zero after a point that ran to completion;
+    // clear them once up front and again only after a point that did not
+    for (size_t i = tid; i < (sc.done_in_smem ? 3 : 4) * words; i += bd) gbits[i] = 0;
+    bool dirty = false;
+    const size_t acc_words = (size_t)g.max_nodes * R;
+    for (size_t i = tid; i < acc_words; i += bd) c.cp[i] = 0;   // epoch 0 = empty
+    unsigned epoch = 0;
 
     for (int cfg = blockIdx.x; cfg < p.n; cfg += gridDim.x) {
         // ---- cost stage (K1): this point's durations ----
@@ -494,7 +622,7 @@ __global__ void __launch_bounds__(1024, 1) sweep_kernel(DevGraph g, DevPoints p,
         const double bwv = p.bw[cfg];
         const int64_t lat = p.latency[cfg];
         int bad = 0, zero = 0;
-        for (int i = tid; i < g.n_inst; i += bd) {
+        for (int i = tid; i < NI; i += bd) {
             int64_t d = coll_time(g, i, algo, topo, bwv, lat, p.rows[cfg], p.cols[cfg]);
             if (d < 0) { bad = 1; d = 0; }
             zero |= d == 0;
@@ -506,121 +634,192 @@ __global__ void __launch_bounds__(1024, 1) sweep_kernel(DevGraph g, DevPoints p,
             c.inst_e[i] = 0;
         }
         const bool recost = p.peak_flops != nullptr;
+        int zdur = 0;   // a zero-duration COMP or non-static HOST could complete at t = 0
         for (int n = tid; n < g.total_nodes; n += bd) {
             int64_t d = g.node_dur[n];
-            if (recost && g.node_kind[n] == FL_COMP && g.node_flops[n] >= 0)
-                d = flops_to_ns(g.node_flops[n], p.peak_flops[cfg], p.efficiency[cfg]);
+            if (recost && g.node_flops[n] >= 0) d = flops_to_ns(g.node_flops[n], p.peak_flops[cfg], p.efficiency[cfg]);
             c.dur[n] = d;
+            if (d == 0) {
+                const uint4 nb_ = rec_b(g, n);
+                zdur |= rec_kind(nb_) == FL_COMP || (rec_kind(nb_) == FL_HOST && !rec_static(nb_));
+            }
         }
-        for (size_t i = tid; i < 4 * bw; i += bd) bits[i] = 0;
-        for (int r = tid; r < g.R; r += bd) { comm_end[r] = 0; ring_tail[r] = 0; }
+        if (dirty) for (size_t i = tid; i < 3 * words; i += bd) gbits[i] = 0;
+        for (size_t i = tid; i < words; i += bd) c.done[i] = 0;
+        for (int r = tid; r < R; r += bd) {
+            c.comm_end[r] = 0;
+            c.ring_tail[r] = 0;
+#pragma unroll
+            for (int k = 0; k < ST_N; k++) c.stat[k * R + r] = 0;
+        }
         bad = __syncthreads_or(bad);
         zero = __syncthreads_or(zero);
+        zdur = __syncthreads_or(zdur);
         if (bad) {
             if (tid == 0) o.status[cfg] = FL_ERR_UNSUPPORTED_ALGO;
+            dirty = false;
             continue;
         }
-        Cfg f;
-        f.dur = c.dur;
-        f.serial = zero;
+        if (++epoch == 64) {       // 6-bit tags wrap: start a fresh accumulator table
+            for (size_t i = tid; i < acc_words; i += bd) c.cp[i] = 0;
+            epoch = 1;
+            __syncthreads();
+        }
+        Step f;
         f.step = 0;
+        f.epoch = (uint64_t)epoch << 58;
         f.init = 1;
+        f.fold = g.fold_ok && !zero && !zdur;
 
         // ---- per-rank state ----
         Rank<K> s;
-        const bool active = tid < g.R;
-        s.r = active ? tid : 0;
-        const int st = g.rank_struct[s.r];
-        s.nb = g.s_node_off[st];
-        s.N = active ? g.s_node_off[st + 1] - s.nb : 0;
-        s.tb = g.s_tens_off[st];
-        s.due_s = s.rc_s = s.rh_s = 0;
+        s.due.head = s.rc.head = s.rh.head = -1;
+        s.due.sum = s.rc.sum = s.rh.sum = 0;
         s.host_slot = 0; s.host_e = 0; s.host_n = -1;
         const int ncs = p.compute_streams;
 #pragma unroll
         for (int q = 0; q < K; q++) { s.slot[q] = q < ncs ? 0 : TINF; s.occ_e[q] = 0; s.occ_n[q] = -1; }
-        s.ring_head = s.ring_acur = 0;
-        s.comp_busy = s.comm_busy = s.overlap = s.finish = s.cur = s.peak = s.free_t = s.cpmax = 0;
-        s.alloc_t = active ? g.s_init_alloc[st] : 0;
+        s.head_s = s.head_e = 0; s.head_node = 0; s.head_alloc = 0;
+        s.ring_head = s.ring_seen = 0;
+        s.alloc_t = active ? g.s_init_alloc[g.rank_struct[L.r]] : 0;
+        s.free_t = 0;
+        s.cpmax = 0;
         s.done_cnt = 0;
         s.pop_seq = 0;
 
         // ---- t = 0: initial dispatch + start phase (simulator.py:275-277) ----
         if (active) {
+            const int st = g.rank_struct[L.r];
             for (int q = g.s_init_off[st]; q < g.s_init_off[st + 1]; q++) {
-                int d = g.init_list[q];
-                if (g.node_flags[s.nb + d] & 1) continue;
-                dispatch(c, f, s, d, 0);
+                const int d = g.init_list[q];
+                const uint4 db = rec_b(g, L.nb + d);
+                if (rec_never(db) || (f.fold && rec_static(db))) continue;
+                dispatch(g, c, L, s, f, d, db, 0, 0);
             }
-            start_phase(c, f, s, 0, cfg);
+            start_phase(g, o, c, L, s, 0, cfg);
         }
-        int64_t cpm = reserve(c, sh, par, 0, true, cfg);
+        int64_t cpm = reserve(g, o, c, sh, par, 0, true, cfg, f.epoch);
+        if (active) refresh_ring(c, L, s);
         f.init = 0;
+        if (f.fold) {
+            // ---- t = 0 host pops, folded.  Every HOST with no dependencies and zero
+            // duration starts at t=0 in the initial start phase and completes at t=0
+            // (simulator.py:282-287); with no other zero-length node in this design
+            // point they are the only t=0 events, popped in id order.  Their effect
+            // is (a) counted away in the dependency accumulators (in-degree without
+            // static hosts) and (b) the dispatch of nodes waiting only on them,
+            // replayed here in (trigger host, position) order, each host's pop
+            // followed by its start phase.
+            f.step++;
+            if (active) {
+                const int st = g.rank_struct[L.r];
+                s.pop_seq = 0;
+                int prev = -1;
+                for (int q = g.trig_off[st]; q < g.trig_off[st + 1]; q++) {
+                    const int4 tr = g.trig[q];
+                    if (tr.x != prev) {
+                        if (prev >= 0) start_phase(g, o, c, L, s, 0, cfg);
+                        s.pop_seq++;
+                        prev = tr.x;
+                    }
+                    dispatch(g, c, L, s, f, tr.y, rec_b(g, L.nb + tr.y), 0, tr.z);
+                }
+                if (prev >= 0) start_phase(g, o, c, L, s, 0, cfg);
+                s.done_cnt += g.s_nstatic[st];
+                if (o.ev_start)
+                    for (int q = g.static_off[st]; q < g.static_off[st + 1]; q++)
+                        record(g, o, cfg, L.r, g.static_list[q], 0, 0);
+            }
+            const int64_t v = reserve(g, o, c, sh, par, 0, false, cfg, f.epoch);
+            cpm = v > cpm ? v : cpm;
+            if (active) refresh_ring(c, L, s);
+        }
         int64_t tcur = 0;
         bool overflow = false;
 
         // ---- event loop ----
+        const int64_t TCAP = (int64_t)1 << 48;   // 48-bit accumulators; keys pack (t, rank)
         for (;;) {
-            int64_t nt = active ? next_time(c, s, tcur) : TINF;
-            const int64_t TCAP = (int64_t)1 << 49;   // keys pack (t, rank) into 64 bits
-            uint64_t key = nt == TINF ? KINF : ((uint64_t)(nt < TCAP ? nt : TCAP) << 14) | (uint64_t)s.r;
+            int64_t nt = active ? next_time(s, tcur) : TINF;
+            uint64_t key = nt == TINF ? KINF : ((uint64_t)(nt < TCAP ? nt : TCAP) << 14) | (uint64_t)L.r;
             uint64_t kmin = block_min_u64(key, sh, par);
+            // collectives completed by the previous step's pops: reserve them now (the
+            // reduction's barrier made every arrival visible), then re-derive the next time
+            const int nc = sh.ncomp;
+            if (nc) {
+                const int64_t v = reserve_n(g, o, c, sh, par, tcur, false, cfg, f.epoch, nc);
+                cpm = v > cpm ? v : cpm;
+                if (active) refresh_ring(c, L, s);
+                nt = active ? next_time(s, tcur) : TINF;
+                key = nt == TINF ? KINF : ((uint64_t)(nt < TCAP ? nt : TCAP) << 14) | (uint64_t)L.r;
+                kmin = block_min_u64(key, sh, par);
+            }
             if (kmin == KINF) break;
             const int64_t t = (int64_t)(kmin >> 14);
             const int rmin = (int)(kmin & 0x3fff);
             if (t >= TCAP || f.step >= (1ull << 25) - 2) { overflow = true; break; }
             if (t > tcur) {
-                if (active) advance(c, s, tcur, t);
+                if (active) advance(g, c, L, s, tcur, t);
                 tcur = t;
             }
             f.step++;
-            if (!f.serial) {
+            if (!zero) {
                 if (active) {
-                    gather_due(c, s, t);
-                    if (s.r > rmin) start_phase(c, f, s, t, cfg);
+                    gather_due(g, c, L, s, t);
+                    if (L.r > rmin) start_phase(g, o, c, L, s, t, cfg);
                     s.pop_seq = 0;
-                    while (s.due_s) {
-                        int x = bm_pop(c.due, s.due_s, s.r);
-                        pop_event(c, f, s, x, t);
-                        start_phase(c, f, s, t, cfg);
+                    while (s.due.head >= 0) {
+                        const int x = ms_pop(s.due, c.due, R, L.r);
+                        pop_event(g, c, L, s, f, x, t);
+                        start_phase(g, o, c, L, s, t, cfg);
                     }
                 }
-                int64_t v = reserve(c, sh, par, t, false, cfg);
-                cpm = v > cpm ? v : cpm;
             } else {
                 // serial mode: the reference loop verbatim, one pop per iteration
-                if (active) gather_due(c, s, t);
+                if (active) gather_due(g, c, L, s, t);
                 for (;;) {
-                    uint64_t k2 = (active && s.due_s) ? (((uint64_t)s.r << 13) | (uint64_t)bm_peek(c.due, s.due_s, s.r)) : KINF;
-                    uint64_t m2 = block_min_u64(k2, sh, par);
+                    const uint64_t k2 = (active && s.due.head >= 0) ? (((uint64_t)L.r << 13) | (uint64_t)s.due.head)
+                                                                     : KINF;
+                    const uint64_t m2 = block_min_u64(k2, sh, par);
                     if (m2 == KINF) break;
                     f.step++;
-                    if (active && (int)(m2 >> 13) == s.r) {
+                    if (active && (int)(m2 >> 13) == L.r) {
                         s.pop_seq = 0;
-                        int x = bm_pop(c.due, s.due_s, s.r);
-                        pop_event(c, f, s, x, t);
+                        const int x = ms_pop(s.due, c.due, R, L.r);
+                        pop_event(g, c, L, s, f, x, t);
                     }
-                    if (active) start_phase(c, f, s, t, cfg);
-                    int64_t v = reserve(c, sh, par, t, false, cfg);
+                    if (active) start_phase(g, o, c, L, s, t, cfg);
+                    const int64_t v = reserve(g, o, c, sh, par, t, false, cfg, f.epoch);
                     cpm = v > cpm ? v : cpm;
-                    if (active) gather_due(c, s, t);
+                    if (active) {
+                        refresh_ring(c, L, s);
+                        gather_due(g, c, L, s, t);
+                    }
                 }
             }
         }
-        if (active) advance(c, s, tcur, TINF);
+        if (active) advance(g, c, L, s, tcur, TINF);
 
         // ---- row: reductions over ranks (cli.py:336-341) ----
-        int dead = active && s.done_cnt != s.N;
-        dead = __syncthreads_or(dead);
-        int64_t exposed = s.comm_busy - s.overlap;
-        int64_t vals[6] = {s.finish, s.cpmax > cpm ? s.cpmax : cpm, s.comp_busy, s.comm_busy, exposed, s.peak};
-        if (!active) for (int k = 0; k < 6; k++) vals[k] = 0;
-        if (o.rank_stats && active) {
-            int64_t *rs = o.rank_stats + ((size_t)cfg * g.R + s.r) * 5;
-            rs[0] = s.finish; rs[1] = s.comp_busy; rs[2] = s.comm_busy; rs[3] = exposed; rs[4] = s.peak;
+        int dead = active && s.done_cnt != my_n;
+        dead = __syncthreads_or(dead | overflow);
+        dirty = dead != 0;
+        int64_t vals[6] = {0, 0, 0, 0, 0, 0};
+        if (active) {
+            const int64_t comm = c.stat[ST_COMM * R + L.r];
+            vals[0] = c.stat[ST_FIN * R + L.r];
+            vals[1] = s.cpmax > cpm ? s.cpmax : cpm;
+            vals[2] = c.stat[ST_COMP * R + L.r];
+            vals[3] = comm;
+            vals[4] = comm - c.stat[ST_OVL * R + L.r];
+            vals[5] = c.stat[ST_PEAK * R + L.r];
+            if (o.rank_stats) {
+                int64_t *rs = o.rank_stats + ((size_t)cfg * R + L.r) * 5;
+                rs[0] = vals[0]; rs[1] = vals[2]; rs[2] = vals[3]; rs[3] = vals[4]; rs[4] = vals[5];
+            }
         }
         for (int k = 0; k < 6; k++) {
-            int64_t v = block_max_i64(vals[k], sh, par);
+            const int64_t v = block_max_i64(vals[k], sh, par);
             if (tid == 0) o.rows[(size_t)cfg * 6 + k] = v;
         }
         if (tid == 0) o.status[cfg] = overflow ? FL_ERR_CAPACITY : dead ? FL_ERR_DEADLOCK : FL_OK;
@@ -641,6 +840,15 @@ cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t s
 cudaError_t sweep_occupancy(int block, size_t smem, int *occ) {
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, sweep_kernel<1>, block, smem);
 }
+
+cudaError_t sweep_set_smem(size_t smem) {
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return e;
+}
+
+size_t sweep_shared_header_bytes() { return (sizeof(Shared) + 15) / 16 * 16; }
 
 cudaError_t launch_cost_only(int n, const uint8_t *kind, const int64_t *size, const int64_t *gn,
                              const uint8_t *algo, const double *alpha, const double *beta,

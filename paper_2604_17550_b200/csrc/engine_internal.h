@@ -20,6 +20,13 @@ struct DevGraph {
     const int32_t *inst_n;
     const int64_t *inst_bytes, *inst_lead_id, *inst_init_key, *inst_mem_off;
     const int32_t *inst_mem_rank, *inst_mem_node, *rank_coll_inst;
+    // derived on upload (capi.cu): packed per-node records and tensor consumer ranges
+    const uint4 *node_rec;       // [2 * total_nodes]
+    const int2 *tens_rng;        // [total_tens] {first, end} into tens_cons
+    // static-host folding (engine.cu "t = 0 host pops")
+    int fold_ok;
+    const int32_t *s_nstatic, *trig_off, *static_off, *static_list;
+    const int4 *trig;            // {trigger host, node, position in the host's dependents, -}
 };
 
 struct DevPoints {
@@ -41,11 +48,16 @@ struct DevOut {
 struct DevScratch {
     unsigned char *base;
     size_t slot_bytes, off_bits, off_cp, off_ring, off_dur, off_inst;
+    // dynamic shared-memory layout (bytes from the start of the CTA's smem)
+    unsigned sm_off_dyn, sm_off_done, sm_off_dur, sm_off_inst;
+    int done_in_smem, dur_in_smem, inst_in_smem;
 };
 
 cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t st, const DevGraph &g,
                          const DevPoints &p, const DevOut &o, const DevScratch &sc);
 cudaError_t sweep_occupancy(int block, size_t smem, int *occ);
+cudaError_t sweep_set_smem(size_t smem);
+size_t sweep_shared_header_bytes();
 cudaError_t launch_cost_only(int n, const uint8_t *kind, const int64_t *size, const int64_t *gn,
                              const uint8_t *algo, const double *alpha, const double *beta,
                              const int32_t *rows, const int32_t *cols, int64_t *out, int32_t *status,

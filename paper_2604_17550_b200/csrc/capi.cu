@@ -162,6 +162,47 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
             }
             static_off[s + 1] = (int32_t)static_list.size();
         }
+        // A tensor is freed when its last consumer completes (simulator.py:384-388).
+        // When one consumer depends (transitively) on all the others it is always the
+        // last to finish, so the free can be attributed to it statically.
+        std::vector<int32_t> last_cons((size_t)(total_t > 0 ? total_t : 1), -1);
+        for (int s = 0; s < S; s++) {
+            const int nb = d->s_node_off[s], n = d->s_node_off[s + 1] - nb;
+            const int tb = d->s_tens_off[s], nt = d->s_tens_off[s + 1] - tb;
+            const int W = (n + 63) / 64;
+            std::vector<uint64_t> anc((size_t)n * (W > 0 ? W : 1), 0);
+            std::vector<int> indeg(n), order;
+            order.reserve(n);
+            for (int v = 0; v < n; v++) {
+                indeg[v] = d->pred_off[nb + v + 1] - d->pred_off[nb + v];
+                if (!indeg[v]) order.push_back(v);
+            }
+            for (size_t k = 0; k < order.size(); k++) {
+                const int v = order[k];
+                for (int q = d->succ_off[nb + v]; q < d->succ_off[nb + v + 1]; q++) {
+                    const int w = d->succ_idx[q];
+                    uint64_t *aw = &anc[(size_t)w * W];
+                    const uint64_t *av = &anc[(size_t)v * W];
+                    for (int k2 = 0; k2 < W; k2++) aw[k2] |= av[k2];
+                    aw[v >> 6] |= 1ull << (v & 63);
+                    if (--indeg[w] == 0) order.push_back(w);
+                }
+            }
+            if ((int)order.size() != n) continue;   // cyclic: leave every free to the run-time check
+            for (int t = 0; t < nt; t++) {
+                const int c0 = d->tens_cons_off[tb + t], c1 = d->tens_cons_off[tb + t + 1];
+                if (c1 - c0 < 2) continue;
+                for (int a = c0; a < c1; a++) {
+                    const int cand = d->tens_cons[a];
+                    bool dom = true;
+                    for (int b = c0; b < c1 && dom; b++) {
+                        const int o = d->tens_cons[b];
+                        if (o != cand) dom = (anc[(size_t)cand * W + (o >> 6)] >> (o & 63)) & 1ull;
+                    }
+                    if (dom) { last_cons[tb + t] = cand; break; }
+                }
+            }
+        }
         int s_of = 0;
         for (int i = 0; i < total; i++) {
             while (s_of + 1 < S && i >= d->s_node_off[s_of + 1]) s_of++;
@@ -175,8 +216,8 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
             for (int q = d->free_off[i]; q < d->free_off[i + 1]; q++) {
                 const int t = d->free_tens[q];
                 const int nc = d->tens_cons_off[tb + t + 1] - d->tens_cons_off[tb + t];
-                if (nc == 1) ufree += (uint64_t)d->tens_bytes[tb + t];   // sole consumer: freed when it completes
-                else mfree.push_back(t);
+                if (nc == 1 || last_cons[tb + t] == i - nb) ufree += (uint64_t)d->tens_bytes[tb + t];
+                else if (last_cons[tb + t] < 0) mfree.push_back(t);     // decided at run time (done bitmap)
             }
             const uint64_t alloc = (uint64_t)d->node_alloc[i];
             const unsigned meta = (unsigned)d->node_kind[i] | ((unsigned)(d->node_flags[i] & 1) << 4) |
@@ -212,6 +253,7 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
         dg.fold_ok = fold_ok;
         std::vector<int2> tc((size_t)(total_t > 0 ? total_t : 1));
         for (int i = 0; i < total_t; i++) tc[i] = make_int2(d->tens_cons_off[i], d->tens_cons_off[i + 1]);
+        dg.needs_done = !mfree.empty();
         if (mfree.empty()) mfree.push_back(0);
         if (trig.empty()) trig.push_back(make_int4(0, 0, 0, 0));
         if (static_list.empty()) static_list.push_back(0);

@@ -197,7 +197,7 @@ __device__ __forceinline__ uint4 rec_c(const DevGraph &g, int gn) { return g.nod
 // (simulator.py:449-453) -- no per-rank in-degree table to initialize.
 constexpr uint64_t VAL48 = (1ull << 48) - 1;
 
-enum { ST_COMP = 0, ST_COMM, ST_OVL, ST_CUR, ST_PEAK, ST_FIN, ST_N };
+enum { ST_COMP = 0, ST_OVL, ST_CUR, ST_PEAK, ST_FIN, ST_N };
 
 // Per-CTA (block-uniform) state pointers.  Bitmaps are word-major,
 // rank-minor ([word][rank]) so a warp's 32 ranks touch one 256-byte segment;
@@ -238,6 +238,8 @@ struct Rank {
     int64_t slot[K], occ_e[K];
     int64_t head_s, head_e;         // comm-FIFO head (valid iff ring_head < ring_seen)
     int64_t alloc_t, free_t, cpmax;
+    int64_t commcum;                // integral of "comm stream busy" up to the current step (= comm busy)
+    int64_t comp_a;                 // commcum when the running compute node started (K == 1)
     int host_n;
     int occ_n[K];
     int head_node, head_alloc;
@@ -330,6 +332,10 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
         const int64_t e = t + c.dur[L.nb + x];
         { const uint4 xb = rec_b(g, L.nb + x); s.alloc_t += rec_u64(xb.z, xb.w); }
         record(g, o, cfg, L.r, x, t, e);
+        if (K == 1 && e > t) {      // one compute stream: its busy intervals are disjoint
+            c.stat[ST_COMP * R + L.r] += e - t;
+            s.comp_a = s.commcum;
+        }
 #pragma unroll
         for (int q = 0; q < K; q++) {
             if (q == k) {
@@ -373,7 +379,7 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
                                           const Step &f, int x, int64_t t) {
     const int R = c.R;
     const uint4 xa = rec_a(g, L.nb + x), xc = rec_c(g, L.nb + x);
-    c.done[(x >> 6) * R + L.r] |= 1ull << (x & 63);
+    if (g.needs_done) c.done[(x >> 6) * R + L.r] |= 1ull << (x & 63);
     s.done_cnt++;
     s.pop_seq++;
     c.stat[ST_FIN * R + L.r] = t;
@@ -441,7 +447,11 @@ __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, cons
     if (s.host_n >= 0 && s.host_e == t) { ms_insert(s.due, c.due, R, L.r, s.host_n); s.host_n = -1; }
 #pragma unroll
     for (int q = 0; q < K; q++)
-        if (s.occ_n[q] >= 0 && s.occ_e[q] == t) { ms_insert(s.due, c.due, R, L.r, s.occ_n[q]); s.occ_n[q] = -1; }
+        if (s.occ_n[q] >= 0 && s.occ_e[q] == t) {
+            ms_insert(s.due, c.due, R, L.r, s.occ_n[q]);
+            s.occ_n[q] = -1;
+            if (K == 1) c.stat[ST_OVL * R + L.r] += s.commcum - s.comp_a;   // comm time under [start, t)
+        }
     while (s.ring_head < s.ring_seen && s.head_e == t) {
         if (!s.head_alloc) { const uint4 hb = rec_b(g, L.nb + s.head_node); s.alloc_t += rec_u64(hb.z, hb.w); }  // zero-length: starts now
         ms_insert(s.due, c.due, R, L.r, s.head_node);
@@ -471,14 +481,16 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
     }
     if (tnew == TINF) return;
     const int64_t dt = tnew - tcur;
-    bool comp_on = false;
-#pragma unroll
-    for (int q = 0; q < K; q++) comp_on |= s.occ_n[q] >= 0;
     const bool comm_on = head && s.head_s <= tcur;
-    if (comp_on) c.stat[ST_COMP * R + L.r] += dt;
-    if (comm_on) {
-        c.stat[ST_COMM * R + L.r] += dt;
-        if (comp_on) c.stat[ST_OVL * R + L.r] += dt;
+    if (comm_on) s.commcum += dt;
+    if (K > 1) {                    // overlapping compute streams: integrate the union
+        bool comp_on = false;
+#pragma unroll
+        for (int q = 0; q < K; q++) comp_on |= s.occ_n[q] >= 0;
+        if (comp_on) {
+            c.stat[ST_COMP * R + L.r] += dt;
+            if (comm_on) c.stat[ST_OVL * R + L.r] += dt;
+        }
     }
 }
 
@@ -615,6 +627,9 @@ __global__ void __launch_bounds__(1024, 1)
     const size_t acc_words = (size_t)g.max_nodes * R;
     for (size_t i = tid; i < acc_words; i += bd) c.cp[i] = 0;   // epoch 0 = empty
     unsigned epoch = 0;
+    bool have_dur = false;          // durations of the previous point's device, reused when unchanged
+    double dev_pk = 0.0, dev_ef = 0.0;
+    int dev_zdur = 0;
 
     for (int cfg = blockIdx.x; cfg < p.n; cfg += gridDim.x) {
         // ---- cost stage (K1): this point's durations ----
@@ -634,8 +649,13 @@ __global__ void __launch_bounds__(1024, 1)
             c.inst_e[i] = 0;
         }
         const bool recost = p.peak_flops != nullptr;
-        int zdur = 0;   // a zero-duration COMP or non-static HOST could complete at t = 0
-        for (int n = tid; n < g.total_nodes; n += bd) {
+        const double pk = recost ? p.peak_flops[cfg] : 0.0, ef = recost ? p.efficiency[cfg] : 0.0;
+        const bool same_dev = have_dur && pk == dev_pk && ef == dev_ef;   // durations already in place
+        have_dur = true;
+        dev_pk = pk;
+        dev_ef = ef;
+        int zdur = same_dev ? dev_zdur : 0;   // a zero-duration COMP or non-static HOST could complete at t = 0
+        if (!same_dev) for (int n = tid; n < g.total_nodes; n += bd) {
             int64_t d = g.node_dur[n];
             if (recost && g.node_flops[n] >= 0) d = flops_to_ns(g.node_flops[n], p.peak_flops[cfg], p.efficiency[cfg]);
             c.dur[n] = d;
@@ -645,7 +665,7 @@ __global__ void __launch_bounds__(1024, 1)
             }
         }
         if (dirty) for (size_t i = tid; i < 3 * words; i += bd) gbits[i] = 0;
-        for (size_t i = tid; i < words; i += bd) c.done[i] = 0;
+        if (g.needs_done) for (size_t i = tid; i < words; i += bd) c.done[i] = 0;
         for (int r = tid; r < R; r += bd) {
             c.comm_end[r] = 0;
             c.ring_tail[r] = 0;
@@ -655,6 +675,7 @@ __global__ void __launch_bounds__(1024, 1)
         bad = __syncthreads_or(bad);
         zero = __syncthreads_or(zero);
         zdur = __syncthreads_or(zdur);
+        dev_zdur = zdur;
         if (bad) {
             if (tid == 0) o.status[cfg] = FL_ERR_UNSUPPORTED_ALGO;
             dirty = false;
@@ -684,6 +705,8 @@ __global__ void __launch_bounds__(1024, 1)
         s.alloc_t = active ? g.s_init_alloc[g.rank_struct[L.r]] : 0;
         s.free_t = 0;
         s.cpmax = 0;
+        s.commcum = 0;
+        s.comp_a = 0;
         s.done_cnt = 0;
         s.pop_seq = 0;
 
@@ -806,7 +829,7 @@ __global__ void __launch_bounds__(1024, 1)
         dirty = dead != 0;
         int64_t vals[6] = {0, 0, 0, 0, 0, 0};
         if (active) {
-            const int64_t comm = c.stat[ST_COMM * R + L.r];
+            const int64_t comm = s.commcum;
             vals[0] = c.stat[ST_FIN * R + L.r];
             vals[1] = s.cpmax > cpm ? s.cpmax : cpm;
             vals[2] = c.stat[ST_COMP * R + L.r];

@@ -25,6 +25,7 @@ struct DevGraph {
     const int2 *tens_rng;        // [total_tens] {first, end} into tens_cons
     // static-host folding (engine.cu "t = 0 host pops")
     int fold_ok;
+    int needs_done;              // some tensor's last consumer is only known at run time
     const int32_t *s_nstatic, *trig_off, *static_off, *static_list;
     const int4 *trig;            // {trigger host, node, position in the host's dependents, -}
 };

@@ -139,6 +139,17 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     {
         int rc = upload(g, d->rank_coll_inst, (size_t)R * dg.coll_stride, &dg.rank_coll_inst);
         if (rc) return rc;
+        std::vector<int32_t> full((size_t)(d->n_inst > 0 ? d->n_inst : 1), -1);
+        for (int i = 0; i < d->n_inst; i++) {
+            const int64_t m0 = d->inst_mem_off[i], nm = d->inst_mem_off[i + 1] - m0;
+            if (nm != R) continue;
+            const int node = d->inst_mem_node[m0];
+            bool ok = true;
+            for (int64_t j = 0; j < nm && ok; j++) ok = d->inst_mem_rank[m0 + j] == j && d->inst_mem_node[m0 + j] == node;
+            if (ok) full[i] = node;
+        }
+        rc = upload(g, full.data(), full.size(), &dg.inst_full_node);
+        if (rc) return rc;
     }
 
     // packed node records and tensor consumer ranges (engine.cu node record layout)

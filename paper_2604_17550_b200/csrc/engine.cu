@@ -128,6 +128,8 @@ constexpr uint64_t KINF = ~0ull;
 struct Shared {
     uint64_t red[2][32];
     int64_t redi[2][32];
+    int64_t cend_all;               // every rank's comm stream ends here (valid iff cend_uniform)
+    int cend_uniform;
     int parity;
     int ncomp;
     int flag;
@@ -513,41 +515,73 @@ __device__ __forceinline__ bool comp_before(const DevGraph &g, const Ctx &c, int
 __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, const Ctx &c, Shared &sh, int &par,
                                           int64_t t, bool init, int cfg, uint64_t epoch, int nc) {
     int64_t cpm = 0;
-    if (threadIdx.x == 0) {
-        for (int a = 1; a < nc; a++) {
-            const int x = c.complist[a];
-            int b = a - 1;
-            while (b >= 0 && comp_before(g, c, x, c.complist[b], init)) { c.complist[b + 1] = c.complist[b]; b--; }
-            c.complist[b + 1] = x;
+    if (nc > 1) {
+        if (threadIdx.x == 0) {
+            for (int a = 1; a < nc; a++) {
+                const int x = c.complist[a];
+                int b = a - 1;
+                while (b >= 0 && comp_before(g, c, x, c.complist[b], init)) { c.complist[b + 1] = c.complist[b]; b--; }
+                c.complist[b + 1] = x;
+            }
         }
+        __syncthreads();
     }
-    __syncthreads();
     const int R = c.R;
+    // While every collective so far spanned all ranks, every comm stream ends at the
+    // same time and a full-world reservation needs no reduction (simulator.py:300-303).
+    bool uni = sh.cend_uniform;
+    int64_t cend = sh.cend_all;
     for (int q = 0; q < nc; q++) {
         const int i = c.complist[q];
         const int64_t m0 = g.inst_mem_off[i], nm = g.inst_mem_off[i + 1] - m0;
-        int64_t local = t;
-        for (int64_t j = threadIdx.x; j < nm; j += blockDim.x) {
-            const int64_t ce = c.comm_end[g.inst_mem_rank[m0 + j]];
-            local = ce > local ? ce : local;
+        const int full_node = g.inst_full_node[i];      // >= 0: members are ranks 0..R-1, all at this node
+        int64_t s;
+        if (full_node >= 0 && uni) {
+            s = cend > t ? cend : t;
+        } else {
+            __syncthreads();        // comm ends written by the previous reservation
+            int64_t local = t;
+            for (int64_t j = threadIdx.x; j < nm; j += blockDim.x) {
+                const int64_t ce = c.comm_end[g.inst_mem_rank[m0 + j]];
+                local = ce > local ? ce : local;
+            }
+            s = block_max_i64(local, sh, par);
         }
-        const int64_t s = block_max_i64(local, sh, par);
         const int64_t e = s + c.inst_dur[i];
         const int64_t cpv = c.inst_cpmax[i] + c.inst_dur[i];
         cpm = cpv > cpm ? cpv : cpm;
         if (threadIdx.x == 0) { c.inst_s[i] = s; c.inst_e[i] = e; }
-        for (int64_t j = threadIdx.x; j < nm; j += blockDim.x) {
-            const int m = g.inst_mem_rank[m0 + j], node = g.inst_mem_node[m0 + j];
-            c.comm_end[m] = e;
-            const int slot = c.ring_tail[m]++;
-            c.ring_inst[slot * R + m] = i;
-            c.ring_node[slot * R + m] = node;
-            c.cp[node * R + m] = (int64_t)(epoch | (uint64_t)cpv);
-            record(g, o, cfg, m, node, s, e);
+        if (full_node >= 0) {
+            for (int m = threadIdx.x; m < R; m += blockDim.x) {
+                c.comm_end[m] = e;
+                const int slot = c.ring_tail[m]++;
+                c.ring_inst[slot * R + m] = i;
+                c.ring_node[slot * R + m] = full_node;
+                c.cp[full_node * R + m] = (int64_t)(epoch | (uint64_t)cpv);
+                record(g, o, cfg, m, full_node, s, e);
+            }
+            uni = true;
+            cend = e;
+        } else {
+            for (int64_t j = threadIdx.x; j < nm; j += blockDim.x) {
+                const int m = g.inst_mem_rank[m0 + j], node = g.inst_mem_node[m0 + j];
+                c.comm_end[m] = e;
+                const int slot = c.ring_tail[m]++;
+                c.ring_inst[slot * R + m] = i;
+                c.ring_node[slot * R + m] = node;
+                c.cp[node * R + m] = (int64_t)(epoch | (uint64_t)cpv);
+                record(g, o, cfg, m, node, s, e);
+            }
+            uni = false;
+            __syncthreads();        // the next reservation reads these comm ends
         }
-        __syncthreads();
     }
-    if (threadIdx.x == 0) sh.ncomp = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        sh.ncomp = 0;
+        sh.cend_uniform = uni;
+        sh.cend_all = cend;
+    }
     __syncthreads();
     return cpm;
 }
@@ -666,6 +700,7 @@ __global__ void __launch_bounds__(1024, 1)
         }
         if (dirty) for (size_t i = tid; i < 3 * words; i += bd) gbits[i] = 0;
         if (g.needs_done) for (size_t i = tid; i < words; i += bd) c.done[i] = 0;
+        if (tid == 0) { sh.cend_all = 0; sh.cend_uniform = 1; }
         for (int r = tid; r < R; r += bd) {
             c.comm_end[r] = 0;
             c.ring_tail[r] = 0;

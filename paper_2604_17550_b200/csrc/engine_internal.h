@@ -20,6 +20,7 @@ struct DevGraph {
     const int32_t *inst_n;
     const int64_t *inst_bytes, *inst_lead_id, *inst_init_key, *inst_mem_off;
     const int32_t *inst_mem_rank, *inst_mem_node, *rank_coll_inst;
+    const int32_t *inst_full_node;   // >= 0 when members are ranks 0..R-1 in order, all at this local node
     // derived on upload (capi.cu): packed per-node records and tensor consumer ranges
     const uint4 *node_rec;       // [2 * total_nodes]
     const int2 *tens_rng;        // [total_tens] {first, end} into tens_cons

@@ -55,6 +55,7 @@ enum fl_topo { FL_SWITCH = 0, FL_MESH2D = 1 };
 /* Engine limits of this build. */
 #define FL_MAX_NODES_PER_RANK 4096   /* 64 bitmap words x 64 bits        */
 #define FL_MAX_RANKS 1024            /* one thread per rank, one CTA per design point */
+#define FL_MAX_P2P_PER_RANK 4096     /* SEND+RECV nodes per rank graph */
 
 /*
  * A compiled graph set.  Ranks are dense 0..R-1 in ascending rank-value
@@ -107,6 +108,16 @@ typedef struct {
     const int32_t *inst_mem_node;     /* member node (local index in that rank's structure) */
     int32_t coll_stride;              /* max collectives per rank (row stride below) */
     const int32_t *rank_coll_inst;    /* [R*coll_stride] instance of rank r's k-th COLL */
+
+    /* point-to-point messages (EXPANDED comm mode), matched as simulator.py:177-200 */
+    const int64_t *rank_value;        /* [R] the graphs' rank ids (routing, ordering keys) */
+    int32_t n_msg;
+    const int32_t *msg_send_rank, *msg_send_node;   /* [M] rank index, local node */
+    const int32_t *msg_recv_rank, *msg_recv_node;
+    const int64_t *msg_bytes;         /* [M] */
+    const int64_t *msg_send_id;       /* [M] node_id of the SEND (order key, simulator.py:311) */
+    int32_t p2p_stride;               /* max SEND+RECV per rank */
+    const int32_t *rank_p2p_msg;      /* [R*p2p_stride] message of rank r's k-th SEND/RECV */
 } fl_graph_desc;
 
 /* Design points, structure of arrays, one entry per point. */
@@ -129,6 +140,8 @@ typedef struct {
     int64_t *rows;                    /* [n*6] */
     int64_t *rank_stats;              /* optional [n*R*5]: finish, compute, comm, exposed, peak */
     int64_t *ev_start, *ev_end;       /* optional [n*R*max_nodes] (record_events) */
+    int64_t *link_busy;               /* optional [n*link_cap]; -1 = link never used (SimReport.link_busy_ns) */
+    int32_t link_cap;                 /* links per point in link_busy: switch 2*R (eg/in per rank), mesh 4*rows*cols */
 } fl_outputs;
 
 typedef struct fl_graph fl_graph;
@@ -149,6 +162,17 @@ int fl_sweep_run(fl_graph *g, const fl_points *host_points, fl_outputs *host_out
  * NULL = legacy default).  *launches receives the number of kernels enqueued. */
 int fl_sweep_run_device(fl_graph *g, const fl_points *dev_points, fl_outputs *dev_out,
                         void *stream, int32_t *launches);
+
+/* Contention-free critical path alone (simulator.py:400-460) for host design
+ * points, over the merged multi-rank graph given as vertices in topological
+ * order (vkind 0: rank va's node vb; 1: collective instance va; RECVs carry
+ * their SEND's vertex in vsend and the message in vmsg) with predecessor CSR.
+ * fl_sweep_run computes the same value as a by-product of the simulation; this
+ * entry point serves critical_path() when the simulation itself deadlocks. */
+int fl_critical_path(fl_graph *g, const fl_points *host_points, int32_t n_vert, const int32_t *order,
+                     const int32_t *vkind, const int32_t *va, const int32_t *vb, const int32_t *vsend,
+                     const int32_t *vmsg, const int32_t *pred_off, const int32_t *pred_idx,
+                     int64_t *out_cp, int32_t *out_status);
 
 /* Cost stage alone (K1 parity hook): alpha-beta time of n collectives and
  * flops->ns of m compute nodes, evaluated by the device code path. Host buffers. */

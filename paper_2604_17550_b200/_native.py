@@ -73,6 +73,9 @@ class GraphDesc(C.Structure):
         ("inst_lead_id", P64), ("inst_init_key", P64), ("inst_mem_off", P64),
         ("inst_mem_rank", P32), ("inst_mem_node", P32),
         ("coll_stride", C.c_int32), ("rank_coll_inst", P32),
+        ("rank_value", P64), ("n_msg", C.c_int32), ("msg_send_rank", P32), ("msg_send_node", P32),
+        ("msg_recv_rank", P32), ("msg_recv_node", P32), ("msg_bytes", P64), ("msg_send_id", P64),
+        ("p2p_stride", C.c_int32), ("rank_p2p_msg", P32),
     ]
 
 
@@ -86,7 +89,7 @@ class Points(C.Structure):
 
 class Outputs(C.Structure):
     _fields_ = [("status", P32), ("rows", P64), ("rank_stats", P64),
-                ("ev_start", P64), ("ev_end", P64)]
+                ("ev_start", P64), ("ev_end", P64), ("link_busy", P64), ("link_cap", C.c_int32)]
 
 
 _lib = None
@@ -112,6 +115,8 @@ def lib():
     L.fl_graph_max_nodes.restype = C.c_int32
     L.fl_sweep_run.argtypes = [C.c_void_p, C.POINTER(Points), C.POINTER(Outputs)]
     L.fl_sweep_run_device.argtypes = [C.c_void_p, C.POINTER(Points), C.POINTER(Outputs), C.c_void_p, P32]
+    L.fl_critical_path.argtypes = [C.c_void_p, C.POINTER(Points), C.c_int32, P32, P32, P32, P32, P32, P32, P32,
+                                   P32, P64, P32]
     L.fl_cost_only.argtypes = [C.c_int32, PU8, P64, P64, PU8, PF64, PF64, P32, P32, P64, P32,
                                C.c_int32, P64, PF64, PF64, P64]
     _lib = L
@@ -123,4 +128,4 @@ def last_error() -> str:
 
 
 EXPORTED = ["fl_version", "fl_last_error", "fl_device_count", "fl_graph_create", "fl_graph_destroy",
-            "fl_graph_max_nodes", "fl_sweep_run", "fl_sweep_run_device", "fl_cost_only"]
+            "fl_graph_max_nodes", "fl_sweep_run", "fl_sweep_run_device", "fl_critical_path", "fl_cost_only"]

@@ -9,6 +9,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -88,8 +89,6 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     const int total = d->s_node_off[S], total_t = d->s_tens_off[S];
     for (int i = 0; i < total; i++) {
         int k = d->node_kind[i];
-        if (k == FL_SEND || k == FL_RECV)
-            return fail(FL_ERR_CAPACITY, "SEND/RECV (expanded comm mode) is not supported by this build");
         if (k > FL_RECV) return fail(FL_ERR_INVALID, "bad node kind");
         if (d->succ_off[i + 1] - d->succ_off[i] >= 4096) return fail(FL_ERR_CAPACITY, "node fan-out >= 4096");
     }
@@ -136,6 +135,20 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     UP(inst_mem_off, d->n_inst + 1);
     UP(inst_mem_rank, ne_mem);
     UP(inst_mem_node, ne_mem);
+    if (d->n_msg < 0 || d->p2p_stride > FL_MAX_P2P_PER_RANK) return fail(FL_ERR_CAPACITY, "too many SEND/RECV nodes per rank");
+    dg.n_msg = d->n_msg;
+    dg.p2p_stride = d->p2p_stride > 0 ? d->p2p_stride : 1;
+    UP(rank_value, R);
+    UP(msg_send_rank, d->n_msg);
+    UP(msg_send_node, d->n_msg);
+    UP(msg_recv_rank, d->n_msg);
+    UP(msg_recv_node, d->n_msg);
+    UP(msg_bytes, d->n_msg);
+    UP(msg_send_id, d->n_msg);
+    {
+        int rc = upload(g, d->rank_p2p_msg, (size_t)R * dg.p2p_stride, &dg.rank_p2p_msg);
+        if (rc) return rc;
+    }
     {
         int rc = upload(g, d->rank_coll_inst, (size_t)R * dg.coll_stride, &dg.rank_coll_inst);
         if (rc) return rc;
@@ -296,6 +309,13 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     sc.off_ring = off; off = align_up(off + 2 * (size_t)dg.coll_stride * R * 4, 256);
     sc.off_dur = off;  off = align_up(off + dur_bytes, 256);
     sc.off_inst = off; off = align_up(off + inst_bytes, 256);
+    // links: switch eg/in per rank; mesh 4 per position (bounded by the largest rank id)
+    int64_t maxv = 0;
+    for (int r = 0; r < R; r++) maxv = d->rank_value[r] > maxv ? d->rank_value[r] : maxv;
+    sc.link_cap = d->n_msg > 0 ? (int)std::max<int64_t>(2 * (int64_t)R, 8 * (maxv + 1)) : 0;
+    sc.off_msg = off;
+    off = align_up(off + (size_t)d->n_msg * 8 * 8 + (size_t)sc.link_cap * 16 + (size_t)d->n_msg * 8 +
+                       (size_t)R * 4 + 2 * (size_t)dg.p2p_stride * R * 4 + 64, 256);
     sc.slot_bytes = off;
 
     // shared memory: header | comm_end, stats, ring tails | [instances] | [durations] | [done bitmap]
@@ -355,6 +375,8 @@ int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stre
     dout.rank_stats = out->rank_stats;
     dout.ev_start = out->ev_start;
     dout.ev_end = out->ev_end;
+    dout.link_busy = out->link_busy;
+    dout.link_cap = out->link_cap;
     CK(fl::launch_sweep(cs == 3 ? 4 : cs, grid, g->block, g->smem, stream, g->dg, dp, dout, g->sc));
     return FL_OK;
 }
@@ -443,6 +465,8 @@ int fl_sweep_run(fl_graph *g, const fl_points *hp, fl_outputs *ho) {
     const size_t o_rs = off; off = align_up(off + (ho->rank_stats ? 40 * n * R : 0), 256);
     const size_t o_es = off; off = align_up(off + (ho->ev_start ? 8 * n * R * MN : 0), 256);
     const size_t o_ee = off; off = align_up(off + (ho->ev_start ? 8 * n * R * MN : 0), 256);
+    const size_t LC = ho->link_busy ? (size_t)(ho->link_cap > 0 ? ho->link_cap : 0) : 0;
+    const size_t o_lb = off; off = align_up(off + 8 * n * LC, 256);
     if (off > g->stage_bytes) {
         if (g->stage) cudaFree(g->stage);
         g->stage = nullptr;
@@ -468,17 +492,61 @@ int fl_sweep_run(fl_graph *g, const fl_points *hp, fl_outputs *ho) {
     dout.rank_stats = ho->rank_stats ? reinterpret_cast<int64_t *>(S + o_rs) : nullptr;
     dout.ev_start = ho->ev_start ? reinterpret_cast<int64_t *>(S + o_es) : nullptr;
     dout.ev_end = ho->ev_start ? reinterpret_cast<int64_t *>(S + o_ee) : nullptr;
+    dout.link_busy = LC ? reinterpret_cast<int64_t *>(S + o_lb) : nullptr;
+    dout.link_cap = (int32_t)LC;
     int rc = launch(g, &dp, &dout, 0);
     if (rc) return rc;
     CK(cudaMemcpyAsync(ho->status, dout.status, 4 * n, cudaMemcpyDeviceToHost, 0));
     CK(cudaMemcpyAsync(ho->rows, dout.rows, 48 * n, cudaMemcpyDeviceToHost, 0));
     if (ho->rank_stats) CK(cudaMemcpyAsync(ho->rank_stats, dout.rank_stats, 40 * n * R, cudaMemcpyDeviceToHost, 0));
+    if (LC) CK(cudaMemcpyAsync(ho->link_busy, dout.link_busy, 8 * n * LC, cudaMemcpyDeviceToHost, 0));
     if (ho->ev_start) {
         CK(cudaMemcpyAsync(ho->ev_start, dout.ev_start, 8 * n * R * MN, cudaMemcpyDeviceToHost, 0));
         CK(cudaMemcpyAsync(ho->ev_end, dout.ev_end, 8 * n * R * MN, cudaMemcpyDeviceToHost, 0));
     }
     cudaError_t e = cudaStreamSynchronize(0);
     if (e != cudaSuccess) return fail(FL_ERR_CUDA, std::string("engine kernel: ") + cudaGetErrorString(e));
+    return FL_OK;
+}
+
+int fl_critical_path(fl_graph *g, const fl_points *hp, int32_t nv, const int32_t *order, const int32_t *vkind,
+                     const int32_t *va, const int32_t *vb, const int32_t *vsend, const int32_t *vmsg,
+                     const int32_t *pred_off, const int32_t *pred_idx, int64_t *out_cp, int32_t *out_status) {
+    if (!g || !hp || nv < 0) return fail(FL_ERR_INVALID, "bad argument");
+    CK(cudaSetDevice(g->device));
+    const size_t n = (size_t)hp->n_points;
+    if (n == 0) return FL_OK;
+    std::vector<void *> tmp;
+    uint8_t *algo, *topo;
+    double *bw, *peak = nullptr, *eff = nullptr;
+    int64_t *lat, *vals, *dout;
+    int32_t *rows, *cols, *dst, *dorder, *dk, *da, *db, *ds, *dm, *dpo, *dpi;
+    int rc;
+    const size_t V = (size_t)(nv > 0 ? nv : 1), E = (size_t)(pred_off ? pred_off[nv] : 0);
+    if ((rc = to_dev(hp->algo, n, &algo, tmp)) || (rc = to_dev(hp->topo_kind, n, &topo, tmp)) ||
+        (rc = to_dev(hp->bw, n, &bw, tmp)) || (rc = to_dev(hp->latency, n, &lat, tmp)) ||
+        (rc = to_dev(hp->rows, n, &rows, tmp)) || (rc = to_dev(hp->cols, n, &cols, tmp)) ||
+        (rc = to_dev(hp->peak_flops, n, &peak, tmp)) || (rc = to_dev(hp->efficiency, n, &eff, tmp)) ||
+        (rc = to_dev(order, V, &dorder, tmp)) || (rc = to_dev(vkind, V, &dk, tmp)) || (rc = to_dev(va, V, &da, tmp)) ||
+        (rc = to_dev(vb, V, &db, tmp)) || (rc = to_dev(vsend, V, &ds, tmp)) || (rc = to_dev(vmsg, V, &dm, tmp)) ||
+        (rc = to_dev(pred_off, V + 1, &dpo, tmp)) || (rc = to_dev(pred_idx, E ? E : 1, &dpi, tmp)) ||
+        (rc = to_dev(out_cp, n, &dout, tmp)) || (rc = to_dev(out_status, n, &dst, tmp))) {
+        free_all(tmp);
+        return rc;
+    }
+    void *pv = nullptr;
+    if (cudaMalloc(&pv, n * V * 8) != cudaSuccess) { free_all(tmp); return fail(FL_ERR_CUDA, "cp scratch"); }
+    tmp.push_back(pv);
+    vals = static_cast<int64_t *>(pv);
+    fl::DevPoints dp;
+    dp.n = (int)n; dp.algo = algo; dp.topo_kind = topo; dp.bw = bw; dp.latency = lat; dp.rows = rows;
+    dp.cols = cols; dp.peak_flops = peak; dp.efficiency = eff; dp.compute_streams = 1;
+    cudaError_t e = fl::launch_cp(g->dg, dp, nv, dorder, dk, da, db, ds, dm, dpo, dpi, vals, dout, dst);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(out_cp, dout, n * 8, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(out_status, dst, n * 4, cudaMemcpyDeviceToHost);
+    free_all(tmp);
+    if (e != cudaSuccess) return fail(FL_ERR_CUDA, cudaGetErrorString(e));
     return FL_OK;
 }
 

@@ -132,6 +132,7 @@ struct Shared {
     int cend_uniform;
     int parity;
     int ncomp;
+    int nmcomp;
     int flag;
 };
 
@@ -217,7 +218,19 @@ struct Ctx {
     int32_t *ring_tail;             // shared [R]
     int *ncomp;                     // shared
     int64_t *stat;                  // shared [ST_N][R]
+    // point-to-point messages (expanded comm mode), simulator.py:177-200, :310-327
+    int64_t *msg_sendt, *msg_recvt, *msg_cps_s, *msg_cps_r, *msg_s, *msg_e, *msg_xfer;
+    unsigned long long *msg_ckey;
+    int32_t *msg_wait, *mcomplist;
+    int *nmcomp;                    // shared: messages completed in this step
+    int64_t *link_free, *link_busy; // [link_cap]
+    int link_cap;
+    int32_t *mlist;                 // [p2p_stride][R] per-rank in-flight messages (id | MSG_ALLOC), by end time
+    int32_t *mlist_node;            // [p2p_stride][R] this rank's endpoint node of that message
+    int32_t *mcount;                // shared [R]
 };
+
+constexpr int32_t MSG_ALLOC = 1 << 30;   // mlist entry flag: the endpoint's outputs are allocated
 
 // Per-thread rank identity: element w of rank r in a [w][R] array is at w * R + r.
 struct Lane {
@@ -237,13 +250,13 @@ template <int K>
 struct Rank {
     MinSet due, rc, rh;             // due events at t / ready compute nodes / ready host nodes
     int64_t host_slot, host_e;
-    int64_t slot[K], occ_e[K];
+    int64_t slot[K & 7], occ_e[K & 7];
     int64_t head_s, head_e;         // comm-FIFO head (valid iff ring_head < ring_seen)
     int64_t alloc_t, free_t, cpmax;
     int64_t commcum;                // integral of "comm stream busy" up to the current step (= comm busy)
     int64_t comp_a;                 // commcum when the running compute node started (K == 1)
     int host_n;
-    int occ_n[K];
+    int occ_n[K & 7];
     int head_node, head_alloc;
     int ring_head, ring_seen;
     int done_cnt, pop_seq;
@@ -325,21 +338,21 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
     while (s.rc.head >= 0) {
         int k = 0;
 #pragma unroll
-        for (int q = 1; q < K; q++) if (s.slot[q] < s.slot[k]) k = q;
+        for (int q = 1; q < (K & 7); q++) if (s.slot[q] < s.slot[k]) k = q;
         int64_t sk = s.slot[0];
 #pragma unroll
-        for (int q = 1; q < K; q++) if (q == k) sk = s.slot[q];
+        for (int q = 1; q < (K & 7); q++) if (q == k) sk = s.slot[q];
         if (sk > t) break;
         const int x = ms_pop(s.rc, c.rdyc, R, L.r);
         const int64_t e = t + c.dur[L.nb + x];
         { const uint4 xb = rec_b(g, L.nb + x); s.alloc_t += rec_u64(xb.z, xb.w); }
         record(g, o, cfg, L.r, x, t, e);
-        if (K == 1 && e > t) {      // one compute stream: its busy intervals are disjoint
+        if ((K & 7) == 1 && e > t) {      // one compute stream: its busy intervals are disjoint
             c.stat[ST_COMP * R + L.r] += e - t;
             s.comp_a = s.commcum;
         }
 #pragma unroll
-        for (int q = 0; q < K; q++) {
+        for (int q = 0; q < (K & 7); q++) {
             if (q == k) {
                 s.slot[q] = e;
                 if (e == t) ms_insert(s.due, c.due, R, L.r, x);
@@ -353,9 +366,21 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
 // is its contention-free critical-path start (simulator.py:449).
 template <int K>
 __device__ __forceinline__ void dispatch(const DevGraph &g, const Ctx &c, const Lane &L, Rank<K> &s,
-                                         const Step &f, int d, const uint4 &rb, int64_t cps, int seq) {
+                                         const Step &f, int d, const uint4 &rb, int64_t cps, int seq, int64_t t) {
     const int R = c.R;
     const int kind = rec_kind(rb);
+    if ((K & 8) && kind >= FL_SEND) {   // simulator.py:259-268: the message is granted once both ends are ready
+        const int m = g.rank_p2p_msg[L.r * g.p2p_stride + (int)rb.y];
+        if (kind == FL_SEND) { c.msg_sendt[m] = t; c.msg_cps_s[m] = cps; }
+        else { c.msg_recvt[m] = t; c.msg_cps_r[m] = cps; }
+        if (f.step) {
+            const unsigned long long key = ((unsigned long long)f.step << 39) | ((unsigned long long)L.r << 25) |
+                                           ((unsigned long long)s.pop_seq << 12) | (unsigned long long)seq;
+            atomicMax(&c.msg_ckey[m], key);
+        }
+        if (atomicSub(&c.msg_wait[m], 1) == 1) c.mcomplist[atomicAdd(c.nmcomp, 1)] = m;
+        return;
+    }
     if (kind == FL_COLL) {
         const int i = g.rank_coll_inst[L.r * g.coll_stride + (int)rb.y];
         atomicMax((unsigned long long *)&c.inst_cpmax[i], (unsigned long long)cps);
@@ -404,7 +429,7 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
         if ((a >> 58) != (f.epoch >> 58)) a = f.epoch | (rec_indeg(db, f.fold) << 48);
         const uint64_t v = (a & VAL48) > fx ? (a & VAL48) : fx;
         const uint64_t left = ((a >> 48) & 0x3ff) - 1;
-        if (left == 0) dispatch(g, c, L, s, f, d, db, (int64_t)v, seq);
+        if (left == 0) dispatch(g, c, L, s, f, d, db, (int64_t)v, seq, t);
         else *slot = (int64_t)(f.epoch | (left << 48) | v);
     }
 }
@@ -432,12 +457,17 @@ __device__ __forceinline__ void refresh_ring(const Ctx &c, const Lane &L, Rank<K
 }
 
 template <int K>
-__device__ __forceinline__ int64_t next_time(const Rank<K> &s, int64_t tcur) {
+__device__ __forceinline__ int64_t next_time(const DevGraph &g, const Ctx &c, const Lane &L, const Rank<K> &s,
+                                             int64_t tcur) {
     if (s.due.head >= 0) return tcur;
     int64_t nt = s.host_n >= 0 ? s.host_e : TINF;
 #pragma unroll
-    for (int q = 0; q < K; q++) if (s.occ_n[q] >= 0 && s.occ_e[q] < nt) nt = s.occ_e[q];
+    for (int q = 0; q < (K & 7); q++) if (s.occ_n[q] >= 0 && s.occ_e[q] < nt) nt = s.occ_e[q];
     if (s.ring_head < s.ring_seen && s.head_e < nt) nt = s.head_e;
+    if ((K & 8) && c.mcount[L.r] > 0) {          // in-flight messages, sorted by end time
+        const int64_t e = c.msg_e[c.mlist[L.r] & ~MSG_ALLOC];
+        nt = e < nt ? e : nt;
+    }
     return nt;
 }
 
@@ -448,17 +478,34 @@ __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, cons
     const int R = c.R;
     if (s.host_n >= 0 && s.host_e == t) { ms_insert(s.due, c.due, R, L.r, s.host_n); s.host_n = -1; }
 #pragma unroll
-    for (int q = 0; q < K; q++)
+    for (int q = 0; q < (K & 7); q++)
         if (s.occ_n[q] >= 0 && s.occ_e[q] == t) {
             ms_insert(s.due, c.due, R, L.r, s.occ_n[q]);
             s.occ_n[q] = -1;
-            if (K == 1) c.stat[ST_OVL * R + L.r] += s.commcum - s.comp_a;   // comm time under [start, t)
+            if ((K & 7) == 1) c.stat[ST_OVL * R + L.r] += s.commcum - s.comp_a;   // comm time under [start, t)
         }
     while (s.ring_head < s.ring_seen && s.head_e == t) {
         if (!s.head_alloc) { const uint4 hb = rec_b(g, L.nb + s.head_node); s.alloc_t += rec_u64(hb.z, hb.w); }  // zero-length: starts now
         ms_insert(s.due, c.due, R, L.r, s.head_node);
         s.ring_head++;
         load_head(c, L, s);
+    }
+    if (K & 8) {
+        int n = c.mcount[L.r], k = 0;
+        for (; k < n; k++) {
+            const int ent = c.mlist[k * R + L.r];
+            if (c.msg_e[ent & ~MSG_ALLOC] != t) break;
+            const int node = c.mlist_node[k * R + L.r];
+            if (!(ent & MSG_ALLOC)) { const uint4 hb = rec_b(g, L.nb + node); s.alloc_t += rec_u64(hb.z, hb.w); }
+            ms_insert(s.due, c.due, R, L.r, node);
+        }
+        if (k) {
+            for (int q = k; q < n; q++) {
+                c.mlist[(q - k) * R + L.r] = c.mlist[q * R + L.r];
+                c.mlist_node[(q - k) * R + L.r] = c.mlist_node[q * R + L.r];
+            }
+            c.mcount[L.r] = n - k;
+        }
     }
 }
 
@@ -474,6 +521,21 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
         s.alloc_t += rec_u64(hb.z, hb.w);
         s.head_alloc = 1;
     }
+    bool msg_on = false;            // a message of this rank is on the wire during [tcur, tnew)
+    if (K & 8) {
+        const int n = c.mcount[L.r];
+        for (int k = 0; k < n; k++) {
+            const int ent = c.mlist[k * R + L.r];
+            if (c.msg_s[ent & ~MSG_ALLOC] <= tcur) {
+                msg_on = true;
+                if (!(ent & MSG_ALLOC)) {
+                    const uint4 hb = rec_b(g, L.nb + c.mlist_node[k * R + L.r]);
+                    s.alloc_t += rec_u64(hb.z, hb.w);
+                    c.mlist[k * R + L.r] = ent | MSG_ALLOC;
+                }
+            }
+        }
+    }
     if (s.alloc_t | s.free_t) {
         int64_t cur = c.stat[ST_CUR * R + L.r] + s.alloc_t;
         const int64_t pk = c.stat[ST_PEAK * R + L.r];
@@ -483,12 +545,12 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
     }
     if (tnew == TINF) return;
     const int64_t dt = tnew - tcur;
-    const bool comm_on = head && s.head_s <= tcur;
+    const bool comm_on = (head && s.head_s <= tcur) || msg_on;
     if (comm_on) s.commcum += dt;
-    if (K > 1) {                    // overlapping compute streams: integrate the union
+    if ((K & 7) > 1) {              // overlapping compute streams: integrate the union
         bool comp_on = false;
 #pragma unroll
-        for (int q = 0; q < K; q++) comp_on |= s.occ_n[q] >= 0;
+        for (int q = 0; q < (K & 7); q++) comp_on |= s.occ_n[q] >= 0;
         if (comp_on) {
             c.stat[ST_COMP * R + L.r] += dt;
             if (comm_on) c.stat[ST_OVL * R + L.r] += dt;
@@ -509,11 +571,99 @@ __device__ __forceinline__ bool comp_before(const DevGraph &g, const Ctx &c, int
     return (c.inst_ckey[a] & 0xfff) < (c.inst_ckey[b] & 0xfff);
 }
 
+__device__ __forceinline__ bool msg_before(const DevGraph &g, const Ctx &c, int a, int b, bool init) {
+    // simulator.py:311: (max(send_t, recv_t), src rank, src node id) within one pop
+    if (!init) {
+        const unsigned long long ka = c.msg_ckey[a] >> 12, kb = c.msg_ckey[b] >> 12;
+        if (ka != kb) return ka < kb;
+    }
+    const int64_t ra = g.rank_value[g.msg_send_rank[a]], rb = g.rank_value[g.msg_send_rank[b]];
+    if (ra != rb) return ra < rb;
+    return g.msg_send_id[a] < g.msg_send_id[b];
+}
+
+// Visit the directed links of a src->dst message in route order
+// (topology.py:68-86); ids: switch eg/in of rank index i -> 2i / 2i+1,
+// mesh a -> neighbour: 4a + {+col, -col, +row, -row}.
+template <typename F>
+__device__ __forceinline__ void for_route(const DevGraph &g, int topo, int cols, int si, int di, F &&fn) {
+    if (si == di) return;
+    if (topo == FL_SWITCH) { fn(2 * si); fn(2 * di + 1); return; }
+    const int64_t src = g.rank_value[si], dst = g.rank_value[di];
+    int r = (int)(src / cols), cc = (int)(src % cols);
+    const int r1 = (int)(dst / cols), c1 = (int)(dst % cols);
+    while (cc != c1) { fn(4 * (r * cols + cc) + (c1 > cc ? 0 : 1)); cc += c1 > cc ? 1 : -1; }
+    while (r != r1) { fn(4 * (r * cols + cc) + (r1 > r ? 2 : 3)); r += r1 > r ? 1 : -1; }
+}
+
+// topology.py:95-102: per-hop latency plus one serialization, integer ns.
+__device__ __forceinline__ int64_t transfer_ns(const DevGraph &g, int topo, int cols, int si, int di, int64_t bytes,
+                                               int64_t lat, double beta) {
+    if (si == di) return 0;
+    int64_t hops = 1;
+    if (topo == FL_MESH2D) {
+        const int64_t src = g.rank_value[si], dst = g.rank_value[di];
+        const int64_t dr = src / cols - dst / cols, dc = src % cols - dst % cols;
+        hops = (dr < 0 ? -dr : dr) + (dc < 0 ? -dc : dc);
+    }
+    return rhu(__dadd_rn((double)(hops * lat), __dmul_rn((double)bytes, beta)));
+}
+
+// Message phase (simulator.py:310-327), one thread: FIFO per link, a message holds
+// every link on its route for the whole transfer.
+__device__ void reserve_msgs(const DevGraph &g, const DevOut &o, const Ctx &c, int nm, bool init, int topo,
+                             int cols, int cfg, uint64_t epoch, int64_t &cpm) {
+    const int R = c.R;
+    for (int a = 1; a < nm; a++) {
+        const int x = c.mcomplist[a];
+        int b = a - 1;
+        while (b >= 0 && msg_before(g, c, x, c.mcomplist[b], init)) { c.mcomplist[b + 1] = c.mcomplist[b]; b--; }
+        c.mcomplist[b + 1] = x;
+    }
+    for (int q = 0; q < nm; q++) {
+        const int m = c.mcomplist[q];
+        const int si = g.msg_send_rank[m], di = g.msg_recv_rank[m];
+        int64_t st = c.msg_sendt[m] > c.msg_recvt[m] ? c.msg_sendt[m] : c.msg_recvt[m];
+        for_route(g, topo, cols, si, di, [&](int l) { st = c.link_free[l] > st ? c.link_free[l] : st; });
+        const int64_t xf = c.msg_xfer[m], e = st + xf;
+        for_route(g, topo, cols, si, di, [&](int l) {
+            c.link_free[l] = e;
+            const int64_t b0 = c.link_busy[l];
+            c.link_busy[l] = (b0 < 0 ? 0 : b0) + (e - st);
+        });
+        c.msg_s[m] = st;
+        c.msg_e[m] = e;
+        // critical path: a RECV also waits for its SEND plus the wire (simulator.py:430-435, :450-452)
+        const int64_t cs = c.msg_cps_s[m];
+        const int64_t cr = c.msg_cps_r[m] > cs + xf ? c.msg_cps_r[m] : cs + xf;
+        cpm = cr > cpm ? cr : cpm;
+        cpm = cs > cpm ? cs : cpm;
+        const int sn = g.msg_send_node[m], dn = g.msg_recv_node[m];
+        c.cp[sn * R + si] = (int64_t)(epoch | (uint64_t)cs);
+        c.cp[dn * R + di] = (int64_t)(epoch | (uint64_t)cr);
+        record(g, o, cfg, si, sn, st, e);
+        record(g, o, cfg, di, dn, st, e);
+        for (int side = 0; side < 2; side++) {     // both endpoints' in-flight lists, ordered by end
+            const int rr = side ? di : si, node = side ? dn : sn;
+            int k = c.mcount[rr];
+            while (k > 0 && c.msg_e[c.mlist[(k - 1) * R + rr] & ~MSG_ALLOC] > e) {
+                c.mlist[k * R + rr] = c.mlist[(k - 1) * R + rr];
+                c.mlist_node[k * R + rr] = c.mlist_node[(k - 1) * R + rr];
+                k--;
+            }
+            c.mlist[k * R + rr] = m;
+            c.mlist_node[k * R + rr] = node;
+            c.mcount[rr]++;
+        }
+    }
+}
+
 // Reserve the comm streams of every instance completed in this step, in the
 // reference's order (simulator.py:298-309); block-wide.  Returns the largest
 // critical-path finish among them.
+template <bool MSG>
 __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, const Ctx &c, Shared &sh, int &par,
-                                          int64_t t, bool init, int cfg, uint64_t epoch, int nc) {
+                                          int64_t t, bool init, int cfg, uint64_t epoch, int nc, int topo, int cols) {
     int64_t cpm = 0;
     if (nc > 1) {
         if (threadIdx.x == 0) {
@@ -581,17 +731,22 @@ __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, co
         sh.ncomp = 0;
         sh.cend_uniform = uni;
         sh.cend_all = cend;
+        if (MSG && sh.nmcomp) {
+            reserve_msgs(g, o, c, sh.nmcomp, init, topo, cols, cfg, epoch, cpm);
+            sh.nmcomp = 0;
+        }
     }
     __syncthreads();
     return cpm;
 }
 
 // Barrier, then reserve whatever completed since the last reservation.
+template <bool MSG>
 __device__ __forceinline__ int64_t reserve(const DevGraph &g, const DevOut &o, const Ctx &c, Shared &sh, int &par,
-                                           int64_t t, bool init, int cfg, uint64_t epoch) {
+                                           int64_t t, bool init, int cfg, uint64_t epoch, int topo, int cols) {
     __syncthreads();
     const int nc = sh.ncomp;
-    return nc ? reserve_n(g, o, c, sh, par, t, init, cfg, epoch, nc) : 0;
+    return (nc | (MSG ? sh.nmcomp : 0)) ? reserve_n<MSG>(g, o, c, sh, par, t, init, cfg, epoch, nc, topo, cols) : 0;
 }
 
 template <int K>
@@ -636,6 +791,25 @@ __global__ void __launch_bounds__(1024, 1)
         c.inst_wait = reinterpret_cast<int32_t *>(c.inst_ckey + NI);
         c.complist = c.inst_wait + NI;
         c.ncomp = &sh.ncomp;
+        c.nmcomp = &sh.nmcomp;
+        const int M = g.n_msg;
+        int64_t *mb = reinterpret_cast<int64_t *>(base + sc.off_msg);
+        c.msg_sendt = mb;
+        c.msg_recvt = mb + M;
+        c.msg_cps_s = mb + 2 * M;
+        c.msg_cps_r = mb + 3 * M;
+        c.msg_s = mb + 4 * M;
+        c.msg_e = mb + 5 * M;
+        c.msg_xfer = mb + 6 * M;
+        c.msg_ckey = reinterpret_cast<unsigned long long *>(mb + 7 * M);
+        c.link_free = mb + 8 * M;
+        c.link_busy = c.link_free + sc.link_cap;
+        c.link_cap = sc.link_cap;
+        c.msg_wait = reinterpret_cast<int32_t *>(c.link_busy + sc.link_cap);
+        c.mcomplist = c.msg_wait + M;
+        c.mcount = c.mcomplist + M;
+        c.mlist = c.mcount + R;
+        c.mlist_node = c.mlist + (size_t)g.p2p_stride * R;
     }
     __syncthreads();
     uint64_t *gbits = c.rdyc;
@@ -653,7 +827,7 @@ __global__ void __launch_bounds__(1024, 1)
     const int my_n = active ? g.s_node_off[g.rank_struct[L.r] + 1] - L.nb : 0;
 
     int par = 0;
-    if (tid == 0) { sh.parity = 0; sh.ncomp = 0; sh.flag = 0; }
+    if (tid == 0) { sh.parity = 0; sh.ncomp = 0; sh.nmcomp = 0; sh.flag = 0; }
     // the three global bitmaps are all-zero after a point that ran to completion;
     // clear them once up front and again only after a point that did not
     for (size_t i = tid; i < (sc.done_in_smem ? 3 : 4) * words; i += bd) gbits[i] = 0;
@@ -670,7 +844,7 @@ __global__ void __launch_bounds__(1024, 1)
         const int algo = p.algo[cfg], topo = p.topo_kind[cfg];
         const double bwv = p.bw[cfg];
         const int64_t lat = p.latency[cfg];
-        int bad = 0, zero = 0;
+        int bad = 0, zero = 0, cap_bad = 0;
         for (int i = tid; i < NI; i += bd) {
             int64_t d = coll_time(g, i, algo, topo, bwv, lat, p.rows[cfg], p.cols[cfg]);
             if (d < 0) { bad = 1; d = 0; }
@@ -681,6 +855,21 @@ __global__ void __launch_bounds__(1024, 1)
             c.inst_wait[i] = (int32_t)(g.inst_mem_off[i + 1] - g.inst_mem_off[i]);
             c.inst_s[i] = 0;
             c.inst_e[i] = 0;
+        }
+        if (K & 8) {                // messages: wire time per design point, fresh link state
+            const double beta = __ddiv_rn(1e9, bwv);
+            const int cols = p.cols[cfg];
+            if (topo == FL_MESH2D && (cols <= 0 || 4LL * p.rows[cfg] * cols > c.link_cap)) cap_bad = 1;
+            for (int m = tid; m < g.n_msg; m += bd) {
+                const int64_t xf = cap_bad ? 0 : transfer_ns(g, topo, cols, g.msg_send_rank[m], g.msg_recv_rank[m],
+                                                         g.msg_bytes[m], lat, beta);
+                zero |= xf == 0;
+                c.msg_xfer[m] = xf;
+                c.msg_wait[m] = 2;
+                c.msg_ckey[m] = 0ull;
+            }
+            for (int l = tid; l < c.link_cap; l += bd) { c.link_free[l] = 0; c.link_busy[l] = -1; }
+            for (int r = tid; r < R; r += bd) c.mcount[r] = 0;
         }
         const bool recost = p.peak_flops != nullptr;
         const double pk = recost ? p.peak_flops[cfg] : 0.0, ef = recost ? p.efficiency[cfg] : 0.0;
@@ -708,11 +897,13 @@ __global__ void __launch_bounds__(1024, 1)
             for (int k = 0; k < ST_N; k++) c.stat[k * R + r] = 0;
         }
         bad = __syncthreads_or(bad);
+        cap_bad = __syncthreads_or(cap_bad);
+        if (cap_bad) bad = 2;
         zero = __syncthreads_or(zero);
         zdur = __syncthreads_or(zdur);
         dev_zdur = zdur;
         if (bad) {
-            if (tid == 0) o.status[cfg] = FL_ERR_UNSUPPORTED_ALGO;
+            if (tid == 0) o.status[cfg] = bad == 2 ? FL_ERR_CAPACITY : FL_ERR_UNSUPPORTED_ALGO;
             dirty = false;
             continue;
         }
@@ -734,7 +925,7 @@ __global__ void __launch_bounds__(1024, 1)
         s.host_slot = 0; s.host_e = 0; s.host_n = -1;
         const int ncs = p.compute_streams;
 #pragma unroll
-        for (int q = 0; q < K; q++) { s.slot[q] = q < ncs ? 0 : TINF; s.occ_e[q] = 0; s.occ_n[q] = -1; }
+        for (int q = 0; q < (K & 7); q++) { s.slot[q] = q < ncs ? 0 : TINF; s.occ_e[q] = 0; s.occ_n[q] = -1; }
         s.head_s = s.head_e = 0; s.head_node = 0; s.head_alloc = 0;
         s.ring_head = s.ring_seen = 0;
         s.alloc_t = active ? g.s_init_alloc[g.rank_struct[L.r]] : 0;
@@ -752,11 +943,11 @@ __global__ void __launch_bounds__(1024, 1)
                 const int d = g.init_list[q];
                 const uint4 db = rec_b(g, L.nb + d);
                 if (rec_never(db) || (f.fold && rec_static(db))) continue;
-                dispatch(g, c, L, s, f, d, db, 0, 0);
+                dispatch(g, c, L, s, f, d, db, 0, 0, 0);
             }
             start_phase(g, o, c, L, s, 0, cfg);
         }
-        int64_t cpm = reserve(g, o, c, sh, par, 0, true, cfg, f.epoch);
+        int64_t cpm = reserve<(K & 8) != 0>(g, o, c, sh, par, 0, true, cfg, f.epoch, topo, p.cols[cfg]);
         if (active) refresh_ring(c, L, s);
         f.init = 0;
         if (f.fold) {
@@ -780,7 +971,7 @@ __global__ void __launch_bounds__(1024, 1)
                         s.pop_seq++;
                         prev = tr.x;
                     }
-                    dispatch(g, c, L, s, f, tr.y, rec_b(g, L.nb + tr.y), 0, tr.z);
+                    dispatch(g, c, L, s, f, tr.y, rec_b(g, L.nb + tr.y), 0, tr.z, 0);
                 }
                 if (prev >= 0) start_phase(g, o, c, L, s, 0, cfg);
                 s.done_cnt += g.s_nstatic[st];
@@ -788,7 +979,7 @@ __global__ void __launch_bounds__(1024, 1)
                     for (int q = g.static_off[st]; q < g.static_off[st + 1]; q++)
                         record(g, o, cfg, L.r, g.static_list[q], 0, 0);
             }
-            const int64_t v = reserve(g, o, c, sh, par, 0, false, cfg, f.epoch);
+            const int64_t v = reserve<(K & 8) != 0>(g, o, c, sh, par, 0, false, cfg, f.epoch, topo, p.cols[cfg]);
             cpm = v > cpm ? v : cpm;
             if (active) refresh_ring(c, L, s);
         }
@@ -798,17 +989,18 @@ __global__ void __launch_bounds__(1024, 1)
         // ---- event loop ----
         const int64_t TCAP = (int64_t)1 << 48;   // 48-bit accumulators; keys pack (t, rank)
         for (;;) {
-            int64_t nt = active ? next_time(s, tcur) : TINF;
+            int64_t nt = active ? next_time(g, c, L, s, tcur) : TINF;
             uint64_t key = nt == TINF ? KINF : ((uint64_t)(nt < TCAP ? nt : TCAP) << 14) | (uint64_t)L.r;
             uint64_t kmin = block_min_u64(key, sh, par);
             // collectives completed by the previous step's pops: reserve them now (the
             // reduction's barrier made every arrival visible), then re-derive the next time
             const int nc = sh.ncomp;
-            if (nc) {
-                const int64_t v = reserve_n(g, o, c, sh, par, tcur, false, cfg, f.epoch, nc);
+            if (nc | ((K & 8) ? sh.nmcomp : 0)) {
+                const int64_t v = reserve_n<(K & 8) != 0>(g, o, c, sh, par, tcur, false, cfg, f.epoch, nc, topo,
+                                                          p.cols[cfg]);
                 cpm = v > cpm ? v : cpm;
                 if (active) refresh_ring(c, L, s);
-                nt = active ? next_time(s, tcur) : TINF;
+                nt = active ? next_time(g, c, L, s, tcur) : TINF;
                 key = nt == TINF ? KINF : ((uint64_t)(nt < TCAP ? nt : TCAP) << 14) | (uint64_t)L.r;
                 kmin = block_min_u64(key, sh, par);
             }
@@ -847,7 +1039,7 @@ __global__ void __launch_bounds__(1024, 1)
                         pop_event(g, c, L, s, f, x, t);
                     }
                     if (active) start_phase(g, o, c, L, s, t, cfg);
-                    const int64_t v = reserve(g, o, c, sh, par, t, false, cfg, f.epoch);
+                    const int64_t v = reserve<(K & 8) != 0>(g, o, c, sh, par, t, false, cfg, f.epoch, topo, p.cols[cfg]);
                     cpm = v > cpm ? v : cpm;
                     if (active) {
                         refresh_ring(c, L, s);
@@ -881,17 +1073,72 @@ __global__ void __launch_bounds__(1024, 1)
             if (tid == 0) o.rows[(size_t)cfg * 6 + k] = v;
         }
         if (tid == 0) o.status[cfg] = overflow ? FL_ERR_CAPACITY : dead ? FL_ERR_DEADLOCK : FL_OK;
+        if (o.link_busy)            // SimReport.link_busy_ns (simulator.py:321, :367)
+            for (int l = tid; l < o.link_cap; l += bd)
+                o.link_busy[(size_t)cfg * o.link_cap + l] = (g.n_msg && l < c.link_cap) ? c.link_busy[l] : -1;
         __syncthreads();
     }
+}
+
+// ------------------------------------------------ standalone critical path
+
+// critical_path (simulator.py:400-460) without the simulation: the longest path
+// through the merged multi-rank graph in a host-computed topological order.
+// Only needed when the simulation itself deadlocks: a SEND completes in the
+// simulation only once its RECV is ready (simulator.py:259-268), a wait the
+// contention-free bound does not have.  One thread per design point.
+//   vertex v: vkind 0 = (rank va, local node vb), 1 = collective instance va;
+//   vsend[v] >= 0 for a RECV: the vertex of its SEND, vmsg[v] the message.
+__global__ void cp_kernel(const __grid_constant__ DevGraph g, const __grid_constant__ DevPoints p, int nv,
+                          const int32_t *order, const int32_t *vkind, const int32_t *va, const int32_t *vb,
+                          const int32_t *vsend, const int32_t *vmsg, const int32_t *poff, const int32_t *pidx,
+                          int64_t *vals, int64_t *out, int32_t *status) {
+    const int cfg = blockIdx.x * blockDim.x + threadIdx.x;
+    if (cfg >= p.n) return;
+    int64_t *cv = vals + (size_t)cfg * nv;
+    const int topo = p.topo_kind[cfg], cols = p.cols[cfg];
+    const double beta = __ddiv_rn(1e9, p.bw[cfg]);
+    int64_t best = 0;
+    int st = FL_OK;
+    for (int q = 0; q < nv; q++) {
+        const int v = order[q];
+        int64_t x = 0;
+        for (int u = poff[v]; u < poff[v + 1]; u++) x = cv[pidx[u]] > x ? cv[pidx[u]] : x;   // :449
+        if (vkind[v] == 1) {                        // collective: union of the members' deps (:419-428)
+            const int64_t d = coll_time(g, va[v], p.algo[cfg], topo, p.bw[cfg], p.latency[cfg], p.rows[cfg], cols);
+            if (d < 0) { st = FL_ERR_UNSUPPORTED_ALGO; break; }
+            x += d;
+        } else {
+            const int gn = g.s_node_off[g.rank_struct[va[v]]] + vb[v];
+            if (vsend[v] >= 0) {                    // RECV waits for its SEND plus the wire (:450-452)
+                const int m = vmsg[v];
+                const int64_t w = cv[vsend[v]] + transfer_ns(g, topo, cols, g.msg_send_rank[m], g.msg_recv_rank[m],
+                                                             g.msg_bytes[m], p.latency[cfg], beta);
+                x = w > x ? w : x;
+            }
+            int64_t d = g.node_dur[gn];
+            if (p.peak_flops && g.node_flops[gn] >= 0) d = flops_to_ns(g.node_flops[gn], p.peak_flops[cfg], p.efficiency[cfg]);
+            if ((g.node_rec[3 * gn + 1].x & 15u) <= FL_COMP) x += d;   // `duration_ns or 0`
+        }
+        cv[v] = x;
+        best = x > best ? x : best;
+    }
+    out[cfg] = best;
+    status[cfg] = st;
 }
 
 // ------------------------------------------------------------ host side
 
 cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t st, const DevGraph &g,
                          const DevPoints &p, const DevOut &o, const DevScratch &sc) {
-    if (K == 1) sweep_kernel<1><<<grid, block, smem, st>>>(g, p, o, sc);
-    else if (K == 2) sweep_kernel<2><<<grid, block, smem, st>>>(g, p, o, sc);
-    else sweep_kernel<4><<<grid, block, smem, st>>>(g, p, o, sc);
+    // template argument: compute streams (1, 2, 4) | 8 when the graphs carry SEND/RECV
+    const int T = K | (g.n_msg > 0 ? 8 : 0);
+    if (T == 1) sweep_kernel<1><<<grid, block, smem, st>>>(g, p, o, sc);
+    else if (T == 2) sweep_kernel<2><<<grid, block, smem, st>>>(g, p, o, sc);
+    else if (T == 4) sweep_kernel<4><<<grid, block, smem, st>>>(g, p, o, sc);
+    else if (T == 9) sweep_kernel<9><<<grid, block, smem, st>>>(g, p, o, sc);
+    else if (T == 10) sweep_kernel<10><<<grid, block, smem, st>>>(g, p, o, sc);
+    else sweep_kernel<12><<<grid, block, smem, st>>>(g, p, o, sc);
     return cudaGetLastError();
 }
 
@@ -900,13 +1147,21 @@ cudaError_t sweep_occupancy(int block, size_t smem, int *occ) {
 }
 
 cudaError_t sweep_set_smem(size_t smem) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaSuccess;
+    for (auto fn : {sweep_kernel<1>, sweep_kernel<2>, sweep_kernel<4>, sweep_kernel<9>, sweep_kernel<10>,
+                    sweep_kernel<12>})
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return e;
 }
 
 size_t sweep_shared_header_bytes() { return (sizeof(Shared) + 15) / 16 * 16; }
+
+cudaError_t launch_cp(const DevGraph &g, const DevPoints &p, int nv, const int32_t *order, const int32_t *vkind,
+                      const int32_t *va, const int32_t *vb, const int32_t *vsend, const int32_t *vmsg,
+                      const int32_t *poff, const int32_t *pidx, int64_t *vals, int64_t *out, int32_t *status) {
+    cp_kernel<<<(p.n + 127) / 128, 128>>>(g, p, nv, order, vkind, va, vb, vsend, vmsg, poff, pidx, vals, out, status);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_cost_only(int n, const uint8_t *kind, const int64_t *size, const int64_t *gn,
                              const uint8_t *algo, const double *alpha, const double *beta,

@@ -29,6 +29,11 @@ struct DevGraph {
     int needs_done;              // some tensor's last consumer is only known at run time
     const int32_t *s_nstatic, *trig_off, *static_off, *static_list;
     const int4 *trig;            // {trigger host, node, position in the host's dependents, -}
+    // messages
+    const int64_t *rank_value;
+    int n_msg, p2p_stride;
+    const int32_t *msg_send_rank, *msg_send_node, *msg_recv_rank, *msg_recv_node, *rank_p2p_msg;
+    const int64_t *msg_bytes, *msg_send_id;
 };
 
 struct DevPoints {
@@ -43,7 +48,8 @@ struct DevPoints {
 
 struct DevOut {
     int32_t *status;
-    int64_t *rows, *rank_stats, *ev_start, *ev_end;
+    int64_t *rows, *rank_stats, *ev_start, *ev_end, *link_busy;
+    int link_cap;
 };
 
 // Per-CTA scratch: slot_bytes each, laid out at the given byte offsets.
@@ -51,6 +57,8 @@ struct DevScratch {
     unsigned char *base;
     size_t slot_bytes, off_bits, off_cp, off_ring, off_dur, off_inst;
     // dynamic shared-memory layout (bytes from the start of the CTA's smem)
+    size_t off_msg;              // message state, link state, per-rank in-flight lists
+    int link_cap;
     unsigned sm_off_dyn, sm_off_done, sm_off_dur, sm_off_inst;
     int done_in_smem, dur_in_smem, inst_in_smem;
 };
@@ -60,6 +68,9 @@ cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t s
 cudaError_t sweep_occupancy(int block, size_t smem, int *occ);
 cudaError_t sweep_set_smem(size_t smem);
 size_t sweep_shared_header_bytes();
+cudaError_t launch_cp(const DevGraph &g, const DevPoints &p, int nv, const int32_t *order, const int32_t *vkind,
+                      const int32_t *va, const int32_t *vb, const int32_t *vsend, const int32_t *vmsg,
+                      const int32_t *poff, const int32_t *pidx, int64_t *vals, int64_t *out, int32_t *status);
 cudaError_t launch_cost_only(int n, const uint8_t *kind, const int64_t *size, const int64_t *gn,
                              const uint8_t *algo, const double *alpha, const double *beta,
                              const int32_t *rows, const int32_t *cols, int64_t *out, int32_t *status,

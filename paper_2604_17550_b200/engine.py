@@ -184,11 +184,23 @@ class Engine:
         except Exception:
             pass
 
-    def run(self, pts: DesignPoints, rank_stats: bool = False, events: bool = False) -> dict:
+    def link_cap(self, pts: DesignPoints) -> int:
+        """Link-id space of these points: switch eg/in per rank, mesh 4 per position."""
+        mesh = pts.topo_kind == 1
+        cap = 2 * self.gs.n_ranks
+        if mesh.any():
+            cap = max(cap, int((4 * pts.rows[mesh].astype(np.int64) * pts.cols[mesh]).max()))
+        return cap
+
+    def run(self, pts: DesignPoints, rank_stats: bool = False, events: bool = False,
+            links: bool = False) -> dict:
         """Evaluate design points from host buffers (copies included)."""
         n = len(pts)
         R = self.gs.n_ranks
         out = {"status": np.zeros(n, np.int32), "rows": np.zeros((n, 6), np.int64)}
+        cap = self.link_cap(pts) if links else 0
+        if links:
+            out["link_busy"] = np.full((n, max(cap, 1)), -1, np.int64)
         if rank_stats:
             out["rank_stats"] = np.zeros((n, R, 5), np.int64)
         if events:
@@ -201,11 +213,28 @@ class Engine:
                            pts.compute_streams)
         o = _native.Outputs(_ptr(out["status"], _native.P32), _ptr(out["rows"], _native.P64),
                             _ptr(out.get("rank_stats"), _native.P64), _ptr(out.get("ev_start"), _native.P64),
-                            _ptr(out.get("ev_end"), _native.P64))
+                            _ptr(out.get("ev_end"), _native.P64), _ptr(out.get("link_busy"), _native.P64), cap)
         rc = _native.lib().fl_sweep_run(self._h, C.byref(p), C.byref(o))
         if rc:
             raise EngineError(f"fl_sweep_run: {_native.last_error()} (status {rc})")
         return out
+
+    def critical_path_only(self, pts: DesignPoints, mg: dict) -> int:
+        """fl_critical_path on one design point over a merged graph (store.merged_cp_graph)."""
+        p = _native.Points(len(pts), _ptr(pts.algo, _native.PU8), _ptr(pts.topo_kind, _native.PU8),
+                           _ptr(pts.bw, _native.PF64), _ptr(pts.latency, _native.P64),
+                           _ptr(pts.rows, _native.P32), _ptr(pts.cols, _native.P32),
+                           _ptr(pts.peak_flops, _native.PF64), _ptr(pts.efficiency, _native.PF64), 1)
+        cp = np.zeros(len(pts), np.int64)
+        st = np.zeros(len(pts), np.int32)
+        arr = {k: np.ascontiguousarray(v if len(v) else np.zeros(1, np.int32)) for k, v in mg.items() if k != "n_vert"}
+        rc = _native.lib().fl_critical_path(self._h, C.byref(p), mg["n_vert"], *(
+            _ptr(arr[k], _native.P32) for k in ("order", "vkind", "va", "vb", "vsend", "vmsg", "pred_off", "pred_idx")),
+            _ptr(cp, _native.P64), _ptr(st, _native.P32))
+        if rc:
+            raise EngineError(f"fl_critical_path: {_native.last_error()} (status {rc})")
+        raise_for_status(int(st[0]))
+        return int(cp[0])
 
     def run_device(self, dev: dict, stream_ptr: int, n: int, compute_streams: int = 1) -> int:
         """Evaluate design points already resident in device memory.
@@ -221,7 +250,7 @@ class Engine:
                            v("peak_flops", _native.PF64), v("efficiency", _native.PF64), compute_streams)
         o = _native.Outputs(v("out_status", _native.P32), v("out_rows", _native.P64),
                             v("out_rank_stats", _native.P64), v("out_ev_start", _native.P64),
-                            v("out_ev_end", _native.P64))
+                            v("out_ev_end", _native.P64), None, 0)
         if not dev.get("out_status") or not dev.get("out_rows"):
             raise EngineError("run_device needs out_status and out_rows device buffers")
         launches = C.c_int32(0)
@@ -239,16 +268,48 @@ def _single_point(topo, algo, compute_streams=1) -> DesignPoints:
     return DesignPoints.from_topologies([topo], [algo], compute_streams=compute_streams)
 
 
+def _raise_pair_error(gs: GraphSet, topo, algo) -> None:
+    """An unmatched SEND/RECV channel is a DeadlockError, raised by the reference
+    only after its collectives were costed (simulator.py:220-228), so an
+    undefined algorithm on this topology wins."""
+    from .costs import analytical_time
+    from .graph import CollectiveKind
+    kinds = {0: CollectiveKind.ALL_REDUCE, 1: CollectiveKind.ALL_GATHER, 2: CollectiveKind.REDUCE_SCATTER}
+    mesh = (topo.rows, topo.cols) if _ev(topo.kind) == "mesh" else None
+    for i in range(gs.n_inst):
+        k, n = kinds[int(gs.inst_kind[i])], int(gs.inst_n[i])
+        size = int(gs.inst_bytes[i]) * n if k == CollectiveKind.ALL_GATHER else int(gs.inst_bytes[i])
+        analytical_time(k, size, n, CollectiveAlgo(_ev(algo)), topo.latency_ns, topo.beta_ns_per_byte, mesh_shape=mesh)
+    from .errors import DeadlockError
+    raise DeadlockError(gs.pair_error)
+
+
+def _link_names(gs: GraphSet, topo, busy) -> dict:
+    out = {}
+    cols = getattr(topo, "cols", 0)
+    for l in np.nonzero(busy >= 0)[0]:
+        l = int(l)
+        if _ev(topo.kind) == "switch":
+            out[f"{'eg' if l % 2 == 0 else 'in'}{int(gs.rank_values[l // 2])}"] = int(busy[l])
+        else:
+            a, d = divmod(l, 4)
+            b = a + (1, -1, cols, -cols)[d]
+            out[f"{a}->{b}"] = int(busy[l])
+    return dict(sorted(out.items()))
+
+
 def simulate(graphs, topo, opts: Optional[SimOptions] = None, device: int = 0) -> SimReport:
     """Drop-in ``trainsim.simulate`` (simulator.py:203) evaluated on the GPU."""
     opts = opts or SimOptions()
     if opts.compute_streams < 1 or opts.comm_streams < 1:
         raise ValueError("stream counts must be >= 1")
     gs = compile_graphs(graphs)
+    if gs.pair_error:
+        _raise_pair_error(gs, topo, opts.algo)
     eng = Engine(gs, device)
     try:
         out = eng.run(_single_point(topo, opts.algo, opts.compute_streams), rank_stats=True,
-                      events=opts.record_events)
+                      events=opts.record_events, links=gs.has_p2p)
     finally:
         eng.close()
     raise_for_status(int(out["status"][0]), "simulation stalled with work remaining"
@@ -258,6 +319,8 @@ def simulate(graphs, topo, opts: Optional[SimOptions] = None, device: int = 0) -
         s = out["rank_stats"][0, r]
         ranks[int(gs.rank_values[r])] = RankStats(*map(int, s))
     rep = SimReport(makespan_ns=int(out["rows"][0, 0]), ranks=ranks)
+    if gs.has_p2p:
+        rep.link_busy_ns = _link_names(gs, topo, out["link_busy"][0])
     if opts.record_events:
         stream_of = {0: "host", 1: "compute", 2: "comm", 3: "comm", 4: "comm"}
         evs = []
@@ -277,9 +340,18 @@ def simulate(graphs, topo, opts: Optional[SimOptions] = None, device: int = 0) -
 
 def critical_path(graphs, topo, algo=CollectiveAlgo.RING, device: int = 0) -> int:
     """Drop-in ``trainsim.critical_path`` (simulator.py:400): contention-free bound."""
-    eng = Engine(graphs, device)
+    gs = compile_graphs(graphs)
+    if gs.pair_error:
+        _raise_pair_error(gs, topo, algo)
+    eng = Engine(gs, device)
     try:
-        out = eng.run(_single_point(topo, algo))
+        pts = _single_point(topo, algo)
+        out = eng.run(pts)
+        if out["status"][0] == 3 and gs.has_p2p:
+            # the simulation deadlocked on a SEND waiting for its RECV (simulator.py:259-268);
+            # the contention-free bound has no such wait: relax the merged graph alone
+            from .store import merged_cp_graph
+            return eng.critical_path_only(pts, merged_cp_graph(gs))
     finally:
         eng.close()
     raise_for_status(int(out["status"][0]), "cyclic cross-rank wait in critical path"

@@ -26,7 +26,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .errors import EngineError, InconsistentGroupsError
+from .errors import DeadlockError, EngineError, InconsistentGroupsError
 
 KIND = {"HOST": 0, "COMP": 1, "COLL": 2, "SEND": 3, "RECV": 4}
 CKIND = {"ALL_REDUCE": 0, "ALL_GATHER": 1, "REDUCE_SCATTER": 2}
@@ -60,6 +60,7 @@ class Structure:
     cons_idx: np.ndarray
     init_alloc: int
     colls: list                     # local indices of COLL nodes in list order
+    p2ps: list = field(default_factory=list)   # local indices of SEND/RECV nodes in list order
 
     @property
     def n(self) -> int:
@@ -92,6 +93,7 @@ def compile_structure(nodes, tensors) -> Structure:
     succs = [[] for _ in range(n)]
     init = []
     colls = []
+    p2ps = []
     for li, node in enumerate(nodes):               # list order: dispatch order of the reference
         k = local[node.node_id]
         kd = KIND[_ev(node.kind)]
@@ -104,6 +106,9 @@ def compile_structure(nodes, tensors) -> Structure:
         elif kd == 2:
             coll_ord[k] = len(colls)
             colls.append(k)
+        else:                                       # SEND / RECV: ordinal among this rank's p2p nodes
+            coll_ord[k] = len(p2ps)
+            p2ps.append(k)
         deps = set(node.dep_ids())
         p = []
         for d in deps:
@@ -149,7 +154,7 @@ def compile_structure(nodes, tensors) -> Structure:
     return Structure([nodes[i] for i in order], np.asarray(ids, np.int64), listpos, kind, flags, dur,
                      flops, alloc, coll_ord, pred_off, pred_idx, succ_off, succ_idx, free_off,
                      free_tens, np.asarray(init, np.int32), tbytes, cons_off, cons_idx,
-                     int(init_alloc), colls)
+                     int(init_alloc), colls, p2ps)
 
 
 @dataclass
@@ -170,6 +175,16 @@ class GraphSet:
     coll_stride: int
     rank_coll_inst: np.ndarray       # [R, coll_stride]
     has_p2p: bool = False
+    # messages (simulator.py:177-200): k-th SEND matched to k-th RECV per (src, dst, tag)
+    msg_send_rank: np.ndarray = None
+    msg_send_node: np.ndarray = None
+    msg_recv_rank: np.ndarray = None
+    msg_recv_node: np.ndarray = None
+    msg_bytes: np.ndarray = None
+    msg_send_id: np.ndarray = None
+    p2p_stride: int = 1
+    rank_p2p_msg: np.ndarray = None  # [R, p2p_stride]
+    pair_error: str = ""             # unmatched channel: DeadlockError once the run starts
     _keep: list = field(default_factory=list)
 
     @property
@@ -281,7 +296,47 @@ def compile_graphs(graphs) -> GraphSet:
      gs.inst_mem_rank, gs.inst_mem_node, gs.coll_stride, gs.rank_coll_inst) = _match_instances(
         gs, graphs, gs.rank_values, rank_struct, structs)
     gs.has_p2p = has_p2p
+    _pair_messages(gs)
     return gs
+
+
+def _pair_messages(gs: GraphSet) -> None:
+    """_pair_messages (simulator.py:177-200): per channel (src, dst, tag), the k-th
+    SEND (by node id) carries the k-th RECV; unequal counts deadlock."""
+    R = gs.n_ranks
+    stride = max((len(gs.structs[gs.rank_struct[r]].p2ps) for r in range(R)), default=0)
+    gs.p2p_stride = max(stride, 1)
+    gs.rank_p2p_msg = np.full((R, gs.p2p_stride), -1, np.int32)
+    sends, recvs = {}, {}
+    for r in range(R):
+        st = gs.structs[gs.rank_struct[r]]
+        rv = int(gs.rank_values[r])
+        for k in st.p2ps:
+            node = st.nodes[k]
+            p = node.p2p
+            if int(st.kind[k]) == 3:
+                sends.setdefault((rv, int(p.peer_rank), int(p.channel_tag)), []).append((node.node_id, r, k))
+            else:
+                recvs.setdefault((int(p.peer_rank), rv, int(p.channel_tag)), []).append((node.node_id, r, k))
+    cols = {name: [] for name in ("sr", "sn", "rr", "rn", "by", "sid")}
+    for key in sorted(set(sends) | set(recvs)):
+        ss, rr = sorted(sends.get(key, [])), sorted(recvs.get(key, []))
+        if len(ss) != len(rr):
+            # simulate raises this after its collective checks (simulator.py:220-228)
+            gs.pair_error = f"channel {key}: {len(ss)} sends but {len(rr)} recvs"
+            break
+        for (sid, sr, sk), (_, dr, dk) in zip(ss, rr):
+            m = len(cols["sr"])
+            st_s = gs.structs[gs.rank_struct[sr]]
+            cols["sr"].append(sr); cols["sn"].append(sk); cols["rr"].append(dr); cols["rn"].append(dk)
+            cols["by"].append(int(st_s.nodes[sk].p2p.comm_bytes)); cols["sid"].append(sid)
+            gs.rank_p2p_msg[sr, st_s.coll_ord[sk]] = m
+            gs.rank_p2p_msg[dr, gs.structs[gs.rank_struct[dr]].coll_ord[dk]] = m
+    i32 = lambda v: np.asarray(v, np.int32)
+    gs.msg_send_rank, gs.msg_send_node = i32(cols["sr"]), i32(cols["sn"])
+    gs.msg_recv_rank, gs.msg_recv_node = i32(cols["rr"]), i32(cols["rn"])
+    gs.msg_bytes = np.asarray(cols["by"], np.int64)
+    gs.msg_send_id = np.asarray(cols["sid"], np.int64)
 
 
 def desc_arrays(gs: GraphSet) -> dict:
@@ -329,13 +384,84 @@ def desc_arrays(gs: GraphSet) -> dict:
         inst_mem_rank=gs.inst_mem_rank, inst_mem_node=gs.inst_mem_node,
         coll_stride=int(gs.coll_stride),
         rank_coll_inst=np.ascontiguousarray(gs.rank_coll_inst.astype(np.int32)),
+        rank_value=np.ascontiguousarray(gs.rank_values.astype(np.int64)),
+        n_msg=len(gs.msg_bytes), msg_send_rank=gs.msg_send_rank, msg_send_node=gs.msg_send_node,
+        msg_recv_rank=gs.msg_recv_rank, msg_recv_node=gs.msg_recv_node, msg_bytes=gs.msg_bytes,
+        msg_send_id=gs.msg_send_id, p2p_stride=int(gs.p2p_stride),
+        rank_p2p_msg=np.ascontiguousarray(gs.rank_p2p_msg.astype(np.int32)),
     )
 
 
 def check_supported(gs: GraphSet, max_ranks: int = 1024, max_nodes: int = 4096) -> None:
-    if gs.has_p2p:
-        raise EngineError("SEND/RECV nodes (expanded comm mode) are not supported by this engine build")
     if gs.n_ranks > max_ranks:
         raise EngineError(f"{gs.n_ranks} ranks exceed this engine build's {max_ranks} per design point")
     if gs.max_nodes > max_nodes:
         raise EngineError(f"a rank graph has {gs.max_nodes} nodes; this build supports {max_nodes}")
+
+
+def merged_cp_graph(gs: GraphSet):
+    """The graph ``critical_path`` relaxes (simulator.py:408-436), in topological order.
+
+    Vertices: every (rank, node) that is not a collective, plus one vertex per
+    collective instance (its members share the union of their dependencies,
+    :419-428); a RECV also depends on its SEND (:430-435).  Returns the arrays of
+    ``fl_critical_path``, or raises DeadlockError when the merged graph has a
+    cycle or a dependency on a missing node (:458-459).
+    """
+    R = gs.n_ranks
+    base = np.zeros(R + 1, np.int64)
+    for r in range(R):
+        base[r + 1] = base[r] + gs.structs[gs.rank_struct[r]].n
+    total = int(base[-1])
+    V = total + gs.n_inst
+    vid = np.arange(total, dtype=np.int64)            # (rank, node) -> vertex, collectives remapped
+    for i in range(gs.n_inst):
+        for j in range(int(gs.inst_mem_off[i]), int(gs.inst_mem_off[i + 1])):
+            vid[base[gs.inst_mem_rank[j]] + gs.inst_mem_node[j]] = total + i
+    preds = [set() for _ in range(V)]
+    never = np.zeros(V, bool)
+    vkind = np.zeros(V, np.int32)
+    va = np.zeros(V, np.int32)
+    vb = np.zeros(V, np.int32)
+    vsend = np.full(V, -1, np.int32)
+    vmsg = np.full(V, -1, np.int32)
+    live = np.zeros(V, bool)
+    for r in range(R):
+        st = gs.structs[gs.rank_struct[r]]
+        for k in range(st.n):
+            v = int(vid[base[r] + k])
+            live[v] = True
+            if v < total:
+                va[v], vb[v] = r, k
+            ps = st.pred_idx[st.pred_off[k]:st.pred_off[k + 1]]
+            preds[v].update(int(vid[base[r] + q]) for q in ps)
+            if st.flags[k] & 1:
+                never[v] = True
+    for i in range(gs.n_inst):
+        vkind[total + i], va[total + i] = 1, i
+    for m in range(len(gs.msg_bytes)):
+        s_v = int(vid[base[gs.msg_send_rank[m]] + gs.msg_send_node[m]])
+        r_v = int(vid[base[gs.msg_recv_rank[m]] + gs.msg_recv_node[m]])
+        preds[r_v].add(s_v)
+        vsend[r_v], vmsg[r_v] = s_v, m
+    indeg = np.array([len(p) for p in preds], np.int64)
+    succ = [[] for _ in range(V)]
+    for v in range(V):
+        for u in preds[v]:
+            succ[u].append(v)
+    order = [v for v in range(V) if live[v] and indeg[v] == 0 and not never[v]]
+    k = 0
+    while k < len(order):
+        u = order[k]
+        k += 1
+        for v in succ[u]:
+            indeg[v] -= 1
+            if indeg[v] == 0 and not never[v]:
+                order.append(v)
+    if len(order) != int(live.sum()):
+        raise DeadlockError("cyclic cross-rank wait in critical path")
+    poff = np.zeros(V + 1, np.int32)
+    poff[1:] = np.cumsum([len(p) for p in preds])
+    pidx = np.fromiter((u for p in preds for u in sorted(p)), np.int32, count=int(poff[-1]))
+    return dict(n_vert=V, order=np.asarray(order, np.int32), vkind=vkind, va=va, vb=vb, vsend=vsend,
+                vmsg=vmsg, pred_off=poff, pred_idx=pidx)

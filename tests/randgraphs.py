@@ -90,3 +90,56 @@ def random_graphs(seed: int, max_world: int = 6, max_nodes: int = 24, p_zero: fl
     lat = rng.choice([0, 1, 10, 100])
     bw = rng.choice([1e9, 4e9, 1e12])
     return graphs, Topology.switch(world, bw, lat)
+
+
+def random_p2p_graphs(seed: int, mesh: bool = False):
+    """Ranks exchanging point-to-point messages (expanded comm mode): random
+    SEND/RECV pairs on shared channels, interleaved with compute and an
+    optional collective; links are contended and some graphs deadlock."""
+    from paper_2604_17550_b200.graph import P2pSpec
+    rng = random.Random(seed)
+    if mesh:
+        rows, cols = rng.choice([(1, 2), (2, 2), (2, 3)])
+        world = rows * cols
+    else:
+        world = rng.randint(2, 5)
+    msgs = []
+    for _ in range(rng.randint(1, 10)):
+        a, b = rng.sample(range(world), 2)
+        msgs.append((a, b, rng.randint(0, 2), rng.choice([0, 8, 100, 1000, 4096])))
+    per_rank = [[] for _ in range(world)]
+    for mi, (a, b, tag, nb) in enumerate(msgs):
+        per_rank[a].append(("send", mi))
+        per_rank[b].append(("recv", mi))
+    graphs = []
+    for rank in range(world):
+        ops = per_rank[rank]
+        rng.shuffle(ops)
+        nodes, tensors = [], {}
+        last = None
+        nid = 0
+        for kind, mi in ops:
+            if rng.random() < 0.6:
+                out = len(tensors)
+                tensors[out] = TensorMeta.make(out, [rng.randint(1, 64)], Dtype.F32)
+                deps = [last] if last is not None and rng.random() < 0.7 else []
+                nodes.append(Node(nid, NodeKind.COMP, "work", outputs=[out], data_deps=deps,
+                                  duration_ns=rng.choice([0, 5, 10, 40])))
+                last = nid
+                nid += 1
+            a, b, tag, nb = msgs[mi]
+            deps = [last] if last is not None and rng.random() < 0.6 else []
+            if kind == "send":
+                nodes.append(Node(nid, NodeKind.SEND, "send", data_deps=deps, p2p=P2pSpec(b, nb, tag)))
+            else:
+                out = len(tensors)
+                tensors[out] = TensorMeta.make(out, [max(1, nb // 4)], Dtype.F32)
+                nodes.append(Node(nid, NodeKind.RECV, "recv", outputs=[out], data_deps=deps, p2p=P2pSpec(a, nb, tag)))
+            if rng.random() < 0.5:
+                last = nid
+            nid += 1
+        graphs.append(WorkloadGraph(rank, world, nodes, tensors, {"graph_inputs": []}))
+    lat = rng.choice([0, 5, 10])
+    bw = rng.choice([1e9, 2e9])
+    topo = Topology.mesh2d(rows, cols, bw, lat) if mesh else Topology.switch(world, bw, lat)
+    return graphs, topo

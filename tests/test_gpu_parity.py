@@ -17,8 +17,7 @@ from randgraphs import random_graphs
 
 pytestmark = pytest.mark.gpu
 
-CASES = [c for c in corpus() if not has_p2p(c)]
-P2P_CASES = [c for c in corpus() if has_p2p(c)]
+CASES = corpus()      # including SEND/RECV (expanded comm mode) cases
 
 
 def engine_result(graphs, topo, algo, cs, events):
@@ -53,12 +52,6 @@ def test_engine_matches_reference(idx):
     assert got["cp"] == case["cp"]
     if "events" in case:
         assert got["events"] == case["events"]
-
-
-def test_p2p_graphs_fail_loudly():
-    """Expanded comm mode is not in this build: the engine must refuse, not guess."""
-    with pytest.raises(EngineError):
-        E.simulate(decode_graphs(P2P_CASES[0]), decode_topo(P2P_CASES[0]["topo"]))
 
 
 def _family(preset, par, mode):
@@ -216,3 +209,41 @@ def test_sweep_cli_exit_codes(tmp_path):
     # bad topology spec: FormatError -> exit 2
     assert main(["sweep", "--preset", "tiny", "--parallel", "dp:4", "--topo", "ring:4",
                  "--algo", "ring", "--out", out]) == 2
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_engine_random_p2p_vs_oracle(seed):
+    """Expanded comm mode: per-link FIFO, message ordering, busy/exposed stats."""
+    from randgraphs import random_p2p_graphs
+    gs, topo = random_p2p_graphs(seed, mesh=seed % 2 == 1)
+    try:
+        ref = O.simulate(gs, topo, "ring", record_events=True)
+        st, en = ref.pop("events")
+        evs, k = [], 0
+        for g in gs:
+            for n in g.nodes:
+                evs.append((int(st[k]), g.rank, n.node_id, int(en[k])))
+                k += 1
+        want = (ref["makespan_ns"], ref["ranks"], ref["links"], sorted(evs))
+    except O.OracleError as e:
+        want = e.kind
+    try:
+        rep = E.simulate(gs, topo, E.SimOptions())
+        got = (rep.makespan_ns, {k: vars(v) for k, v in rep.ranks.items()}, rep.link_busy_ns,
+               sorted((e.start_ns, e.rank, e.node_id, e.end_ns) for e in rep.events))
+    except EngineError:
+        raise
+    except Exception as e:
+        got = type(e).__name__
+    assert got == want, seed
+    try:
+        want_cp = O.critical_path(gs, topo, "ring")
+    except O.OracleError as e:
+        want_cp = e.kind
+    try:
+        got_cp = E.critical_path(gs, topo, "ring")
+    except EngineError:
+        raise
+    except Exception as e:
+        got_cp = type(e).__name__
+    assert got_cp == want_cp, seed

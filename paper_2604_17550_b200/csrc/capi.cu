@@ -304,7 +304,7 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     const size_t dur_bytes = (size_t)(total > 0 ? total : 1) * 8;
     const size_t done_bytes = (size_t)dg.max_words * R * 8;
     size_t off = 0;
-    sc.off_bits = off; off = align_up(off + 4 * done_bytes, 256);
+    sc.off_bits = off; off = align_up(off + 5 * done_bytes, 256);
     sc.off_cp = off;   off = align_up(off + (size_t)dg.max_nodes * R * 8, 256);
     sc.off_ring = off; off = align_up(off + 2 * (size_t)dg.coll_stride * R * 4, 256);
     sc.off_dur = off;  off = align_up(off + dur_bytes, 256);
@@ -327,8 +327,10 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     if (sc.inst_in_smem) { sc.sm_off_inst = (unsigned)sm; sm = align_up(sm + inst_bytes, 16); }
     sc.dur_in_smem = sm + dur_bytes <= budget;
     if (sc.dur_in_smem) { sc.sm_off_dur = (unsigned)sm; sm = align_up(sm + dur_bytes, 16); }
-    sc.done_in_smem = sm + done_bytes <= budget;
+    sc.done_in_smem = dg.needs_done && sm + done_bytes <= budget;
     if (sc.done_in_smem) { sc.sm_off_done = (unsigned)sm; sm = align_up(sm + done_bytes, 16); }
+    sc.touch_in_smem = sm + done_bytes <= budget;
+    if (sc.touch_in_smem) { sc.sm_off_touch = (unsigned)sm; sm = align_up(sm + done_bytes, 16); }
     if (sm > budget) return fail(FL_ERR_CAPACITY, "per-rank state exceeds shared memory");
     g->smem = sm;
     CK(fl::sweep_set_smem(sm));

@@ -208,6 +208,7 @@ enum { ST_COMP = 0, ST_OVL, ST_CUR, ST_PEAK, ST_FIN, ST_N };
 struct Ctx {
     int R;
     uint64_t *done, *rdyc, *rdyh, *due;
+    uint64_t *touched;              // [word][rank]: accumulator written in this design point
     int64_t *cp;                    // [max_nodes][R]
     int32_t *ring_inst, *ring_node; // [coll_stride][R] per-rank comm FIFO
     int64_t *dur;                   // [total_nodes] this design point's durations
@@ -425,8 +426,17 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
         const uint4 db = rec_b(g, L.nb + d);
         if (rec_never(db)) continue;
         int64_t *slot = c.cp + (d * R + L.r);
-        uint64_t a = (uint64_t)*slot;
-        if ((a >> 58) != (f.epoch >> 58)) a = f.epoch | (rec_indeg(db, f.fold) << 48);
+        // first dependency to complete: the word holds nothing of this design point,
+        // so skip reading it (a DRAM round trip on the critical chain)
+        uint64_t &tw = c.touched[(d >> 6) * R + L.r];
+        const uint64_t tb = 1ull << (d & 63);
+        uint64_t a;
+        if (tw & tb) {
+            a = (uint64_t)*slot;
+        } else {
+            tw |= tb;
+            a = f.epoch | (rec_indeg(db, f.fold) << 48);
+        }
         const uint64_t v = (a & VAL48) > fx ? (a & VAL48) : fx;
         const uint64_t left = ((a >> 48) & 0x3ff) - 1;
         if (left == 0) dispatch(g, c, L, s, f, d, db, (int64_t)v, seq, t);
@@ -776,6 +786,7 @@ __global__ void __launch_bounds__(1024, 1)
         c.rdyh = gbits + words;
         c.due = gbits + 2 * words;
         c.done = sc.done_in_smem ? reinterpret_cast<uint64_t *>(smem + sc.sm_off_done) : gbits + 3 * words;
+        c.touched = sc.touch_in_smem ? reinterpret_cast<uint64_t *>(smem + sc.sm_off_touch) : gbits + 4 * words;
         c.cp = reinterpret_cast<int64_t *>(base + sc.off_cp);
         c.ring_inst = reinterpret_cast<int32_t *>(base + sc.off_ring);
         c.ring_node = c.ring_inst + (size_t)g.coll_stride * R;
@@ -889,6 +900,7 @@ __global__ void __launch_bounds__(1024, 1)
         }
         if (dirty) for (size_t i = tid; i < 3 * words; i += bd) gbits[i] = 0;
         if (g.needs_done) for (size_t i = tid; i < words; i += bd) c.done[i] = 0;
+        for (size_t i = tid; i < words; i += bd) c.touched[i] = 0;
         if (tid == 0) { sh.cend_all = 0; sh.cend_uniform = 1; }
         for (int r = tid; r < R; r += bd) {
             c.comm_end[r] = 0;

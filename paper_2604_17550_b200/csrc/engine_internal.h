@@ -59,8 +59,8 @@ struct DevScratch {
     // dynamic shared-memory layout (bytes from the start of the CTA's smem)
     size_t off_msg;              // message state, link state, per-rank in-flight lists
     int link_cap;
-    unsigned sm_off_dyn, sm_off_done, sm_off_dur, sm_off_inst;
-    int done_in_smem, dur_in_smem, inst_in_smem;
+    unsigned sm_off_dyn, sm_off_done, sm_off_dur, sm_off_inst, sm_off_touch;
+    int done_in_smem, dur_in_smem, inst_in_smem, touch_in_smem;
 };
 
 cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t st, const DevGraph &g,

@@ -102,7 +102,7 @@ class ClockSampler:
 
 def load_workload(name: str):
     from paper_2604_17550_b200 import sweep as S
-    w = S.c3_workload() if name == "c3" else S.c2_workload()
+    w = {"c3": S.c3_workload, "c2": S.c2_workload, "c4": S.c4_workload}[name]()
     graphs = S.workload_graphs(w)
     return w, graphs
 
@@ -113,7 +113,10 @@ def workload_desc(w, gs) -> dict:
                                "points = {switch:1024+ring, mesh:32x32+mesh-hier} x 64 bw [10GB/s,1.8TB/s] x "
                                "32 latency [100ns,20us]",
                          "c2": "BASELINE config 2: GPT-2 small dp:64, 256 design points = {ring, tree} x 16 bw "
-                               "[10GB/s,1.8TB/s] x 8 latency [100ns,10us]"}[w.name],
+                               "[10GB/s,1.8TB/s] x 8 latency [100ns,10us]",
+                         "c4": "BASELINE config 4 scale: llama-70b-like FSDP graph at 8192 ranks (clusters of 8 "
+                               "CTAs per design point), design points from {switch:8192+ring, mesh:64x128+"
+                               "mesh-hier} x 128 bw [10GB/s,1.8TB/s] x 64 latency [100ns,20us]"}[w.name],
             "model": w.model, "parallel": w.parallel, "ranks": gs.n_ranks, "nodes_per_rank": st.n,
             "edges_per_rank": int(st.pred_off[-1]), "points_per_gpu": len(w.points),
             "units_per_point": gs.units()}
@@ -239,6 +242,8 @@ def run_ours(args):
     from paper_2604_17550_b200 import sweep as S
     from paper_2604_17550_b200.engine import Engine
     w, graphs = load_workload(args.workload)
+    if args.points:
+        w.points = w.points.take(np.linspace(0, len(w.points) - 1, args.points).round().astype(np.int64))
     eng = Engine(graphs, device=local)
     gs = eng.gs
     n = len(w.points)
@@ -383,7 +388,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c3", "c2"], default="c3")
+    ap.add_argument("--workload", choices=["c3", "c2", "c4"], default="c3")
+    ap.add_argument("--points", type=int, default=0, help="evaluate an evenly spaced subset of the grid")
     ap.add_argument("--cpu-points", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -54,7 +54,7 @@ enum fl_topo { FL_SWITCH = 0, FL_MESH2D = 1 };
 
 /* Engine limits of this build. */
 #define FL_MAX_NODES_PER_RANK 4096   /* 64 bitmap words x 64 bits        */
-#define FL_MAX_RANKS 1024            /* one thread per rank, one CTA per design point */
+#define FL_MAX_RANKS 16384           /* one thread per rank; > 1024 ranks run on a CTA cluster (<= 16) */
 #define FL_MAX_P2P_PER_RANK 4096     /* SEND+RECV nodes per rank graph */
 
 /*

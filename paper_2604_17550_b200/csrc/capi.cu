@@ -49,6 +49,7 @@ struct fl_graph {
     size_t stage_bytes = 0;
     int grid_cap = 0;
     int block = 32;
+    int cluster = 1;
     size_t smem = 0;
 };
 
@@ -292,8 +293,11 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
         if (rc) return rc;
     }
 
-    // launch geometry: one thread per rank, one CTA per design point at a time
-    g->block = (R + 31) / 32 * 32;
+    // launch geometry: one thread per rank; a design point runs on one CTA, or on a
+    // cluster of CTAs (1024 ranks each) when it has more ranks than a CTA has threads
+    g->cluster = (R + 1023) / 1024;
+    g->block = g->cluster > 1 ? 1024 : (R + 31) / 32 * 32;
+    const int CS = g->cluster;
     int sms = 0, optin = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
@@ -307,7 +311,7 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     sc.off_bits = off; off = align_up(off + 5 * done_bytes, 256);
     sc.off_cp = off;   off = align_up(off + (size_t)dg.max_nodes * R * 8, 256);
     sc.off_ring = off; off = align_up(off + 2 * (size_t)dg.coll_stride * R * 4, 256);
-    sc.off_dur = off;  off = align_up(off + dur_bytes, 256);
+    sc.off_dur = off;  off = align_up(off + dur_bytes * CS, 256);      // one copy per CTA of a cluster
     sc.off_inst = off; off = align_up(off + inst_bytes, 256);
     // links: switch eg/in per rank; mesh 4 per position (bounded by the largest rank id)
     int64_t maxv = 0;
@@ -316,28 +320,31 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     sc.off_msg = off;
     off = align_up(off + (size_t)d->n_msg * 8 * 8 + (size_t)sc.link_cap * 16 + (size_t)d->n_msg * 8 +
                        (size_t)R * 4 + 2 * (size_t)dg.p2p_stride * R * 4 + 64, 256);
+    sc.off_ctr = off;  off = align_up(off + 64, 256);
     sc.slot_bytes = off;
 
     // shared memory: header | comm_end, stats, ring tails | [instances] | [durations] | [done bitmap]
     size_t sm = fl::sweep_shared_header_bytes();
     sc.sm_off_dyn = (unsigned)sm;
-    sm = align_up(sm + (size_t)R * (8 + 6 * 8 + 4), 16);
+    const size_t B = (size_t)g->block;              // shared per-rank arrays have blockDim stride
+    sm = align_up(sm + B * (8 + 5 * 8 + 4), 16);    // comm ends, 5 statistics, ring tails
     const size_t budget = (size_t)optin;
-    sc.inst_in_smem = sm + inst_bytes <= budget;
+    const size_t sbits = (size_t)dg.max_words * B * 8;   // a bitmap over this CTA's ranks
+    sc.inst_in_smem = CS == 1 && sm + inst_bytes <= budget;   // clusters share instance state in HBM
     if (sc.inst_in_smem) { sc.sm_off_inst = (unsigned)sm; sm = align_up(sm + inst_bytes, 16); }
     sc.dur_in_smem = sm + dur_bytes <= budget;
     if (sc.dur_in_smem) { sc.sm_off_dur = (unsigned)sm; sm = align_up(sm + dur_bytes, 16); }
-    sc.done_in_smem = dg.needs_done && sm + done_bytes <= budget;
-    if (sc.done_in_smem) { sc.sm_off_done = (unsigned)sm; sm = align_up(sm + done_bytes, 16); }
-    sc.touch_in_smem = sm + done_bytes <= budget;
-    if (sc.touch_in_smem) { sc.sm_off_touch = (unsigned)sm; sm = align_up(sm + done_bytes, 16); }
+    sc.done_in_smem = dg.needs_done && sm + sbits <= budget;
+    if (sc.done_in_smem) { sc.sm_off_done = (unsigned)sm; sm = align_up(sm + sbits, 16); }
+    sc.touch_in_smem = sm + sbits <= budget;
+    if (sc.touch_in_smem) { sc.sm_off_touch = (unsigned)sm; sm = align_up(sm + sbits, 16); }
     if (sm > budget) return fail(FL_ERR_CAPACITY, "per-rank state exceeds shared memory");
     g->smem = sm;
     CK(fl::sweep_set_smem(sm));
     int occ = 0;
-    CK(fl::sweep_occupancy(g->block, g->smem, &occ));
+    CK(fl::sweep_occupancy(g->block, g->smem, CS, &occ));
     if (occ < 1) return fail(FL_ERR_CAPACITY, "engine kernel cannot be resident with this shared-memory footprint");
-    g->grid_cap = sms * occ;
+    g->grid_cap = CS > 1 ? occ : sms * occ;           // concurrent design points (clusters or CTAs)
     return FL_OK;
 }
 
@@ -357,7 +364,7 @@ int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stre
     if (pts->n_points <= 0) return FL_OK;
     int cs = pts->compute_streams;
     if (cs < 1 || cs > 4) return fail(FL_ERR_CAPACITY, "compute_streams must be 1..4 in this build");
-    int grid = pts->n_points < g->grid_cap ? pts->n_points : g->grid_cap;
+    int grid = pts->n_points < g->grid_cap ? pts->n_points : g->grid_cap;   // design points in flight
     int rc = ensure_scratch(g, grid);
     if (rc) return rc;
     fl::DevPoints dp;
@@ -379,7 +386,8 @@ int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stre
     dout.ev_end = out->ev_end;
     dout.link_busy = out->link_busy;
     dout.link_cap = out->link_cap;
-    CK(fl::launch_sweep(cs == 3 ? 4 : cs, grid, g->block, g->smem, stream, g->dg, dp, dout, g->sc));
+    CK(fl::launch_sweep(cs == 3 ? 4 : cs, grid * g->cluster, g->block, g->smem, stream, g->cluster, g->dg, dp, dout,
+                        g->sc));
     return FL_OK;
 }
 

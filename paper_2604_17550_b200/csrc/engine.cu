@@ -36,6 +36,7 @@
 // each expression is the reference's Python evaluation order with no FMA
 // contraction.  Times are int64 ns.
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -43,6 +44,8 @@
 #include "engine_internal.h"
 
 namespace fl {
+
+namespace cg = cooperative_groups;
 
 // ------------------------------------------------------------------ costs
 
@@ -134,6 +137,10 @@ struct Shared {
     int ncomp;
     int nmcomp;
     int flag;
+    // cluster variant: per-CTA partial results, written by every CTA of the cluster (DSMEM)
+    uint64_t xkmin[2][16];
+    int64_t xvmax[2][16];
+    int xvor[2][16];
 };
 
 // Warp min of keys (time << 14 | rank).  Ranks step in lockstep most of the
@@ -169,6 +176,57 @@ __device__ __forceinline__ int64_t block_max_i64(int64_t v, Shared &sh, int &par
 #pragma unroll
     for (int o = 16; o; o >>= 1) { int64_t w = __shfl_xor_sync(FULL, v, o); v = w > v ? w : v; }
     return v;
+}
+
+// A design point with more ranks than one CTA holds runs on a thread-block
+// cluster (one CTA per 1024 ranks); its reductions and barriers span the
+// cluster through distributed shared memory.  CL selects that variant.  The
+// per-CTA partials are double-buffered on the same parity as the block-level
+// buffers, so each buffer is reused only after another cluster barrier.
+template <bool CL>
+__device__ __forceinline__ void gsync() {
+    if (CL) cg::this_cluster().sync();
+    else __syncthreads();
+}
+
+template <bool CL>
+__device__ __forceinline__ uint64_t gmin_key(uint64_t v, Shared &sh, int &par) {
+    v = block_min_u64(v, sh, par);
+    if (!CL) return v;
+    cg::cluster_group cl = cg::this_cluster();
+    const int n = (int)cl.num_blocks(), me = (int)cl.block_rank(), q = par ^ 1;
+    if ((int)threadIdx.x < n) *cl.map_shared_rank(&sh.xkmin[q][me], (int)threadIdx.x) = v;
+    cl.sync();
+    uint64_t m = KINF;
+    for (int j = 0; j < n; j++) m = sh.xkmin[q][j] < m ? sh.xkmin[q][j] : m;
+    return m;
+}
+
+template <bool CL>
+__device__ __forceinline__ int64_t gmax_i64(int64_t v, Shared &sh, int &par) {
+    v = block_max_i64(v, sh, par);
+    if (!CL) return v;
+    cg::cluster_group cl = cg::this_cluster();
+    const int n = (int)cl.num_blocks(), me = (int)cl.block_rank(), q = par ^ 1;
+    if ((int)threadIdx.x < n) *cl.map_shared_rank(&sh.xvmax[q][me], (int)threadIdx.x) = v;
+    cl.sync();
+    int64_t m = INT64_MIN;
+    for (int j = 0; j < n; j++) m = sh.xvmax[q][j] > m ? sh.xvmax[q][j] : m;
+    return m;
+}
+
+template <bool CL>
+__device__ __forceinline__ int gor(int v, Shared &sh, int &par) {
+    v = __syncthreads_or(v);
+    if (!CL) return v;
+    cg::cluster_group cl = cg::this_cluster();
+    const int n = (int)cl.num_blocks(), me = (int)cl.block_rank(), q = par;
+    par ^= 1;
+    if ((int)threadIdx.x < n) *cl.map_shared_rank(&sh.xvor[q][me], (int)threadIdx.x) = v;
+    cl.sync();
+    int m = 0;
+    for (int j = 0; j < n; j++) m |= sh.xvor[q][j];
+    return m;
 }
 
 // ---------------------------------------------------------- rank state
@@ -207,6 +265,12 @@ enum { ST_COMP = 0, ST_OVL, ST_CUR, ST_PEAK, ST_FIN, ST_N };
 // `done` lives in shared memory when it fits.
 struct Ctx {
     int R;
+    int RL;                         // ranks owned by this CTA
+    int SR;                         // stride of the shared per-rank arrays (blockDim)
+    int base;                       // first rank owned by this CTA (clusters of CTAs share a design point)
+    int BR, DR;                     // strides of the touched / done bitmaps (RL in shared memory, else R)
+    int crank, CS;                  // this CTA's rank in its cluster, cluster size (1 without clusters)
+    bool lead_cta;                  // the cluster's first CTA (its thread 0 does the serial work)
     uint64_t *done, *rdyc, *rdyh, *due;
     uint64_t *touched;              // [word][rank]: accumulator written in this design point
     int64_t *cp;                    // [max_nodes][R]
@@ -236,7 +300,28 @@ constexpr int32_t MSG_ALLOC = 1 << 30;   // mlist entry flag: the endpoint's out
 // Per-thread rank identity: element w of rank r in a [w][R] array is at w * R + r.
 struct Lane {
     int r, nb, tb;
+    int lr;                         // rank index within this CTA (shared-memory arrays)
+    int br, dr;                     // rank index for the touched / done bitmaps (lr in shared memory, else r)
 };
+
+// Per-rank indices and strides.  Bit 16 of K marks the cluster variant, whose
+// shared-memory arrays and bitmaps cover only this CTA's ranks (index lr,
+// stride blockDim); a single CTA indexes everything by rank (index r, stride R).
+template <int K> __device__ __forceinline__ int lidx(const Lane &L) { return (K & 16) ? L.lr : L.r; }
+// R is the caller's register copy of c.R (Ctx lives in shared memory, and a
+// re-read after every shared store would cost an LDS per access).
+template <int K> __device__ __forceinline__ int64_t &stat_ref(const Ctx &c, const Lane &L, int R, int k) {
+    if constexpr ((K & 16) != 0) return c.stat[k * c.SR + L.lr];
+    else return c.stat[k * R + L.r];
+}
+template <int K> __device__ __forceinline__ uint64_t &done_ref(const Ctx &c, const Lane &L, int R, int w) {
+    if constexpr ((K & 16) != 0) return c.done[w * c.DR + L.dr];
+    else return c.done[w * R + L.r];
+}
+template <int K> __device__ __forceinline__ uint64_t &touch_ref(const Ctx &c, const Lane &L, int R, int w) {
+    if constexpr ((K & 16) != 0) return c.touched[w * c.BR + L.br];
+    else return c.touched[w * R + L.r];
+}
 
 // A node set with its minimum cached in a register and the rest in a global
 // bitmap (+ register summary of non-empty words).  Invariant: head < every
@@ -292,10 +377,6 @@ __device__ __forceinline__ int bm_peek(const uint64_t *b, int R, int r, uint64_t
     return (w << 6) | (__ffsll((long long)b[w * R + r]) - 1);
 }
 
-__device__ __forceinline__ bool bm_has(const uint64_t *b, int R, int r, int idx) {
-    return (b[(idx >> 6) * R + r] >> (idx & 63)) & 1ull;
-}
-
 __device__ __forceinline__ void ms_insert(MinSet &m, uint64_t *b, int R, int r, int idx) {
     if (m.head < 0) {
         m.head = idx;
@@ -349,7 +430,7 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
         { const uint4 xb = rec_b(g, L.nb + x); s.alloc_t += rec_u64(xb.z, xb.w); }
         record(g, o, cfg, L.r, x, t, e);
         if ((K & 7) == 1 && e > t) {      // one compute stream: its busy intervals are disjoint
-            c.stat[ST_COMP * R + L.r] += e - t;
+            stat_ref<K>(c, L, R, ST_COMP) += e - t;
             s.comp_a = s.commcum;
         }
 #pragma unroll
@@ -407,16 +488,19 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
                                           const Step &f, int x, int64_t t) {
     const int R = c.R;
     const uint4 xa = rec_a(g, L.nb + x), xc = rec_c(g, L.nb + x);
-    if (g.needs_done) c.done[(x >> 6) * R + L.r] |= 1ull << (x & 63);
+    if (g.needs_done) done_ref<K>(c, L, R, x >> 6) |= 1ull << (x & 63);
     s.done_cnt++;
     s.pop_seq++;
-    c.stat[ST_FIN * R + L.r] = t;
+    stat_ref<K>(c, L, R, ST_FIN) = t;
     s.free_t += rec_u64(xc.x, xc.y);
     for (uint32_t q = xa.z; q < xa.w; q++) {
         const int tt = L.tb + g.free_tens[q];
         const int2 cr = g.tens_rng[tt];
         bool all = true;
-        for (int u = cr.x; u < cr.y && all; u++) all = bm_has(c.done, R, L.r, g.tens_cons[u]);
+        for (int u = cr.x; u < cr.y && all; u++) {
+            const int q = g.tens_cons[u];
+            all = (done_ref<K>(c, L, R, q >> 6) >> (q & 63)) & 1;
+        }
         if (all) s.free_t += g.tens_bytes[tt];
     }
     const uint64_t fx = (uint64_t)c.cp[x * R + L.r] & VAL48;    // this node's critical-path finish
@@ -428,7 +512,7 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
         int64_t *slot = c.cp + (d * R + L.r);
         // first dependency to complete: the word holds nothing of this design point,
         // so skip reading it (a DRAM round trip on the critical chain)
-        uint64_t &tw = c.touched[(d >> 6) * R + L.r];
+        uint64_t &tw = touch_ref<K>(c, L, R, d >> 6);
         const uint64_t tb = 1ull << (d & 63);
         uint64_t a;
         if (tw & tb) {
@@ -458,7 +542,7 @@ __device__ __forceinline__ void load_head(const Ctx &c, const Lane &L, Rank<K> &
 // After reservations: pick up comm-FIFO entries appended for this rank.
 template <int K>
 __device__ __forceinline__ void refresh_ring(const Ctx &c, const Lane &L, Rank<K> &s) {
-    const int tail = c.ring_tail[L.r];
+    const int tail = c.ring_tail[lidx<K>(L)];
     if (tail != s.ring_seen) {
         const bool was_empty = s.ring_head == s.ring_seen;
         s.ring_seen = tail;
@@ -492,7 +576,7 @@ __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, cons
         if (s.occ_n[q] >= 0 && s.occ_e[q] == t) {
             ms_insert(s.due, c.due, R, L.r, s.occ_n[q]);
             s.occ_n[q] = -1;
-            if ((K & 7) == 1) c.stat[ST_OVL * R + L.r] += s.commcum - s.comp_a;   // comm time under [start, t)
+            if ((K & 7) == 1) stat_ref<K>(c, L, R, ST_OVL) += s.commcum - s.comp_a;   // comm time under [start, t)
         }
     while (s.ring_head < s.ring_seen && s.head_e == t) {
         if (!s.head_alloc) { const uint4 hb = rec_b(g, L.nb + s.head_node); s.alloc_t += rec_u64(hb.z, hb.w); }  // zero-length: starts now
@@ -547,10 +631,10 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
         }
     }
     if (s.alloc_t | s.free_t) {
-        int64_t cur = c.stat[ST_CUR * R + L.r] + s.alloc_t;
-        const int64_t pk = c.stat[ST_PEAK * R + L.r];
-        if (cur > pk) c.stat[ST_PEAK * R + L.r] = cur;
-        c.stat[ST_CUR * R + L.r] = cur - s.free_t;
+        int64_t cur = stat_ref<K>(c, L, R, ST_CUR) + s.alloc_t;
+        const int64_t pk = stat_ref<K>(c, L, R, ST_PEAK);
+        if (cur > pk) stat_ref<K>(c, L, R, ST_PEAK) = cur;
+        stat_ref<K>(c, L, R, ST_CUR) = cur - s.free_t;
         s.alloc_t = s.free_t = 0;
     }
     if (tnew == TINF) return;
@@ -562,8 +646,8 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
 #pragma unroll
         for (int q = 0; q < (K & 7); q++) comp_on |= s.occ_n[q] >= 0;
         if (comp_on) {
-            c.stat[ST_COMP * R + L.r] += dt;
-            if (comm_on) c.stat[ST_OVL * R + L.r] += dt;
+            stat_ref<K>(c, L, R, ST_COMP) += dt;
+            if (comm_on) stat_ref<K>(c, L, R, ST_OVL) += dt;
         }
     }
 }
@@ -669,14 +753,16 @@ __device__ void reserve_msgs(const DevGraph &g, const DevOut &o, const Ctx &c, i
 }
 
 // Reserve the comm streams of every instance completed in this step, in the
-// reference's order (simulator.py:298-309); block-wide.  Returns the largest
-// critical-path finish among them.
-template <bool MSG>
+// reference's order (simulator.py:298-309), block- (or cluster-) wide; then the
+// step's messages (simulator.py:310-327).  Returns the largest critical-path
+// finish among them.
+template <bool MSG, bool CL>
 __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, const Ctx &c, Shared &sh, int &par,
-                                          int64_t t, bool init, int cfg, uint64_t epoch, int nc, int topo, int cols) {
+                                          int64_t t, bool init, int cfg, uint64_t epoch,
+                                          int nc, int nmc, int topo, int cols) {
     int64_t cpm = 0;
-    if (nc > 1) {
-        if (threadIdx.x == 0) {
+    if (nc > 1 || CL) {             // one thread orders the list (shared by the cluster's CTAs)
+        if ((!CL || c.lead_cta) && threadIdx.x == 0) {
             for (int a = 1; a < nc; a++) {
                 const int x = c.complist[a];
                 int b = a - 1;
@@ -684,9 +770,9 @@ __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, co
                 c.complist[b + 1] = x;
             }
         }
-        __syncthreads();
+        gsync<CL>();
     }
-    const int R = c.R;
+    const int R = c.R, RL = CL ? c.RL : c.R, base = CL ? c.base : 0;
     // While every collective so far spanned all ranks, every comm stream ends at the
     // same time and a full-world reservation needs no reduction (simulator.py:300-303).
     bool uni = sh.cend_uniform;
@@ -699,22 +785,25 @@ __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, co
         if (full_node >= 0 && uni) {
             s = cend > t ? cend : t;
         } else {
-            __syncthreads();        // comm ends written by the previous reservation
+            gsync<CL>();            // comm ends written by the previous reservation
             int64_t local = t;
             for (int64_t j = threadIdx.x; j < nm; j += blockDim.x) {
-                const int64_t ce = c.comm_end[g.inst_mem_rank[m0 + j]];
+                const int lm = g.inst_mem_rank[m0 + j] - base;
+                if (lm < 0 || lm >= RL) continue;       // another CTA's rank
+                const int64_t ce = c.comm_end[lm];
                 local = ce > local ? ce : local;
             }
-            s = block_max_i64(local, sh, par);
+            s = gmax_i64<CL>(local, sh, par);
         }
         const int64_t e = s + c.inst_dur[i];
         const int64_t cpv = c.inst_cpmax[i] + c.inst_dur[i];
         cpm = cpv > cpm ? cpv : cpm;
-        if (threadIdx.x == 0) { c.inst_s[i] = s; c.inst_e[i] = e; }
+        if ((!CL || c.lead_cta) && threadIdx.x == 0) { c.inst_s[i] = s; c.inst_e[i] = e; }
         if (full_node >= 0) {
-            for (int m = threadIdx.x; m < R; m += blockDim.x) {
-                c.comm_end[m] = e;
-                const int slot = c.ring_tail[m]++;
+            for (int lm = threadIdx.x; lm < RL; lm += blockDim.x) {
+                const int m = base + lm;
+                c.comm_end[lm] = e;
+                const int slot = c.ring_tail[lm]++;
                 c.ring_inst[slot * R + m] = i;
                 c.ring_node[slot * R + m] = full_node;
                 c.cp[full_node * R + m] = (int64_t)(epoch | (uint64_t)cpv);
@@ -725,73 +814,99 @@ __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, co
         } else {
             for (int64_t j = threadIdx.x; j < nm; j += blockDim.x) {
                 const int m = g.inst_mem_rank[m0 + j], node = g.inst_mem_node[m0 + j];
-                c.comm_end[m] = e;
-                const int slot = c.ring_tail[m]++;
+                const int lm = m - base;
+                if (lm < 0 || lm >= RL) continue;
+                c.comm_end[lm] = e;
+                const int slot = c.ring_tail[lm]++;
                 c.ring_inst[slot * R + m] = i;
                 c.ring_node[slot * R + m] = node;
                 c.cp[node * R + m] = (int64_t)(epoch | (uint64_t)cpv);
                 record(g, o, cfg, m, node, s, e);
             }
             uni = false;
-            __syncthreads();        // the next reservation reads these comm ends
+            gsync<CL>();            // the next reservation reads these comm ends
         }
     }
-    __syncthreads();
+    gsync<CL>();                    // every CTA has read the counters and the list
     if (threadIdx.x == 0) {
-        sh.ncomp = 0;
         sh.cend_uniform = uni;
         sh.cend_all = cend;
-        if (MSG && sh.nmcomp) {
-            reserve_msgs(g, o, c, sh.nmcomp, init, topo, cols, cfg, epoch, cpm);
-            sh.nmcomp = 0;
-        }
     }
-    __syncthreads();
+    if ((!CL || c.lead_cta) && threadIdx.x == 0) {
+        if (CL) *c.ncomp = 0; else sh.ncomp = 0;
+        if (MSG && nmc) reserve_msgs(g, o, c, nmc, init, topo, cols, cfg, epoch, cpm);
+        if (MSG) { if (CL) *c.nmcomp = 0; else sh.nmcomp = 0; }
+    }
+    gsync<CL>();
     return cpm;
 }
 
 // Barrier, then reserve whatever completed since the last reservation.
-template <bool MSG>
+template <bool MSG, bool CL>
 __device__ __forceinline__ int64_t reserve(const DevGraph &g, const DevOut &o, const Ctx &c, Shared &sh, int &par,
-                                           int64_t t, bool init, int cfg, uint64_t epoch, int topo, int cols) {
-    __syncthreads();
-    const int nc = sh.ncomp;
-    return (nc | (MSG ? sh.nmcomp : 0)) ? reserve_n<MSG>(g, o, c, sh, par, t, init, cfg, epoch, nc, topo, cols) : 0;
+                                           int64_t t, bool init, int cfg, uint64_t epoch,
+                                           int topo, int cols) {
+    gsync<CL>();
+    const int nc = CL ? *c.ncomp : sh.ncomp, nmc = MSG ? (CL ? *c.nmcomp : sh.nmcomp) : 0;
+    return (nc | nmc) ? reserve_n<MSG, CL>(g, o, c, sh, par, t, init, cfg, epoch, nc, nmc, topo, cols) : 0;
 }
 
-template <int K>
+// Zero this CTA's ranks' columns of a [rows][R] array (clusters split a point's ranks).
+template <bool CL, typename T>
+__device__ __forceinline__ void zero_cols(T *a, size_t rows, int R, int base, int RL) {
+    if constexpr (!CL) {
+        for (size_t i = threadIdx.x; i < rows * R; i += blockDim.x) a[i] = 0;
+    } else {
+        for (size_t i = threadIdx.x; i < rows * RL; i += blockDim.x) a[(i / RL) * R + base + (i % RL)] = 0;
+    }
+}
+
+template <int K, bool CL>
 __global__ void __launch_bounds__(1024, 1)
     sweep_kernel(const __grid_constant__ DevGraph g, const __grid_constant__ DevPoints p,
                  const __grid_constant__ DevOut o, const __grid_constant__ DevScratch sc) {
     extern __shared__ __align__(16) unsigned char smem[];
     Shared &sh = *reinterpret_cast<Shared *>(smem);
+    constexpr int KK = K | (CL ? 16 : 0);   // helpers see the cluster variant through K's bit 16
     const int R = g.R;
     const int tid = threadIdx.x, bd = blockDim.x;
+    const int CS = CL ? (int)cg::this_cluster().num_blocks() : 1;
+    const int crank = CL ? (int)cg::this_cluster().block_rank() : 0;
+    const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;     // this cluster, clusters in the grid
+    const int base_r = crank * bd;
+    const int RL = R - base_r < bd ? R - base_r : bd;          // ranks owned by this CTA
 
-    // ---- carve shared memory and this CTA's scratch slot ----
+    // ---- carve shared memory and this cluster's scratch slot ----
     // (the pointer table lives in shared memory: it is block-uniform and would
     // otherwise pin ~34 registers per thread)
     __shared__ Ctx c_sh;
     Ctx &c = c_sh;
     if (tid == 0) {
         c.R = R;
+        c.RL = RL;
+        c.SR = CL ? bd : R;
+        c.base = base_r;
+        c.crank = crank;
+        c.CS = CS;
         unsigned char *sp = smem + sc.sm_off_dyn;
         c.comm_end = reinterpret_cast<int64_t *>(sp);
-        c.stat = c.comm_end + R;
-        c.ring_tail = reinterpret_cast<int32_t *>(c.stat + ST_N * R);
-        unsigned char *base = sc.base + (size_t)blockIdx.x * sc.slot_bytes;
+        c.stat = c.comm_end + bd;
+        c.ring_tail = reinterpret_cast<int32_t *>(c.stat + ST_N * bd);
+        unsigned char *base = sc.base + (size_t)cid * sc.slot_bytes;
         const size_t words = (size_t)g.max_words * R;
         uint64_t *gbits = reinterpret_cast<uint64_t *>(base + sc.off_bits);
         c.rdyc = gbits;
         c.rdyh = gbits + words;
         c.due = gbits + 2 * words;
         c.done = sc.done_in_smem ? reinterpret_cast<uint64_t *>(smem + sc.sm_off_done) : gbits + 3 * words;
+        c.DR = sc.done_in_smem ? bd : R;
         c.touched = sc.touch_in_smem ? reinterpret_cast<uint64_t *>(smem + sc.sm_off_touch) : gbits + 4 * words;
+        c.BR = sc.touch_in_smem ? bd : R;
         c.cp = reinterpret_cast<int64_t *>(base + sc.off_cp);
         c.ring_inst = reinterpret_cast<int32_t *>(base + sc.off_ring);
         c.ring_node = c.ring_inst + (size_t)g.coll_stride * R;
         c.dur = sc.dur_in_smem ? reinterpret_cast<int64_t *>(smem + sc.sm_off_dur)
-                               : reinterpret_cast<int64_t *>(base + sc.off_dur);
+                               : reinterpret_cast<int64_t *>(base + sc.off_dur) + (size_t)crank * g.total_nodes;
         unsigned char *ib = sc.inst_in_smem ? smem + sc.sm_off_inst : base + sc.off_inst;
         const int NI = g.n_inst;
         c.inst_dur = reinterpret_cast<int64_t *>(ib);
@@ -801,8 +916,10 @@ __global__ void __launch_bounds__(1024, 1)
         c.inst_ckey = reinterpret_cast<unsigned long long *>(c.inst_cpmax + NI);
         c.inst_wait = reinterpret_cast<int32_t *>(c.inst_ckey + NI);
         c.complist = c.inst_wait + NI;
-        c.ncomp = &sh.ncomp;
-        c.nmcomp = &sh.nmcomp;
+        int *ctr = reinterpret_cast<int *>(base + sc.off_ctr);   // cluster-wide completion counters
+        c.ncomp = CL ? ctr : &sh.ncomp;
+        c.nmcomp = CL ? ctr + 1 : &sh.nmcomp;
+        c.lead_cta = crank == 0;
         const int M = g.n_msg;
         int64_t *mb = reinterpret_cast<int64_t *>(base + sc.off_msg);
         c.msg_sendt = mb;
@@ -823,13 +940,16 @@ __global__ void __launch_bounds__(1024, 1)
         c.mlist_node = c.mlist + (size_t)g.p2p_stride * R;
     }
     __syncthreads();
+    const bool is_leader = crank == 0 && tid == 0;      // writes the point's row
     uint64_t *gbits = c.rdyc;
-    const size_t words = (size_t)g.max_words * R;
     const int NI = g.n_inst;
 
-    const bool active = tid < R;
+    const bool active = tid < RL;
     Lane L;
-    L.r = active ? tid : 0;
+    L.r = active ? base_r + tid : base_r;
+    L.lr = CL ? tid : L.r;
+    L.br = sc.touch_in_smem ? tid : L.r;
+    L.dr = sc.done_in_smem ? tid : L.r;
     {
         const int st = g.rank_struct[L.r];
         L.nb = g.s_node_off[st];
@@ -839,24 +959,26 @@ __global__ void __launch_bounds__(1024, 1)
 
     int par = 0;
     if (tid == 0) { sh.parity = 0; sh.ncomp = 0; sh.nmcomp = 0; sh.flag = 0; }
-    // the three global bitmaps are all-zero after a point that ran to completion;
+    if (CL && is_leader) { c.ncomp[0] = 0; c.nmcomp[0] = 0; }
+    // the global bitmaps are all-zero after a point that ran to completion;
     // clear them once up front and again only after a point that did not
-    for (size_t i = tid; i < (sc.done_in_smem ? 3 : 4) * words; i += bd) gbits[i] = 0;
+    zero_cols<CL>(gbits, (size_t)g.max_words * 5, R, base_r, RL);  // ready/due/done/touched columns
     bool dirty = false;
-    const size_t acc_words = (size_t)g.max_nodes * R;
-    for (size_t i = tid; i < acc_words; i += bd) c.cp[i] = 0;   // epoch 0 = empty
+    zero_cols<CL>(c.cp, (size_t)g.max_nodes, R, base_r, RL);        // epoch 0 = empty
+    gsync<CL>();
     unsigned epoch = 0;
     bool have_dur = false;          // durations of the previous point's device, reused when unchanged
     double dev_pk = 0.0, dev_ef = 0.0;
     int dev_zdur = 0;
+    const int gt = crank * bd + tid, gstride = CS * bd;        // cluster-wide thread index / stride
 
-    for (int cfg = blockIdx.x; cfg < p.n; cfg += gridDim.x) {
+    for (int cfg = cid; cfg < p.n; cfg += ncl) {
         // ---- cost stage (K1): this point's durations ----
         const int algo = p.algo[cfg], topo = p.topo_kind[cfg];
         const double bwv = p.bw[cfg];
         const int64_t lat = p.latency[cfg];
         int bad = 0, zero = 0, cap_bad = 0;
-        for (int i = tid; i < NI; i += bd) {
+        for (int i = gt; i < NI; i += gstride) {
             int64_t d = coll_time(g, i, algo, topo, bwv, lat, p.rows[cfg], p.cols[cfg]);
             if (d < 0) { bad = 1; d = 0; }
             zero |= d == 0;
@@ -871,7 +993,7 @@ __global__ void __launch_bounds__(1024, 1)
             const double beta = __ddiv_rn(1e9, bwv);
             const int cols = p.cols[cfg];
             if (topo == FL_MESH2D && (cols <= 0 || 4LL * p.rows[cfg] * cols > c.link_cap)) cap_bad = 1;
-            for (int m = tid; m < g.n_msg; m += bd) {
+            for (int m = gt; m < g.n_msg; m += gstride) {
                 const int64_t xf = cap_bad ? 0 : transfer_ns(g, topo, cols, g.msg_send_rank[m], g.msg_recv_rank[m],
                                                          g.msg_bytes[m], lat, beta);
                 zero |= xf == 0;
@@ -879,8 +1001,8 @@ __global__ void __launch_bounds__(1024, 1)
                 c.msg_wait[m] = 2;
                 c.msg_ckey[m] = 0ull;
             }
-            for (int l = tid; l < c.link_cap; l += bd) { c.link_free[l] = 0; c.link_busy[l] = -1; }
-            for (int r = tid; r < R; r += bd) c.mcount[r] = 0;
+            for (int l = gt; l < c.link_cap; l += gstride) { c.link_free[l] = 0; c.link_busy[l] = -1; }
+            if (active) c.mcount[L.r] = 0;
         }
         const bool recost = p.peak_flops != nullptr;
         const double pk = recost ? p.peak_flops[cfg] : 0.0, ef = recost ? p.efficiency[cfg] : 0.0;
@@ -898,31 +1020,36 @@ __global__ void __launch_bounds__(1024, 1)
                 zdur |= rec_kind(nb_) == FL_COMP || (rec_kind(nb_) == FL_HOST && !rec_static(nb_));
             }
         }
-        if (dirty) for (size_t i = tid; i < 3 * words; i += bd) gbits[i] = 0;
-        if (g.needs_done) for (size_t i = tid; i < words; i += bd) c.done[i] = 0;
-        for (size_t i = tid; i < words; i += bd) c.touched[i] = 0;
-        if (tid == 0) { sh.cend_all = 0; sh.cend_uniform = 1; }
-        for (int r = tid; r < R; r += bd) {
-            c.comm_end[r] = 0;
-            c.ring_tail[r] = 0;
-#pragma unroll
-            for (int k = 0; k < ST_N; k++) c.stat[k * R + r] = 0;
+        if (dirty) zero_cols<CL>(gbits, (size_t)g.max_words * 3, R, base_r, RL);
+        if (g.needs_done) {
+            if (sc.done_in_smem) for (size_t i = tid; i < (size_t)g.max_words * bd; i += bd) c.done[i] = 0;
+            else zero_cols<CL>(c.done, (size_t)g.max_words, R, base_r, RL);
         }
-        bad = __syncthreads_or(bad);
-        cap_bad = __syncthreads_or(cap_bad);
+        if (sc.touch_in_smem) for (size_t i = tid; i < (size_t)g.max_words * bd; i += bd) c.touched[i] = 0;
+        else zero_cols<CL>(c.touched, (size_t)g.max_words, R, base_r, RL);
+        if (tid == 0) { sh.cend_all = 0; sh.cend_uniform = 1; }
+        for (int lr = tid; lr < bd; lr += bd) {
+            c.comm_end[lr] = 0;
+            c.ring_tail[lr] = 0;
+#pragma unroll
+            for (int k = 0; k < ST_N; k++) c.stat[k * bd + lr] = 0;
+        }
+        bad = gor<CL>(bad, sh, par);
+        cap_bad = gor<CL>(cap_bad, sh, par);
         if (cap_bad) bad = 2;
-        zero = __syncthreads_or(zero);
-        zdur = __syncthreads_or(zdur);
+        zero = gor<CL>(zero, sh, par);
+        zdur = gor<CL>(zdur, sh, par);
         dev_zdur = zdur;
         if (bad) {
-            if (tid == 0) o.status[cfg] = bad == 2 ? FL_ERR_CAPACITY : FL_ERR_UNSUPPORTED_ALGO;
+            if (is_leader) o.status[cfg] = bad == 2 ? FL_ERR_CAPACITY : FL_ERR_UNSUPPORTED_ALGO;
             dirty = false;
+            gsync<CL>();
             continue;
         }
         if (++epoch == 64) {       // 6-bit tags wrap: start a fresh accumulator table
-            for (size_t i = tid; i < acc_words; i += bd) c.cp[i] = 0;
+            zero_cols<CL>(c.cp, (size_t)g.max_nodes, R, base_r, RL);
             epoch = 1;
-            __syncthreads();
+            gsync<CL>();
         }
         Step f;
         f.step = 0;
@@ -931,7 +1058,7 @@ __global__ void __launch_bounds__(1024, 1)
         f.fold = g.fold_ok && !zero && !zdur;
 
         // ---- per-rank state ----
-        Rank<K> s;
+        Rank<KK> s;
         s.due.head = s.rc.head = s.rh.head = -1;
         s.due.sum = s.rc.sum = s.rh.sum = 0;
         s.host_slot = 0; s.host_e = 0; s.host_n = -1;
@@ -947,6 +1074,7 @@ __global__ void __launch_bounds__(1024, 1)
         s.comp_a = 0;
         s.done_cnt = 0;
         s.pop_seq = 0;
+        constexpr bool MSG = (K & 8) != 0;
 
         // ---- t = 0: initial dispatch + start phase (simulator.py:275-277) ----
         if (active) {
@@ -959,7 +1087,7 @@ __global__ void __launch_bounds__(1024, 1)
             }
             start_phase(g, o, c, L, s, 0, cfg);
         }
-        int64_t cpm = reserve<(K & 8) != 0>(g, o, c, sh, par, 0, true, cfg, f.epoch, topo, p.cols[cfg]);
+        int64_t cpm = reserve<MSG, CL>(g, o, c, sh, par, 0, true, cfg, f.epoch, topo, p.cols[cfg]);
         if (active) refresh_ring(c, L, s);
         f.init = 0;
         if (f.fold) {
@@ -991,7 +1119,7 @@ __global__ void __launch_bounds__(1024, 1)
                     for (int q = g.static_off[st]; q < g.static_off[st + 1]; q++)
                         record(g, o, cfg, L.r, g.static_list[q], 0, 0);
             }
-            const int64_t v = reserve<(K & 8) != 0>(g, o, c, sh, par, 0, false, cfg, f.epoch, topo, p.cols[cfg]);
+            const int64_t v = reserve<MSG, CL>(g, o, c, sh, par, 0, false, cfg, f.epoch, topo, p.cols[cfg]);
             cpm = v > cpm ? v : cpm;
             if (active) refresh_ring(c, L, s);
         }
@@ -1003,18 +1131,18 @@ __global__ void __launch_bounds__(1024, 1)
         for (;;) {
             int64_t nt = active ? next_time(g, c, L, s, tcur) : TINF;
             uint64_t key = nt == TINF ? KINF : ((uint64_t)(nt < TCAP ? nt : TCAP) << 14) | (uint64_t)L.r;
-            uint64_t kmin = block_min_u64(key, sh, par);
+            uint64_t kmin = gmin_key<CL>(key, sh, par);
             // collectives completed by the previous step's pops: reserve them now (the
             // reduction's barrier made every arrival visible), then re-derive the next time
-            const int nc = sh.ncomp;
-            if (nc | ((K & 8) ? sh.nmcomp : 0)) {
-                const int64_t v = reserve_n<(K & 8) != 0>(g, o, c, sh, par, tcur, false, cfg, f.epoch, nc, topo,
-                                                          p.cols[cfg]);
+            const int nc = CL ? *c.ncomp : sh.ncomp, nmc = MSG ? (CL ? *c.nmcomp : sh.nmcomp) : 0;
+            if (nc | nmc) {
+                const int64_t v = reserve_n<MSG, CL>(g, o, c, sh, par, tcur, false, cfg, f.epoch, nc, nmc,
+                                                     topo, p.cols[cfg]);
                 cpm = v > cpm ? v : cpm;
                 if (active) refresh_ring(c, L, s);
                 nt = active ? next_time(g, c, L, s, tcur) : TINF;
                 key = nt == TINF ? KINF : ((uint64_t)(nt < TCAP ? nt : TCAP) << 14) | (uint64_t)L.r;
-                kmin = block_min_u64(key, sh, par);
+                kmin = gmin_key<CL>(key, sh, par);
             }
             if (kmin == KINF) break;
             const int64_t t = (int64_t)(kmin >> 14);
@@ -1042,7 +1170,7 @@ __global__ void __launch_bounds__(1024, 1)
                 for (;;) {
                     const uint64_t k2 = (active && s.due.head >= 0) ? (((uint64_t)L.r << 13) | (uint64_t)s.due.head)
                                                                      : KINF;
-                    const uint64_t m2 = block_min_u64(k2, sh, par);
+                    const uint64_t m2 = gmin_key<CL>(k2, sh, par);
                     if (m2 == KINF) break;
                     f.step++;
                     if (active && (int)(m2 >> 13) == L.r) {
@@ -1051,7 +1179,8 @@ __global__ void __launch_bounds__(1024, 1)
                         pop_event(g, c, L, s, f, x, t);
                     }
                     if (active) start_phase(g, o, c, L, s, t, cfg);
-                    const int64_t v = reserve<(K & 8) != 0>(g, o, c, sh, par, t, false, cfg, f.epoch, topo, p.cols[cfg]);
+                    const int64_t v = reserve<MSG, CL>(g, o, c, sh, par, t, false, cfg, f.epoch, topo,
+                                                       p.cols[cfg]);
                     cpm = v > cpm ? v : cpm;
                     if (active) {
                         refresh_ring(c, L, s);
@@ -1064,31 +1193,31 @@ __global__ void __launch_bounds__(1024, 1)
 
         // ---- row: reductions over ranks (cli.py:336-341) ----
         int dead = active && s.done_cnt != my_n;
-        dead = __syncthreads_or(dead | overflow);
+        dead = gor<CL>(dead | overflow, sh, par);
         dirty = dead != 0;
         int64_t vals[6] = {0, 0, 0, 0, 0, 0};
         if (active) {
             const int64_t comm = s.commcum;
-            vals[0] = c.stat[ST_FIN * R + L.r];
+            vals[0] = stat_ref<KK>(c, L, R, ST_FIN);
             vals[1] = s.cpmax > cpm ? s.cpmax : cpm;
-            vals[2] = c.stat[ST_COMP * R + L.r];
+            vals[2] = stat_ref<KK>(c, L, R, ST_COMP);
             vals[3] = comm;
-            vals[4] = comm - c.stat[ST_OVL * R + L.r];
-            vals[5] = c.stat[ST_PEAK * R + L.r];
+            vals[4] = comm - stat_ref<KK>(c, L, R, ST_OVL);
+            vals[5] = stat_ref<KK>(c, L, R, ST_PEAK);
             if (o.rank_stats) {
                 int64_t *rs = o.rank_stats + ((size_t)cfg * R + L.r) * 5;
                 rs[0] = vals[0]; rs[1] = vals[2]; rs[2] = vals[3]; rs[3] = vals[4]; rs[4] = vals[5];
             }
         }
         for (int k = 0; k < 6; k++) {
-            const int64_t v = block_max_i64(vals[k], sh, par);
-            if (tid == 0) o.rows[(size_t)cfg * 6 + k] = v;
+            const int64_t v = gmax_i64<CL>(vals[k], sh, par);
+            if (is_leader) o.rows[(size_t)cfg * 6 + k] = v;
         }
-        if (tid == 0) o.status[cfg] = overflow ? FL_ERR_CAPACITY : dead ? FL_ERR_DEADLOCK : FL_OK;
-        if (o.link_busy)            // SimReport.link_busy_ns (simulator.py:321, :367)
+        if (is_leader) o.status[cfg] = overflow ? FL_ERR_CAPACITY : dead ? FL_ERR_DEADLOCK : FL_OK;
+        if (o.link_busy && crank == 0)   // SimReport.link_busy_ns (simulator.py:321, :367)
             for (int l = tid; l < o.link_cap; l += bd)
                 o.link_busy[(size_t)cfg * o.link_cap + l] = (g.n_msg && l < c.link_cap) ? c.link_busy[l] : -1;
-        __syncthreads();
+        gsync<CL>();
     }
 }
 
@@ -1141,28 +1270,66 @@ __global__ void cp_kernel(const __grid_constant__ DevGraph g, const __grid_const
 
 // ------------------------------------------------------------ host side
 
-cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t st, const DevGraph &g,
+template <int T>
+static cudaError_t launch_t(int grid, int block, size_t smem, cudaStream_t st, int cluster, const DevGraph &g,
+                            const DevPoints &p, const DevOut &o, const DevScratch &sc) {
+    if (cluster <= 1) {
+        sweep_kernel<T, false><<<grid, block, smem, st>>>(g, p, o, sc);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, sweep_kernel<T, true>, g, p, o, sc);
+}
+
+cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t st, int cluster, const DevGraph &g,
                          const DevPoints &p, const DevOut &o, const DevScratch &sc) {
     // template argument: compute streams (1, 2, 4) | 8 when the graphs carry SEND/RECV
     const int T = K | (g.n_msg > 0 ? 8 : 0);
-    if (T == 1) sweep_kernel<1><<<grid, block, smem, st>>>(g, p, o, sc);
-    else if (T == 2) sweep_kernel<2><<<grid, block, smem, st>>>(g, p, o, sc);
-    else if (T == 4) sweep_kernel<4><<<grid, block, smem, st>>>(g, p, o, sc);
-    else if (T == 9) sweep_kernel<9><<<grid, block, smem, st>>>(g, p, o, sc);
-    else if (T == 10) sweep_kernel<10><<<grid, block, smem, st>>>(g, p, o, sc);
-    else sweep_kernel<12><<<grid, block, smem, st>>>(g, p, o, sc);
-    return cudaGetLastError();
+    switch (T) {
+        case 1: return launch_t<1>(grid, block, smem, st, cluster, g, p, o, sc);
+        case 2: return launch_t<2>(grid, block, smem, st, cluster, g, p, o, sc);
+        case 4: return launch_t<4>(grid, block, smem, st, cluster, g, p, o, sc);
+        case 9: return launch_t<9>(grid, block, smem, st, cluster, g, p, o, sc);
+        case 10: return launch_t<10>(grid, block, smem, st, cluster, g, p, o, sc);
+        default: return launch_t<12>(grid, block, smem, st, cluster, g, p, o, sc);
+    }
 }
 
-cudaError_t sweep_occupancy(int block, size_t smem, int *occ) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, sweep_kernel<1>, block, smem);
+cudaError_t sweep_occupancy(int block, size_t smem, int cluster, int *occ) {
+    if (cluster <= 1) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, sweep_kernel<1, false>, block, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cluster);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaOccupancyMaxActiveClusters(occ, sweep_kernel<1, true>, &cfg);   // clusters, not blocks
 }
 
 cudaError_t sweep_set_smem(size_t smem) {
     cudaError_t e = cudaSuccess;
-    for (auto fn : {sweep_kernel<1>, sweep_kernel<2>, sweep_kernel<4>, sweep_kernel<9>, sweep_kernel<10>,
-                    sweep_kernel<12>})
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+#define FL_SET(T)                                                                                               \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<T, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    FL_SET(1) FL_SET(2) FL_SET(4) FL_SET(9) FL_SET(10) FL_SET(12)
+#undef FL_SET
     return e;
 }
 

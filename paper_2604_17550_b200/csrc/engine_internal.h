@@ -58,14 +58,15 @@ struct DevScratch {
     size_t slot_bytes, off_bits, off_cp, off_ring, off_dur, off_inst;
     // dynamic shared-memory layout (bytes from the start of the CTA's smem)
     size_t off_msg;              // message state, link state, per-rank in-flight lists
+    size_t off_ctr;              // cluster-wide completion counters
     int link_cap;
     unsigned sm_off_dyn, sm_off_done, sm_off_dur, sm_off_inst, sm_off_touch;
     int done_in_smem, dur_in_smem, inst_in_smem, touch_in_smem;
 };
 
-cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t st, const DevGraph &g,
+cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t st, int cluster, const DevGraph &g,
                          const DevPoints &p, const DevOut &o, const DevScratch &sc);
-cudaError_t sweep_occupancy(int block, size_t smem, int *occ);
+cudaError_t sweep_occupancy(int block, size_t smem, int cluster, int *occ);
 cudaError_t sweep_set_smem(size_t smem);
 size_t sweep_shared_header_bytes();
 cudaError_t launch_cp(const DevGraph &g, const DevPoints &p, int nv, const int32_t *order, const int32_t *vkind,

@@ -136,6 +136,11 @@ class DesignPoints:
         return DesignPoints(f(self.algo), f(self.topo_kind), f(self.bw), f(self.latency), f(self.rows),
                             f(self.cols), f(self.peak_flops), f(self.efficiency), self.compute_streams)
 
+    def take(self, idx) -> "DesignPoints":
+        f = lambda x: None if x is None else np.ascontiguousarray(x[idx])
+        return DesignPoints(f(self.algo), f(self.topo_kind), f(self.bw), f(self.latency), f(self.rows),
+                            f(self.cols), f(self.peak_flops), f(self.efficiency), self.compute_streams)
+
 
 def _ptr(a, typ):
     return None if a is None else a.ctypes.data_as(typ)

@@ -92,6 +92,19 @@ def c2_workload() -> Workload:
     return Workload("c2", "gpt2-small", "dp:64", pts, [p for p in pairs for _ in range(16 * 8)])
 
 
+def c4_workload() -> Workload:
+    """BASELINE config 4 at its rank count: 8192 ranks, 16384 points =
+    {switch:8192 + ring, mesh:64x128 + mesh-hier} x 128 bandwidths in
+    [10 GB/s, 1.8 TB/s] x 64 latencies in [100 ns, 20 us].  The reference's
+    synthesizer has no pipeline/3-D strategy (synth.py:29-32 in this package,
+    trainsim synth.py), so the graph is its largest family at that scale:
+    llama-70b-like fsdp:8192 (2080 nodes per rank).  A design point spans a
+    cluster of 8 CTAs."""
+    pairs = [("switch", "ring"), ("mesh", "mesh-hier")]
+    pts = _grid(pairs, log_grid(10e9, 1.8e12, 128), latency_grid(100, 20000, 64), (64, 128))
+    return Workload("c4", "llama-70b-like", "fsdp:8192", pts, [p for p in pairs for _ in range(128 * 64)])
+
+
 def workload_graphs(w: Workload):
     from .synth import GPT2_SMALL
     m = GPT2_SMALL if w.model == "gpt2-small" else PRESETS[w.model]

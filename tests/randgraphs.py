@@ -20,9 +20,9 @@ KINDS = [CollectiveKind.ALL_REDUCE, CollectiveKind.ALL_GATHER, CollectiveKind.RE
 
 
 def random_graphs(seed: int, max_world: int = 6, max_nodes: int = 24, p_zero: float = 0.25,
-                  subgroups: bool = True, shuffle: bool = True, sparse_ids: bool = True):
+                  subgroups: bool = True, shuffle: bool = True, sparse_ids: bool = True, min_world: int = 1):
     rng = random.Random(seed)
-    world = rng.randint(1, max_world)
+    world = rng.randint(min_world, max_world)
     n_inst = rng.randint(0, 4)
     insts = []
     for _ in range(n_inst):
@@ -92,7 +92,7 @@ def random_graphs(seed: int, max_world: int = 6, max_nodes: int = 24, p_zero: fl
     return graphs, Topology.switch(world, bw, lat)
 
 
-def random_p2p_graphs(seed: int, mesh: bool = False):
+def random_p2p_graphs(seed: int, mesh: bool = False, world: int = 0, n_msgs: int = 10):
     """Ranks exchanging point-to-point messages (expanded comm mode): random
     SEND/RECV pairs on shared channels, interleaved with compute and an
     optional collective; links are contended and some graphs deadlock."""
@@ -101,10 +101,10 @@ def random_p2p_graphs(seed: int, mesh: bool = False):
     if mesh:
         rows, cols = rng.choice([(1, 2), (2, 2), (2, 3)])
         world = rows * cols
-    else:
+    elif not world:
         world = rng.randint(2, 5)
     msgs = []
-    for _ in range(rng.randint(1, 10)):
+    for _ in range(rng.randint(1, n_msgs)):
         a, b = rng.sample(range(world), 2)
         msgs.append((a, b, rng.randint(0, 2), rng.choice([0, 8, 100, 1000, 4096])))
     per_rank = [[] for _ in range(world)]

@@ -105,7 +105,11 @@ def test_engine_c3_north_star_points():
 @pytest.mark.parametrize("seed", range(400))
 def test_engine_random_race_graphs_vs_oracle(seed):
     gs, topo = random_graphs(seed)
-    for algo, cs in (("ring", 1), ("ring", 2), ("tree", 1), ("ring", 3)):
+    _check_race(gs, topo, seed, (("ring", 1), ("ring", 2), ("tree", 1), ("ring", 3)))
+
+
+def _check_race(gs, topo, seed, configs):
+    for algo, cs in configs:
         try:
             ref = O.simulate(gs, topo, algo, cs, 1, record_events=True)
             st, en = ref.pop("events")
@@ -216,6 +220,10 @@ def test_engine_random_p2p_vs_oracle(seed):
     """Expanded comm mode: per-link FIFO, message ordering, busy/exposed stats."""
     from randgraphs import random_p2p_graphs
     gs, topo = random_p2p_graphs(seed, mesh=seed % 2 == 1)
+    _check_p2p(gs, topo, seed)
+
+
+def _check_p2p(gs, topo, seed):
     try:
         ref = O.simulate(gs, topo, "ring", record_events=True)
         st, en = ref.pop("events")
@@ -247,3 +255,42 @@ def test_engine_random_p2p_vs_oracle(seed):
     except Exception as e:
         got_cp = type(e).__name__
     assert got_cp == want_cp, seed
+
+
+# ---- more ranks than one CTA has threads: a design point spans a thread-block cluster ----
+
+@pytest.mark.parametrize("seed", range(12))
+def test_engine_cluster_race_graphs_vs_oracle(seed):
+    """1025..3000 ranks (2-3 CTAs per point): cross-CTA ties, sub-group collectives, zero durations."""
+    gs, topo = random_graphs(10_000 + seed, min_world=1025, max_world=3000, max_nodes=10)
+    _check_race(gs, topo, seed, (("ring", 1), ("ring", 2), ("tree", 1)))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_engine_cluster_p2p_vs_oracle(seed):
+    from randgraphs import random_p2p_graphs
+    gs, topo = random_p2p_graphs(20_000 + seed, world=1024 + 512 * (seed % 3) + seed, n_msgs=3000)
+    _check_p2p(gs, topo, seed)
+
+
+@pytest.mark.parametrize("spec,algo", [("switch:2048:50GB:1us", "ring"), ("switch:2048:900GB:200ns", "tree"),
+                                       ("mesh:32x64:200GB:500ns", "mesh-hier")])
+def test_engine_cluster_fsdp2048_vs_oracle(spec, algo):
+    gs = synth.synth_transformer(synth.PRESETS["llama-8b-like"], synth.ParallelConfig(synth.Strategy.FSDP, 2048), 2048)
+    out = _batch(gs, [(spec, algo)])
+    try:
+        want = O.sweep_row(gs, parse_topology(spec), algo)
+    except O.OracleError as e:       # TREE is ALL_REDUCE-only (collectives.py:273-275)
+        assert e.kind == "UnsupportedAlgoTopologyError" and out["status"][0] == 4
+        return
+    assert {k: int(out[k][0]) for k in ROW_KEYS} == want
+
+
+def test_engine_cluster_8192_ranks_vs_oracle():
+    """BASELINE config-4 scale: 8192 ranks = a cluster of 8 CTAs per design point."""
+    gs = synth.synth_transformer(synth.PRESETS["tiny"], synth.ParallelConfig(synth.Strategy.DP, 8192), 8192)
+    specs = [("switch:8192:100GB:1us", "ring"), ("switch:8192:25GB:5us", "tree"), ("mesh:64x128:400GB:100ns", "mesh-hier")]
+    out = _batch(gs, specs)
+    flat = O.flatten(gs)
+    for i, (spec, algo) in enumerate(specs):
+        assert {k: int(out[k][i]) for k in ROW_KEYS} == O.sweep_row(gs, parse_topology(spec), algo, flat=flat), spec

@@ -14,6 +14,8 @@ from .engine import (ROW_FIELDS, DesignPoints, Engine, RankStats, SimOptions, Si
                      cost_only, critical_path, simulate, simulate_batch)
 from .errors import (DeadlockError, EngineError, FormatError, InconsistentGroupsError, TrainsimError,
                      UnsupportedAlgoTopologyError, UnsupportedComboError)
+from .expansion import (P2pPlan, PlanOp, check_plan, collective_instances, dataflow_check, expand,
+                     expand_collectives, wire_bytes)
 from .graph import (CollectiveKind, CollSpec, Dtype, Node, NodeKind, P2pSpec, TensorMeta, WorkloadGraph,
                     tensor_bytes, topo_order)
 from .synth import (PRESETS, FsdpMode, ModelConfig, ParallelConfig, Strategy, parse_parallel,

@@ -28,6 +28,7 @@ import numpy as np
 
 from .costs import CollectiveAlgo, load_profile
 from .engine import ROW_FIELDS, DesignPoints, Engine
+from .expansion import expand_collectives
 from .errors import (EngineError, FL_OK, TrainsimError, UnsupportedAlgoTopologyError,
                      UnsupportedComboError, raise_for_status)
 from .synth import PRESETS, FsdpMode, parse_parallel, synth_transformer
@@ -152,46 +153,66 @@ def gather_rows(local_status, local_rows, n_total: int, world: int, rank: int, d
 
 def sweep_rows(preset: str, parallels, topos, algos, comm_mode: str = "analytical",
                fsdp_mode: str = "delayed", profile_path: Optional[str] = None, device: int = 0) -> list:
-    """Rows of ``trainsim sweep`` (cli.py:345-358) computed on the GPU."""
-    if comm_mode != "analytical":
-        raise EngineError("expanded comm mode is not supported by this engine build")
+    """Rows of ``trainsim sweep`` (cli.py:319-358) computed on the GPU.
+
+    Design points that share a graph are evaluated in one engine launch: all
+    points of a parallel token in ANALYTICAL mode; in EXPANDED mode the graph
+    also depends on the algorithm and, for MESH_HIER, on the mesh shape
+    (collectives.py:456-537), so those join the grouping key."""
+    if comm_mode not in ("analytical", "expanded"):
+        raise UnsupportedComboError(f"unknown comm mode {comm_mode!r}")
     if not parallels or not topos or not algos:
         raise UnsupportedComboError("sweep lists must be non-empty")
+    expanded = comm_mode == "expanded"
     profile = load_profile(profile_path) if profile_path else None
     tasks = list(itertools.product(parallels, topos, algos))
-    by_par: dict = {}
-    for i, (par, topo, algo) in enumerate(tasks):
-        by_par.setdefault(par, []).append(i)
-    results = [None] * len(tasks)
-    first_error = None
-    for par, idxs in by_par.items():
-        m = PRESETS[preset]
-        p = dataclasses.replace(parse_parallel(par), fsdp_mode=FsdpMode(fsdp_mode))
+    groups: dict = {}
+    errors: dict = {}
+    parsed = {}
+    for i, (par, spec, algo) in enumerate(tasks):
         try:
-            graphs = synth_transformer(m, p, p.degree, profile=profile)
-            topo_objs = [parse_topology(tasks[i][1]) for i in idxs]
-            algo_objs = [CollectiveAlgo(tasks[i][2]) for i in idxs]
+            topo = parse_topology(spec)
+            a = CollectiveAlgo(algo)
+        except (TrainsimError, ValueError) as e:
+            errors[i] = e
+            continue
+        parsed[i] = (topo, a)
+        key = (par,)
+        if expanded:
+            key += (a.value, topo.kind.value, topo.rows, topo.cols) if a == CollectiveAlgo.MESH_HIER else (a.value,)
+        groups.setdefault(key, []).append(i)
+    results = {}
+    synth_cache: dict = {}
+    for key, idxs in groups.items():
+        par = key[0]
+        try:
+            if par not in synth_cache:
+                p = dataclasses.replace(parse_parallel(par), fsdp_mode=FsdpMode(fsdp_mode))
+                synth_cache[par] = (p, synth_transformer(PRESETS[preset], p, p.degree, profile=profile))
+            p, graphs = synth_cache[par]
+            if expanded:
+                topo0, a0 = parsed[idxs[0]]
+                graphs = expand_collectives(graphs, a0, topo0)
         except TrainsimError as e:
-            first_error = first_error or (idxs[0], e)
+            for i in idxs:
+                errors[i] = e
             continue
         eng = Engine(graphs, device)
         try:
-            out = eng.run(DesignPoints.from_topologies(topo_objs, algo_objs))
+            out = eng.run(DesignPoints.from_topologies([parsed[i][0] for i in idxs], [parsed[i][1] for i in idxs]))
         finally:
             eng.close()
         for j, i in enumerate(idxs):
             results[i] = (int(out["status"][j]), out["rows"][j], p.degree)
     rows = []
-    for i, (par, topo, algo) in enumerate(tasks):
-        if first_error and first_error[0] == i:
-            raise first_error[1]
-        st, vals, deg = results[i] if results[i] is not None else (None, None, None)
-        if results[i] is None:
-            continue
+    for i, (par, spec, algo) in enumerate(tasks):      # first failure in task order, like the pool map
+        if i in errors:
+            raise errors[i]
+        st, vals, deg = results[i]
         if st != FL_OK:
-            raise_for_status(st, f"design point {par} {topo} {algo}")
+            raise_for_status(st, f"design point {par} {spec} {algo}")
         row = {"model": preset, "parallel": par, "fsdp_mode": fsdp_mode, "algo": algo,
-               "comm_mode": comm_mode, "topology": topo, "world_size": deg}
+               "comm_mode": comm_mode, "topology": spec, "world_size": deg}
         row.update({k: int(v) for k, v in zip(ROW_FIELDS, vals)})
         rows.append(row)
     return rows

@@ -3,6 +3,7 @@
 from __future__ import annotations
 
 import gzip
+import hashlib
 import json
 from functools import lru_cache
 from pathlib import Path
@@ -51,3 +52,25 @@ def decode_topo(t) -> Topology:
 
 def has_p2p(case) -> bool:
     return any(n[1] in ("SEND", "RECV") for nl in case["node_lists"] for n in nl)
+
+
+def _v(x):
+    return getattr(x, "value", x)
+
+
+def canon(graphs) -> str:
+    """sha256 of a graph set's canonical encoding (either package's classes)."""
+    enc = []
+    for g in graphs:
+        nodes = [[n.node_id, _v(n.kind), n.op_name, list(n.inputs), list(n.outputs), list(n.data_deps),
+                  [list(c) for c in n.ctrl_deps], n.duration_ns,
+                  [_v(n.coll.kind), list(n.coll.group), n.coll.comm_bytes] if n.coll else None,
+                  [n.p2p.peer_rank, n.p2p.comm_bytes, n.p2p.channel_tag] if n.p2p else None] for n in g.nodes]
+        enc.append([g.rank, g.world_size, nodes, sorted(g.tensors), g.meta.get("passes")])
+    return hashlib.sha256(json.dumps(enc, separators=(",", ":")).encode()).hexdigest()
+
+
+@lru_cache(maxsize=None)
+def expand_fixtures() -> dict:
+    with gzip.open(GOLDEN / "expand.json.gz", "rt") as f:
+        return json.load(f)

@@ -134,3 +134,133 @@ def topo_order(g) -> list:
     if len(out) != len(ids):
         raise CyclicGraphError("graph has a dependency cycle; no topological order")
     return out
+
+
+# ------------------------------------------------------------ validation
+
+
+@dataclass
+class Violation:
+    """One broken structural rule (reference graph.py:137-150)."""
+    rule: str
+    detail: str
+    node_id: Optional[int] = None
+    tensor_id: Optional[int] = None
+
+    def __str__(self) -> str:
+        where = [f"node {self.node_id}"] * (self.node_id is not None) + \
+                [f"tensor {self.tensor_id}"] * (self.tensor_id is not None)
+        return f"[{self.rule}] {' @ '.join(where) or 'graph'}: {self.detail}"
+
+
+def _kv(x):
+    return getattr(x, "value", x)
+
+
+def _cycle(g, nmap) -> Optional[list]:
+    """One dependency cycle, found by an iterative depth-first walk over data and
+    control edges in node-list order (reference graph.py:246-279)."""
+    state = dict.fromkeys(nmap, 0)          # 0 unvisited, 1 on the path, 2 finished
+    parent: dict = {}
+    for root in nmap:
+        if state[root]:
+            continue
+        state[root] = 1
+        path = [(root, iter(nmap[root].dep_ids()))]
+        while path:
+            nid, deps = path[-1]
+            for d in deps:
+                if d not in state or d == nid:
+                    continue
+                if state[d] == 1:
+                    cyc, cur = [d, nid], nid
+                    while cur in parent and parent[cur] != d:
+                        cur = parent[cur]
+                        cyc.append(cur)
+                    return cyc[::-1]
+                if state[d] == 0:
+                    state[d], parent[d] = 1, nid
+                    path.append((d, iter(nmap[d].dep_ids())))
+                    break
+            else:
+                state[nid] = 2
+                path.pop()
+    return None
+
+
+def validate_graph(g) -> list:
+    """Every structural invariant of a rank graph (reference graph.py:153-243)."""
+    out = []
+    seen = set()
+    for n in g.nodes:
+        if n.node_id in seen:
+            out.append(Violation("duplicate-node-id", "node_id appears twice", node_id=n.node_id))
+        seen.add(n.node_id)
+    nmap = {n.node_id: n for n in g.nodes}
+    ginputs = set(g.meta.get("graph_inputs", []))
+    for tid, tm in g.tensors.items():
+        if tid != tm.tensor_id:
+            out.append(Violation("tensor-id-mismatch", f"table key {tid} != tensor_id {tm.tensor_id}", tensor_id=tid))
+        if not tm.shape or min(tm.shape) <= 0:
+            out.append(Violation("tensor-shape", f"shape must be non-empty positive ints, got {tm.shape}",
+                                 tensor_id=tid))
+        elif tm.bytes != math.prod(tm.shape) * Dtype(_kv(tm.dtype)).byte_width:
+            want = math.prod(tm.shape) * Dtype(_kv(tm.dtype)).byte_width
+            out.append(Violation("tensor-bytes", f"bytes {tm.bytes} != prod(shape)*width {want}", tensor_id=tid))
+    prod: dict = {}
+    for n in g.nodes:
+        for t in n.outputs:
+            prod.setdefault(t, []).append(n.node_id)
+    out += [Violation("multi-producer", f"produced by nodes {ps}", tensor_id=t) for t, ps in prod.items() if len(ps) > 1]
+    for n in g.nodes:
+        kind = _kv(n.kind)
+        if (n.coll is not None) != (kind == "COLL"):
+            out.append(Violation("coll-presence", f"coll attrs on {kind} node", node_id=n.node_id))
+        if (n.p2p is not None) != (kind in ("SEND", "RECV")):
+            out.append(Violation("p2p-presence", f"p2p attrs on {kind} node", node_id=n.node_id))
+        if n.duration_ns is not None:
+            if kind != "COMP":
+                out.append(Violation("duration-on-non-comp", f"duration on {kind} node", node_id=n.node_id))
+            elif n.duration_ns < 0:
+                out.append(Violation("negative-duration", f"duration {n.duration_ns}", node_id=n.node_id))
+        for d in n.dep_ids():
+            if d not in nmap:
+                out.append(Violation("dangling-dep", f"dep on missing node {d}", node_id=n.node_id))
+            elif d == n.node_id:
+                out.append(Violation("self-dep", "node depends on itself", node_id=n.node_id))
+        for t in list(n.inputs) + list(n.outputs):
+            if t not in g.tensors:
+                out.append(Violation("unknown-tensor", f"references tensor {t} not in table", node_id=n.node_id,
+                                     tensor_id=t))
+        # data deps = producers of the inputs, plus deps on HOST launch twins and
+        # on SEND/RECV plan operations
+        need = set()
+        for t in n.inputs:
+            if prod.get(t):
+                need.add(prod[t][0])
+            elif t not in ginputs and t in g.tensors:
+                out.append(Violation("missing-producer", "consumed tensor has no producer and is not a graph input",
+                                     node_id=n.node_id, tensor_id=t))
+        have = set(n.data_deps)
+        out += [Violation("missing-data-dep", f"input producer {m} not in data_deps", node_id=n.node_id)
+                for m in sorted(need - have)]
+        out += [Violation("spurious-data-dep", f"data_dep {x} is not an input producer", node_id=n.node_id)
+                for x in sorted(have - need) if x in nmap and _kv(nmap[x].kind) not in ("HOST", "SEND", "RECV")]
+        if n.coll is not None:
+            grp = n.coll.group
+            if not grp:
+                out.append(Violation("empty-group", "collective group is empty", node_id=n.node_id))
+            else:
+                if g.rank not in grp:
+                    out.append(Violation("rank-not-in-group", f"rank {g.rank} not in group {grp}", node_id=n.node_id))
+                if any(r < 0 or r >= g.world_size for r in grp):
+                    out.append(Violation("group-out-of-range", f"group {grp} outside world {g.world_size}",
+                                         node_id=n.node_id))
+            if n.coll.comm_bytes < 0:
+                out.append(Violation("negative-comm-bytes", str(n.coll.comm_bytes), node_id=n.node_id))
+        if n.p2p is not None and (n.p2p.peer_rank == g.rank or not 0 <= n.p2p.peer_rank < g.world_size):
+            out.append(Violation("bad-peer", f"peer {n.p2p.peer_rank}", node_id=n.node_id))
+    cyc = _cycle(g, nmap)
+    if cyc:
+        out.append(Violation("cycle", "dependency cycle through nodes " + "->".join(map(str, cyc))))
+    return out

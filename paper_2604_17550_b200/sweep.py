@@ -29,6 +29,7 @@ import numpy as np
 from .costs import CollectiveAlgo, load_profile
 from .engine import ROW_FIELDS, DesignPoints, Engine
 from .expansion import expand_collectives
+from .passes import apply_pass
 from .errors import (EngineError, FL_OK, TrainsimError, UnsupportedAlgoTopologyError,
                      UnsupportedComboError, raise_for_status)
 from .synth import PRESETS, FsdpMode, parse_parallel, synth_transformer
@@ -152,24 +153,31 @@ def gather_rows(local_status, local_rows, n_total: int, world: int, rank: int, d
 
 
 def sweep_rows(preset: str, parallels, topos, algos, comm_mode: str = "analytical",
-               fsdp_mode: str = "delayed", profile_path: Optional[str] = None, device: int = 0) -> list:
+               fsdp_mode: str = "delayed", profile_path: Optional[str] = None, device: int = 0,
+               passes: Optional[list] = None) -> list:
     """Rows of ``trainsim sweep`` (cli.py:319-358) computed on the GPU.
 
     Design points that share a graph are evaluated in one engine launch: all
     points of a parallel token in ANALYTICAL mode; in EXPANDED mode the graph
     also depends on the algorithm and, for MESH_HIER, on the mesh shape
-    (collectives.py:456-537), so those join the grouping key."""
+    (collectives.py:456-537), so those join the grouping key.
+
+    ``passes`` (an extension; the reference sweeps one graph per parallel
+    token) adds a graph-rewrite axis, e.g. ``["none", "reorder-allgather:1",
+    "bucket-allreduce:2097152"]`` (passes.apply_pass); rows then carry a
+    ``pass`` column and each value is another graph structure."""
     if comm_mode not in ("analytical", "expanded"):
         raise UnsupportedComboError(f"unknown comm mode {comm_mode!r}")
     if not parallels or not topos or not algos:
         raise UnsupportedComboError("sweep lists must be non-empty")
     expanded = comm_mode == "expanded"
     profile = load_profile(profile_path) if profile_path else None
-    tasks = list(itertools.product(parallels, topos, algos))
+    pass_axis = list(passes) if passes else ["none"]
+    tasks = [(par, ps, spec, algo) for par in parallels for ps in pass_axis for spec in topos for algo in algos]
     groups: dict = {}
     errors: dict = {}
     parsed = {}
-    for i, (par, spec, algo) in enumerate(tasks):
+    for i, (par, ps, spec, algo) in enumerate(tasks):
         try:
             topo = parse_topology(spec)
             a = CollectiveAlgo(algo)
@@ -177,23 +185,24 @@ def sweep_rows(preset: str, parallels, topos, algos, comm_mode: str = "analytica
             errors[i] = e
             continue
         parsed[i] = (topo, a)
-        key = (par,)
+        key = (par, ps)
         if expanded:
             key += (a.value, topo.kind.value, topo.rows, topo.cols) if a == CollectiveAlgo.MESH_HIER else (a.value,)
         groups.setdefault(key, []).append(i)
     results = {}
     synth_cache: dict = {}
     for key, idxs in groups.items():
-        par = key[0]
+        par, ps = key[0], key[1]
         try:
             if par not in synth_cache:
                 p = dataclasses.replace(parse_parallel(par), fsdp_mode=FsdpMode(fsdp_mode))
                 synth_cache[par] = (p, synth_transformer(PRESETS[preset], p, p.degree, profile=profile))
             p, graphs = synth_cache[par]
+            graphs = apply_pass(graphs, ps)
             if expanded:
                 topo0, a0 = parsed[idxs[0]]
                 graphs = expand_collectives(graphs, a0, topo0)
-        except TrainsimError as e:
+        except (TrainsimError, ValueError) as e:
             for i in idxs:
                 errors[i] = e
             continue
@@ -205,7 +214,7 @@ def sweep_rows(preset: str, parallels, topos, algos, comm_mode: str = "analytica
         for j, i in enumerate(idxs):
             results[i] = (int(out["status"][j]), out["rows"][j], p.degree)
     rows = []
-    for i, (par, spec, algo) in enumerate(tasks):      # first failure in task order, like the pool map
+    for i, (par, ps, spec, algo) in enumerate(tasks):  # first failure in task order, like the pool map
         if i in errors:
             raise errors[i]
         st, vals, deg = results[i]
@@ -213,6 +222,8 @@ def sweep_rows(preset: str, parallels, topos, algos, comm_mode: str = "analytica
             raise_for_status(st, f"design point {par} {spec} {algo}")
         row = {"model": preset, "parallel": par, "fsdp_mode": fsdp_mode, "algo": algo,
                "comm_mode": comm_mode, "topology": spec, "world_size": deg}
+        if passes:
+            row["pass"] = ps
         row.update({k: int(v) for k, v in zip(ROW_FIELDS, vals)})
         rows.append(row)
     return rows
@@ -224,14 +235,18 @@ def normalize(rows: list, normalize_to: Optional[str]) -> None:
     if normalize_to:
         for row in rows:
             if row["parallel"] == normalize_to:
-                base[(row["model"], row["topology"], row["algo"], row["comm_mode"])] = row["makespan_ns"]
+                base[(row["model"], row["topology"], row["algo"], row["comm_mode"], row.get("pass"))] = \
+                    row["makespan_ns"]
     for row in rows:
-        b = base.get((row["model"], row["topology"], row["algo"], row["comm_mode"]))
+        b = base.get((row["model"], row["topology"], row["algo"], row["comm_mode"], row.get("pass")))
         row["speedup_vs_base"] = f"{b / row['makespan_ns']:.6f}" if b and row["makespan_ns"] else "1.000000"
 
 
 def write_csv(rows: list, path: str) -> None:
     with open(path, "w", newline="") as f:
-        w = csv.DictWriter(f, fieldnames=SWEEP_FIELDS, lineterminator="\n")
+        fields = SWEEP_FIELDS
+        if rows and "pass" in rows[0]:
+            fields = SWEEP_FIELDS[:3] + ["pass"] + SWEEP_FIELDS[3:]
+        w = csv.DictWriter(f, fieldnames=fields, lineterminator="\n")
         w.writeheader()
         w.writerows(rows)

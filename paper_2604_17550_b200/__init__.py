@@ -16,8 +16,10 @@ from .errors import (DeadlockError, EngineError, FormatError, InconsistentGroups
                      UnsupportedAlgoTopologyError, UnsupportedComboError)
 from .expansion import (P2pPlan, PlanOp, check_plan, collective_instances, dataflow_check, expand,
                      expand_collectives, wire_bytes)
-from .graph import (CollectiveKind, CollSpec, Dtype, Node, NodeKind, P2pSpec, TensorMeta, WorkloadGraph,
-                    tensor_bytes, topo_order)
+from .graph import (CollectiveKind, CollSpec, Dtype, Node, NodeKind, P2pSpec, TensorMeta, Violation, WorkloadGraph,
+                    tensor_bytes, topo_order, validate_graph)
+from .ingest import RawExport, RawIrNode, convert, parse_raw_export, read_raw_export
+from .passes import apply_pass, bucket_allreduce, reorder_allgather, verify_pass_safety
 from .synth import (PRESETS, FsdpMode, ModelConfig, ParallelConfig, Strategy, parse_parallel,
                     synth_transformer)
 from .topology import Topology, TopologyKind, parse_bandwidth, parse_latency, parse_topology

@@ -37,6 +37,18 @@ def nvcc() -> str:
     return "nvcc"
 
 
+def build_variant(out: Path, defines=(), verbose: bool = False) -> str:
+    """Compile the engine with extra -D flags into `out` (A/B experiments)."""
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(ROOT / "include"), "-I", str(PKG / "csrc"),
+           *map(str, SOURCES), "-o", str(out)]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise EngineError("nvcc failed:\n" + res.stderr[-4000:])
+    return res.stderr
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
     newest = max(p.stat().st_mtime for p in SOURCES + HEADERS)
@@ -100,12 +112,20 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
+    override = os.environ.get("FLINT_B200_LIB")     # A/B builds of the same engine (scripts/ab.py)
+    if override:
+        _lib = _bind(C.CDLL(override))
+        return _lib
     if not LIB.exists():
         try:
             build()
         except (OSError, EngineError) as e:
             raise EngineError(f"CUDA engine library {LIB} is missing and could not be built: {e}") from e
-    L = C.CDLL(str(LIB))
+    _lib = _bind(C.CDLL(str(LIB)))
+    return _lib
+
+
+def _bind(L):
     L.fl_version.restype = C.c_int
     L.fl_last_error.restype = C.c_char_p
     L.fl_device_count.argtypes = [P32]
@@ -119,7 +139,6 @@ def lib():
                                    P32, P64, P32]
     L.fl_cost_only.argtypes = [C.c_int32, PU8, P64, P64, PU8, PF64, PF64, P32, P32, P64, P32,
                                C.c_int32, P64, PF64, PF64, P64]
-    _lib = L
     return L
 
 

@@ -141,6 +141,7 @@ struct Shared {
     uint64_t xkmin[2][16];
     int64_t xvmax[2][16];
     int xvor[2][16];
+    int64_t *prg;                   // per-rank fields F_NSM.. in this CTA's HBM scratch
 };
 
 // Warp min of keys (time << 14 | rank).  Ranks step in lockstep most of the
@@ -258,7 +259,46 @@ __device__ __forceinline__ uint4 rec_c(const DevGraph &g, int gn) { return g.nod
 // (simulator.py:449-453) -- no per-rank in-degree table to initialize.
 constexpr uint64_t VAL48 = (1ull << 48) - 1;
 
-enum { ST_COMP = 0, ST_OVL, ST_CUR, ST_PEAK, ST_FIN, ST_N };
+// Per-rank state that is not needed on every step lives in shared memory, one
+// [field][blockDim] plane per field (a warp touches 256 contiguous bytes), addressed
+// from the kernel's own shared symbol so every access is an LDS/STS.  Registers
+// hold only what each step reads (the set heads, stream occupancy, the comm-FIFO
+// head): a CTA of 1024 ranks has 64 registers per rank, and what does not fit would
+// spill to local memory, i.e. to L2.
+//   *_CP: contention-free critical-path finish of the node at the head of a set /
+//   on a stream, carried along with it so that popping a node needs no HBM read;
+//   a node that overflows a set's head into its bitmap parks the value in the
+//   node's accumulator word instead (simulator.py:449-453 values, see below).
+// Hottest first: the first F_NSM fields are in shared memory, the rest in this CTA's
+// HBM scratch (same layout, L1-cached).  The plane stride is the compile-time
+// maximum block size, so a field access is one LDS/LD at an immediate offset from
+// the lane's own address.
+enum {
+    F_DUE_CP = 0, F_RC_CP, F_OCC_CP,                // heads of the due / ready-compute sets, running compute node
+    F_COMM_END,                                     // end of this rank's comm stream (FIFO tail)
+    F_FIN, F_CPMAX,                                 // last pop time; max critical-path finish popped
+    F_COMP, F_OVL, F_COMP_A,                        // compute busy, compute-under-comm, commcum at compute start
+    F_ALLOC, F_FREE, F_CUR, F_PEAK,                 // bytes allocated / freed at this step; memory in use, peak
+    F_RH_CP, F_HOST_E, F_HOST_CP,                   // host stream (its slot is free at t iff host_n < 0)
+    F_DUE_SUM, F_RC_SUM, F_RH_SUM,                  // non-empty-word summaries of the sets' bitmaps
+    F_N64
+};
+#ifndef FL_NSM
+#define FL_NSM F_N64
+#endif
+constexpr int F_NSM = FL_NSM;
+constexpr int FL_SR = 1024;                         // plane stride (lanes)
+enum { Q_RING_TAIL = 0, Q_HEAD_NODE, Q_HEAD_INST, Q_DONE, Q_N32 };
+
+extern __shared__ __align__(16) unsigned char fl_smem[];
+constexpr unsigned SM_HDR = (sizeof(Shared) + 15) / 16 * 16;
+__device__ __forceinline__ int64_t &F64(int k, int lr) {
+    if (k < F_NSM) return reinterpret_cast<int64_t *>(fl_smem + SM_HDR)[k * FL_SR + lr];
+    return reinterpret_cast<Shared *>(fl_smem)->prg[(k - F_NSM) * FL_SR + lr];
+}
+__device__ __forceinline__ int32_t &F32(int k, int lr) {
+    return reinterpret_cast<int32_t *>(fl_smem + SM_HDR + (size_t)F_NSM * 8 * FL_SR)[k * FL_SR + lr];
+}
 
 // Per-CTA (block-uniform) state pointers.  Bitmaps are word-major,
 // rank-minor ([word][rank]) so a warp's 32 ranks touch one 256-byte segment;
@@ -266,11 +306,11 @@ enum { ST_COMP = 0, ST_OVL, ST_CUR, ST_PEAK, ST_FIN, ST_N };
 struct Ctx {
     int R;
     int RL;                         // ranks owned by this CTA
-    int SR;                         // stride of the shared per-rank arrays (blockDim)
     int base;                       // first rank owned by this CTA (clusters of CTAs share a design point)
     int BR, DR;                     // strides of the touched / done bitmaps (RL in shared memory, else R)
     int crank, CS;                  // this CTA's rank in its cluster, cluster size (1 without clusters)
     bool lead_cta;                  // the cluster's first CTA (its thread 0 does the serial work)
+    int touch;                      // first-dependency bitmap in shared memory (else epoch tags)
     uint64_t *done, *rdyc, *rdyh, *due;
     uint64_t *touched;              // [word][rank]: accumulator written in this design point
     int64_t *cp;                    // [max_nodes][R]
@@ -279,10 +319,7 @@ struct Ctx {
     int64_t *inst_dur, *inst_s, *inst_e, *inst_cpmax;
     unsigned long long *inst_ckey;
     int32_t *inst_wait, *complist;
-    int64_t *comm_end;              // shared [R]
-    int32_t *ring_tail;             // shared [R]
     int *ncomp;                     // shared
-    int64_t *stat;                  // shared [ST_N][R]
     // point-to-point messages (expanded comm mode), simulator.py:177-200, :310-327
     int64_t *msg_sendt, *msg_recvt, *msg_cps_s, *msg_cps_r, *msg_s, *msg_e, *msg_xfer;
     unsigned long long *msg_ckey;
@@ -300,20 +337,15 @@ constexpr int32_t MSG_ALLOC = 1 << 30;   // mlist entry flag: the endpoint's out
 // Per-thread rank identity: element w of rank r in a [w][R] array is at w * R + r.
 struct Lane {
     int r, nb, tb;
-    int lr;                         // rank index within this CTA (shared-memory arrays)
+    int lr;                         // this thread's lane of the shared per-rank fields (threadIdx.x)
     int br, dr;                     // rank index for the touched / done bitmaps (lr in shared memory, else r)
 };
 
 // Per-rank indices and strides.  Bit 16 of K marks the cluster variant, whose
 // shared-memory arrays and bitmaps cover only this CTA's ranks (index lr,
 // stride blockDim); a single CTA indexes everything by rank (index r, stride R).
-template <int K> __device__ __forceinline__ int lidx(const Lane &L) { return (K & 16) ? L.lr : L.r; }
 // R is the caller's register copy of c.R (Ctx lives in shared memory, and a
 // re-read after every shared store would cost an LDS per access).
-template <int K> __device__ __forceinline__ int64_t &stat_ref(const Ctx &c, const Lane &L, int R, int k) {
-    if constexpr ((K & 16) != 0) return c.stat[k * c.SR + L.lr];
-    else return c.stat[k * R + L.r];
-}
 template <int K> __device__ __forceinline__ uint64_t &done_ref(const Ctx &c, const Lane &L, int R, int w) {
     if constexpr ((K & 16) != 0) return c.done[w * c.DR + L.dr];
     else return c.done[w * R + L.r];
@@ -324,28 +356,29 @@ template <int K> __device__ __forceinline__ uint64_t &touch_ref(const Ctx &c, co
 }
 
 // A node set with its minimum cached in a register and the rest in a global
-// bitmap (+ register summary of non-empty words).  Invariant: head < every
-// bitmap member, head < 0 iff the set is empty.  The due / ready sets rarely
-// hold more than one node, so most inserts and pops never touch memory.
+// bitmap ([word][rank]) with a summary of its non-empty words in shared field FS.
+// head < 0: empty; else bits 0-15 = the minimum, bit 16 = the bitmap is non-empty
+// (invariant: the minimum < every bitmap member).  The due / ready sets rarely hold
+// more than one node, so most inserts and pops are register operations.
 struct MinSet {
     int head;
-    uint64_t sum;
 };
+constexpr int MS_MORE = 1 << 16;
+__device__ __forceinline__ int ms_min(const MinSet &m) { return m.head & 0xffff; }
 
 template <int K>
 struct Rank {
     MinSet due, rc, rh;             // due events at t / ready compute nodes / ready host nodes
-    int64_t host_slot, host_e;
-    int64_t slot[K & 7], occ_e[K & 7];
+    int64_t slot[K & 7];            // compute stream free-at times (K > 1 only: with one stream
+                                    // the stream is busy at t iff it has an occupant)
+    int64_t occ_e[K & 7];           // end of the node running on each compute stream
     int64_t head_s, head_e;         // comm-FIFO head (valid iff ring_head < ring_seen)
-    int64_t alloc_t, free_t, cpmax;
     int64_t commcum;                // integral of "comm stream busy" up to the current step (= comm busy)
-    int64_t comp_a;                 // commcum when the running compute node started (K == 1)
-    int host_n;
+    int host_n;                     // node running on the host stream (end in F_HOST_E), or -1
     int occ_n[K & 7];
-    int head_node, head_alloc;
+    int head_alloc;
     int ring_head, ring_seen;
-    int done_cnt, pop_seq;
+    int pop_seq;
 };
 
 struct Step {                       // block-uniform per-step context
@@ -353,44 +386,63 @@ struct Step {                       // block-uniform per-step context
     uint64_t epoch;                 // design-point epoch << 58 (accumulator tag)
     int init;
     int fold;                       // static hosts folded (see "t = 0 host pops")
+    int touch;                      // first-dependency bitmap in shared memory (else epoch tags)
 };
 
-__device__ __forceinline__ void bm_set(uint64_t *b, int R, int r, uint64_t &sum, int idx) {
+__device__ __forceinline__ void bm_set(uint64_t *b, int R, int r, int64_t &sum, int idx) {
     const int w = idx >> 6;
     b[w * R + r] |= 1ull << (idx & 63);
-    sum |= 1ull << w;
+    sum |= 1ll << w;
 }
 
-__device__ __forceinline__ int bm_pop(uint64_t *b, int R, int r, uint64_t &sum) {
-    const int w = __ffsll((long long)sum) - 1;
+// pops the smallest member; returns it, and whether the bitmap is still non-empty
+__device__ __forceinline__ int bm_pop(uint64_t *b, int R, int r, int64_t &sum, bool &more) {
+    int64_t sm = sum;
+    const int w = __ffsll((long long)sm) - 1;
     uint64_t *p = b + (w * R + r);
     uint64_t word = *p;
     const int bit = __ffsll((long long)word) - 1;
     word &= word - 1;
     *p = word;
-    if (!word) sum &= sum - 1;
+    if (!word) { sm &= sm - 1; sum = sm; }
+    more = sm != 0;
     return (w << 6) | bit;
 }
 
-__device__ __forceinline__ int bm_peek(const uint64_t *b, int R, int r, uint64_t sum) {
-    const int w = __ffsll((long long)sum) - 1;
-    return (w << 6) | (__ffsll((long long)b[w * R + r]) - 1);
-}
-
-__device__ __forceinline__ void ms_insert(MinSet &m, uint64_t *b, int R, int r, int idx) {
+// Sets carrying each member's critical-path finish: the minimum's in shared field F,
+// bitmap members' in their accumulator word cp[node][rank].
+template <int F, int FS>
+__device__ __forceinline__ void ms_insert_cp(MinSet &m, uint64_t *b, int64_t *cp, int R, const Lane &L, int idx,
+                                             int64_t v) {
     if (m.head < 0) {
         m.head = idx;
-    } else if (idx < m.head) {
-        bm_set(b, R, r, m.sum, m.head);
-        m.head = idx;
+        F64(F, L.lr) = v;
+    } else if (idx < ms_min(m)) {
+        const int h = ms_min(m);
+        cp[h * R + L.r] = F64(F, L.lr);
+        bm_set(b, R, L.r, F64(FS, L.lr), h);
+        m.head = idx | MS_MORE;
+        F64(F, L.lr) = v;
     } else {
-        bm_set(b, R, r, m.sum, idx);
+        cp[idx * R + L.r] = v;
+        bm_set(b, R, L.r, F64(FS, L.lr), idx);
+        m.head |= MS_MORE;
     }
 }
 
-__device__ __forceinline__ int ms_pop(MinSet &m, uint64_t *b, int R, int r) {
-    const int x = m.head;
-    m.head = m.sum ? bm_pop(b, R, r, m.sum) : -1;
+template <int F, int FS>
+__device__ __forceinline__ int ms_pop_cp(MinSet &m, uint64_t *b, const int64_t *cp, int R, const Lane &L,
+                                         int64_t &v) {
+    const int x = ms_min(m);
+    v = F64(F, L.lr);
+    if (m.head & MS_MORE) {
+        bool more;
+        const int h = bm_pop(b, R, L.r, F64(FS, L.lr), more);
+        m.head = h | (more ? MS_MORE : 0);
+        F64(F, L.lr) = cp[h * R + L.r] & (int64_t)VAL48;
+    } else {
+        m.head = -1;
+    }
     return x;
 }
 
@@ -408,37 +460,62 @@ template <int K>
 __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, const Ctx &c, const Lane &L,
                                             Rank<K> &s, int64_t t, int cfg) {
     const int R = c.R;
-    while (s.rh.head >= 0 && s.host_slot <= t) {
-        const int h = ms_pop(s.rh, c.rdyh, R, L.r);
+    while (s.rh.head >= 0 && s.host_n < 0) {      // the host stream is free at t (gather_due ran at t)
+        int64_t v;
+        const int h = ms_pop_cp<F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, v);
         const int64_t e = t + c.dur[L.nb + h];
-        s.host_slot = e;
-        { const uint4 hb = rec_b(g, L.nb + h); s.alloc_t += rec_u64(hb.z, hb.w); }
+        { const uint4 hb = rec_b(g, L.nb + h); F64(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
         record(g, o, cfg, L.r, h, t, e);
-        if (e == t) ms_insert(s.due, c.due, R, L.r, h);
-        else { s.host_e = e; s.host_n = h; }
+        if (e == t) {
+            ms_insert_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, h, v);
+        } else {
+            F64(F_HOST_E, L.lr) = e;
+            F64(F_HOST_CP, L.lr) = v;
+            s.host_n = h;
+        }
     }
     while (s.rc.head >= 0) {
         int k = 0;
+        if constexpr ((K & 7) == 1) {
+            if (s.occ_n[0] >= 0) break;   // the occupant ends after t (gather_due ran at t)
+        } else {
 #pragma unroll
-        for (int q = 1; q < (K & 7); q++) if (s.slot[q] < s.slot[k]) k = q;
-        int64_t sk = s.slot[0];
+            for (int q = 1; q < (K & 7); q++) if (s.slot[q] < s.slot[k]) k = q;
+            int64_t sk = s.slot[0];
 #pragma unroll
-        for (int q = 1; q < (K & 7); q++) if (q == k) sk = s.slot[q];
-        if (sk > t) break;
-        const int x = ms_pop(s.rc, c.rdyc, R, L.r);
+            for (int q = 1; q < (K & 7); q++) if (q == k) sk = s.slot[q];
+            if (sk > t) break;
+        }
+        int64_t v;
+        const int x = ms_pop_cp<F_RC_CP, F_RC_SUM>(s.rc, c.rdyc, c.cp, R, L, v);
         const int64_t e = t + c.dur[L.nb + x];
-        { const uint4 xb = rec_b(g, L.nb + x); s.alloc_t += rec_u64(xb.z, xb.w); }
+        { const uint4 xb = rec_b(g, L.nb + x); F64(F_ALLOC, L.lr) += rec_u64(xb.z, xb.w); }
         record(g, o, cfg, L.r, x, t, e);
         if ((K & 7) == 1 && e > t) {      // one compute stream: its busy intervals are disjoint
-            stat_ref<K>(c, L, R, ST_COMP) += e - t;
-            s.comp_a = s.commcum;
+            F64(F_COMP, L.lr) += e - t;
+            F64(F_COMP_A, L.lr) = s.commcum;
         }
+#ifdef FL_PREFETCH
+        if (e > t && !c.touch) {          // the successors' accumulator words are read when x completes
+            const uint4 xa = rec_a(g, L.nb + x);
+            for (uint32_t q = xa.x; q < xa.y; q++) {
+                const int64_t *w = c.cp + (g.succ_idx[q] * R + L.r);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(w));
+            }
+        }
+#endif
 #pragma unroll
         for (int q = 0; q < (K & 7); q++) {
             if (q == k) {
-                s.slot[q] = e;
-                if (e == t) ms_insert(s.due, c.due, R, L.r, x);
-                else { s.occ_e[q] = e; s.occ_n[q] = x; }
+                if constexpr ((K & 7) > 1) s.slot[q] = e;
+                if (e == t) {
+                    ms_insert_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, x, v);
+                } else {
+                    s.occ_e[q] = e;
+                    s.occ_n[q] = x;
+                    if (q == 0) F64(F_OCC_CP, L.lr) = v;
+                    else c.cp[x * R + L.r] = v;      // streams 1..3: the running node's own accumulator word
+                }
             }
         }
     }
@@ -475,24 +552,26 @@ __device__ __forceinline__ void dispatch(const DevGraph &g, const Ctx &c, const 
         return;
     }
     const int64_t fin = cps + c.dur[L.nb + d];
-    c.cp[d * R + L.r] = (int64_t)(f.epoch | (uint64_t)fin);
-    s.cpmax = fin > s.cpmax ? fin : s.cpmax;
-    if (kind == FL_COMP) ms_insert(s.rc, c.rdyc, R, L.r, d);
-    else ms_insert(s.rh, c.rdyh, R, L.r, d);
+    if (kind == FL_COMP) ms_insert_cp<F_RC_CP, F_RC_SUM>(s.rc, c.rdyc, c.cp, R, L, d, fin);
+    else ms_insert_cp<F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, d, fin);
 }
 
 // Pop one completion event (simulator.py:335-340) and free tensors whose last
 // consumer it was (simulator.py:384-388).
 template <int K>
 __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const Lane &L, Rank<K> &s,
-                                          const Step &f, int x, int64_t t) {
+                                          const Step &f, int x, int64_t fx64, int64_t t) {
     const int R = c.R;
     const uint4 xa = rec_a(g, L.nb + x), xc = rec_c(g, L.nb + x);
     if (g.needs_done) done_ref<K>(c, L, R, x >> 6) |= 1ull << (x & 63);
-    s.done_cnt++;
+    F32(Q_DONE, L.lr)++;
     s.pop_seq++;
-    stat_ref<K>(c, L, R, ST_FIN) = t;
-    s.free_t += rec_u64(xc.x, xc.y);
+    F64(F_FIN, L.lr) = t;
+    {
+        const int64_t cm = F64(F_CPMAX, L.lr);
+        if (fx64 > cm) F64(F_CPMAX, L.lr) = fx64;
+    }
+    int64_t freed = rec_u64(xc.x, xc.y);
     for (uint32_t q = xa.z; q < xa.w; q++) {
         const int tt = L.tb + g.free_tens[q];
         const int2 cr = g.tens_rng[tt];
@@ -501,9 +580,10 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
             const int q = g.tens_cons[u];
             all = (done_ref<K>(c, L, R, q >> 6) >> (q & 63)) & 1;
         }
-        if (all) s.free_t += g.tens_bytes[tt];
+        if (all) freed += g.tens_bytes[tt];
     }
-    const uint64_t fx = (uint64_t)c.cp[x * R + L.r] & VAL48;    // this node's critical-path finish
+    if (freed) F64(F_FREE, L.lr) += freed;
+    const uint64_t fx = (uint64_t)fx64;     // this node's critical-path finish
     int seq = 0;
     for (uint32_t q = xa.x; q < xa.y; q++, seq++) {
         const int d = g.succ_idx[q];
@@ -512,14 +592,19 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
         int64_t *slot = c.cp + (d * R + L.r);
         // first dependency to complete: the word holds nothing of this design point,
         // so skip reading it (a DRAM round trip on the critical chain)
-        uint64_t &tw = touch_ref<K>(c, L, R, d >> 6);
-        const uint64_t tb = 1ull << (d & 63);
         uint64_t a;
-        if (tw & tb) {
+        if (f.touch) {
+            uint64_t &tw = touch_ref<K>(c, L, R, d >> 6);
+            const uint64_t tb = 1ull << (d & 63);
+            if (tw & tb) {
+                a = (uint64_t)*slot;
+            } else {
+                tw |= tb;
+                a = f.epoch | (rec_indeg(db, f.fold) << 48);
+            }
+        } else {                // a word of an earlier design point reads as "no dependency completed"
             a = (uint64_t)*slot;
-        } else {
-            tw |= tb;
-            a = f.epoch | (rec_indeg(db, f.fold) << 48);
+            if ((a >> 58) != (f.epoch >> 58)) a = f.epoch | (rec_indeg(db, f.fold) << 48);
         }
         const uint64_t v = (a & VAL48) > fx ? (a & VAL48) : fx;
         const uint64_t left = ((a >> 48) & 0x3ff) - 1;
@@ -532,7 +617,8 @@ template <int K>
 __device__ __forceinline__ void load_head(const Ctx &c, const Lane &L, Rank<K> &s) {
     if (s.ring_head < s.ring_seen) {
         const int i = c.ring_inst[s.ring_head * c.R + L.r];
-        s.head_node = c.ring_node[s.ring_head * c.R + L.r];
+        F32(Q_HEAD_NODE, L.lr) = c.ring_node[s.ring_head * c.R + L.r];
+        F32(Q_HEAD_INST, L.lr) = i;
         s.head_s = c.inst_s[i];
         s.head_e = c.inst_e[i];
         s.head_alloc = 0;
@@ -542,7 +628,7 @@ __device__ __forceinline__ void load_head(const Ctx &c, const Lane &L, Rank<K> &
 // After reservations: pick up comm-FIFO entries appended for this rank.
 template <int K>
 __device__ __forceinline__ void refresh_ring(const Ctx &c, const Lane &L, Rank<K> &s) {
-    const int tail = c.ring_tail[lidx<K>(L)];
+    const int tail = F32(Q_RING_TAIL, L.lr);
     if (tail != s.ring_seen) {
         const bool was_empty = s.ring_head == s.ring_seen;
         s.ring_seen = tail;
@@ -554,7 +640,7 @@ template <int K>
 __device__ __forceinline__ int64_t next_time(const DevGraph &g, const Ctx &c, const Lane &L, const Rank<K> &s,
                                              int64_t tcur) {
     if (s.due.head >= 0) return tcur;
-    int64_t nt = s.host_n >= 0 ? s.host_e : TINF;
+    int64_t nt = s.host_n >= 0 ? F64(F_HOST_E, L.lr) : TINF;
 #pragma unroll
     for (int q = 0; q < (K & 7); q++) if (s.occ_n[q] >= 0 && s.occ_e[q] < nt) nt = s.occ_e[q];
     if (s.ring_head < s.ring_seen && s.head_e < nt) nt = s.head_e;
@@ -570,17 +656,24 @@ template <int K>
 __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, const Lane &L, Rank<K> &s,
                                            int64_t t) {
     const int R = c.R;
-    if (s.host_n >= 0 && s.host_e == t) { ms_insert(s.due, c.due, R, L.r, s.host_n); s.host_n = -1; }
+    if (s.host_n >= 0 && F64(F_HOST_E, L.lr) == t) {
+        ms_insert_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, s.host_n, F64(F_HOST_CP, L.lr));
+        s.host_n = -1;
+    }
 #pragma unroll
     for (int q = 0; q < (K & 7); q++)
         if (s.occ_n[q] >= 0 && s.occ_e[q] == t) {
-            ms_insert(s.due, c.due, R, L.r, s.occ_n[q]);
+            const int64_t v = q == 0 ? F64(F_OCC_CP, L.lr) : c.cp[s.occ_n[q] * R + L.r];
+            ms_insert_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, s.occ_n[q], v);
             s.occ_n[q] = -1;
-            if ((K & 7) == 1) stat_ref<K>(c, L, R, ST_OVL) += s.commcum - s.comp_a;   // comm time under [start, t)
+            if ((K & 7) == 1) F64(F_OVL, L.lr) += s.commcum - F64(F_COMP_A, L.lr);   // comm time under [start, t)
         }
     while (s.ring_head < s.ring_seen && s.head_e == t) {
-        if (!s.head_alloc) { const uint4 hb = rec_b(g, L.nb + s.head_node); s.alloc_t += rec_u64(hb.z, hb.w); }  // zero-length: starts now
-        ms_insert(s.due, c.due, R, L.r, s.head_node);
+        const int hn = F32(Q_HEAD_NODE, L.lr), hi = F32(Q_HEAD_INST, L.lr);
+        if (!s.head_alloc) { const uint4 hb = rec_b(g, L.nb + hn); F64(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }  // zero-length: starts now
+        // every member of an instance finishes at max over members' critical-path starts + duration
+        // (simulator.py:419-428)
+        ms_insert_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, hn, c.inst_cpmax[hi] + c.inst_dur[hi]);
         s.ring_head++;
         load_head(c, L, s);
     }
@@ -590,8 +683,8 @@ __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, cons
             const int ent = c.mlist[k * R + L.r];
             if (c.msg_e[ent & ~MSG_ALLOC] != t) break;
             const int node = c.mlist_node[k * R + L.r];
-            if (!(ent & MSG_ALLOC)) { const uint4 hb = rec_b(g, L.nb + node); s.alloc_t += rec_u64(hb.z, hb.w); }
-            ms_insert(s.due, c.due, R, L.r, node);
+            if (!(ent & MSG_ALLOC)) { const uint4 hb = rec_b(g, L.nb + node); F64(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
+            ms_insert_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, node, c.cp[node * R + L.r] & (int64_t)VAL48);
         }
         if (k) {
             for (int q = k; q < n; q++) {
@@ -611,8 +704,8 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
     const int R = c.R;
     const bool head = s.ring_head < s.ring_seen;
     if (head && !s.head_alloc && s.head_s <= tcur) {   // a collective that started by tcur
-        const uint4 hb = rec_b(g, L.nb + s.head_node);
-        s.alloc_t += rec_u64(hb.z, hb.w);
+        const uint4 hb = rec_b(g, L.nb + F32(Q_HEAD_NODE, L.lr));
+        F64(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w);
         s.head_alloc = 1;
     }
     bool msg_on = false;            // a message of this rank is on the wire during [tcur, tnew)
@@ -624,18 +717,21 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
                 msg_on = true;
                 if (!(ent & MSG_ALLOC)) {
                     const uint4 hb = rec_b(g, L.nb + c.mlist_node[k * R + L.r]);
-                    s.alloc_t += rec_u64(hb.z, hb.w);
+                    F64(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w);
                     c.mlist[k * R + L.r] = ent | MSG_ALLOC;
                 }
             }
         }
     }
-    if (s.alloc_t | s.free_t) {
-        int64_t cur = stat_ref<K>(c, L, R, ST_CUR) + s.alloc_t;
-        const int64_t pk = stat_ref<K>(c, L, R, ST_PEAK);
-        if (cur > pk) stat_ref<K>(c, L, R, ST_PEAK) = cur;
-        stat_ref<K>(c, L, R, ST_CUR) = cur - s.free_t;
-        s.alloc_t = s.free_t = 0;
+    {
+        const int64_t at = F64(F_ALLOC, L.lr), ft = F64(F_FREE, L.lr);
+        if (at | ft) {
+            const int64_t cur = F64(F_CUR, L.lr) + at;
+            if (cur > F64(F_PEAK, L.lr)) F64(F_PEAK, L.lr) = cur;
+            F64(F_CUR, L.lr) = cur - ft;
+            F64(F_ALLOC, L.lr) = 0;
+            F64(F_FREE, L.lr) = 0;
+        }
     }
     if (tnew == TINF) return;
     const int64_t dt = tnew - tcur;
@@ -646,8 +742,8 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
 #pragma unroll
         for (int q = 0; q < (K & 7); q++) comp_on |= s.occ_n[q] >= 0;
         if (comp_on) {
-            stat_ref<K>(c, L, R, ST_COMP) += dt;
-            if (comm_on) stat_ref<K>(c, L, R, ST_OVL) += dt;
+            F64(F_COMP, L.lr) += dt;
+            if (comm_on) F64(F_OVL, L.lr) += dt;
         }
     }
 }
@@ -790,7 +886,7 @@ __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, co
             for (int64_t j = threadIdx.x; j < nm; j += blockDim.x) {
                 const int lm = g.inst_mem_rank[m0 + j] - base;
                 if (lm < 0 || lm >= RL) continue;       // another CTA's rank
-                const int64_t ce = c.comm_end[lm];
+                const int64_t ce = F64(F_COMM_END, lm);
                 local = ce > local ? ce : local;
             }
             s = gmax_i64<CL>(local, sh, par);
@@ -802,11 +898,10 @@ __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, co
         if (full_node >= 0) {
             for (int lm = threadIdx.x; lm < RL; lm += blockDim.x) {
                 const int m = base + lm;
-                c.comm_end[lm] = e;
-                const int slot = c.ring_tail[lm]++;
+                F64(F_COMM_END, lm) = e;
+                const int slot = F32(Q_RING_TAIL, lm)++;
                 c.ring_inst[slot * R + m] = i;
                 c.ring_node[slot * R + m] = full_node;
-                c.cp[full_node * R + m] = (int64_t)(epoch | (uint64_t)cpv);
                 record(g, o, cfg, m, full_node, s, e);
             }
             uni = true;
@@ -816,11 +911,10 @@ __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, co
                 const int m = g.inst_mem_rank[m0 + j], node = g.inst_mem_node[m0 + j];
                 const int lm = m - base;
                 if (lm < 0 || lm >= RL) continue;
-                c.comm_end[lm] = e;
-                const int slot = c.ring_tail[lm]++;
+                F64(F_COMM_END, lm) = e;
+                const int slot = F32(Q_RING_TAIL, lm)++;
                 c.ring_inst[slot * R + m] = i;
                 c.ring_node[slot * R + m] = node;
-                c.cp[node * R + m] = (int64_t)(epoch | (uint64_t)cpv);
                 record(g, o, cfg, m, node, s, e);
             }
             uni = false;
@@ -865,7 +959,7 @@ template <int K, bool CL>
 __global__ void __launch_bounds__(1024, 1)
     sweep_kernel(const __grid_constant__ DevGraph g, const __grid_constant__ DevPoints p,
                  const __grid_constant__ DevOut o, const __grid_constant__ DevScratch sc) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned char *smem = fl_smem;
     Shared &sh = *reinterpret_cast<Shared *>(smem);
     constexpr int KK = K | (CL ? 16 : 0);   // helpers see the cluster variant through K's bit 16
     const int R = g.R;
@@ -884,14 +978,9 @@ __global__ void __launch_bounds__(1024, 1)
     if (tid == 0) {
         c.R = R;
         c.RL = RL;
-        c.SR = CL ? bd : R;
         c.base = base_r;
         c.crank = crank;
         c.CS = CS;
-        unsigned char *sp = smem + sc.sm_off_dyn;
-        c.comm_end = reinterpret_cast<int64_t *>(sp);
-        c.stat = c.comm_end + bd;
-        c.ring_tail = reinterpret_cast<int32_t *>(c.stat + ST_N * bd);
         unsigned char *base = sc.base + (size_t)cid * sc.slot_bytes;
         const size_t words = (size_t)g.max_words * R;
         uint64_t *gbits = reinterpret_cast<uint64_t *>(base + sc.off_bits);
@@ -920,6 +1009,8 @@ __global__ void __launch_bounds__(1024, 1)
         c.ncomp = CL ? ctr : &sh.ncomp;
         c.nmcomp = CL ? ctr + 1 : &sh.nmcomp;
         c.lead_cta = crank == 0;
+        c.touch = sc.touch_in_smem;
+        sh.prg = reinterpret_cast<int64_t *>(base + sc.off_prf) + (size_t)crank * (F_N64 - F_NSM) * FL_SR;
         const int M = g.n_msg;
         int64_t *mb = reinterpret_cast<int64_t *>(base + sc.off_msg);
         c.msg_sendt = mb;
@@ -947,7 +1038,7 @@ __global__ void __launch_bounds__(1024, 1)
     const bool active = tid < RL;
     Lane L;
     L.r = active ? base_r + tid : base_r;
-    L.lr = CL ? tid : L.r;
+    L.lr = tid;
     L.br = sc.touch_in_smem ? tid : L.r;
     L.dr = sc.done_in_smem ? tid : L.r;
     {
@@ -1026,14 +1117,11 @@ __global__ void __launch_bounds__(1024, 1)
             else zero_cols<CL>(c.done, (size_t)g.max_words, R, base_r, RL);
         }
         if (sc.touch_in_smem) for (size_t i = tid; i < (size_t)g.max_words * bd; i += bd) c.touched[i] = 0;
-        else zero_cols<CL>(c.touched, (size_t)g.max_words, R, base_r, RL);
         if (tid == 0) { sh.cend_all = 0; sh.cend_uniform = 1; }
-        for (int lr = tid; lr < bd; lr += bd) {
-            c.comm_end[lr] = 0;
-            c.ring_tail[lr] = 0;
 #pragma unroll
-            for (int k = 0; k < ST_N; k++) c.stat[k * bd + lr] = 0;
-        }
+        for (int k = 0; k < F_N64; k++) F64(k, tid) = 0;
+#pragma unroll
+        for (int k = 0; k < Q_N32; k++) F32(k, tid) = 0;
         bad = gor<CL>(bad, sh, par);
         cap_bad = gor<CL>(cap_bad, sh, par);
         if (cap_bad) bad = 2;
@@ -1056,23 +1144,23 @@ __global__ void __launch_bounds__(1024, 1)
         f.epoch = (uint64_t)epoch << 58;
         f.init = 1;
         f.fold = g.fold_ok && !zero && !zdur;
+        f.touch = sc.touch_in_smem;
 
         // ---- per-rank state ----
         Rank<KK> s;
         s.due.head = s.rc.head = s.rh.head = -1;
-        s.due.sum = s.rc.sum = s.rh.sum = 0;
-        s.host_slot = 0; s.host_e = 0; s.host_n = -1;
+        s.host_n = -1;
         const int ncs = p.compute_streams;
 #pragma unroll
-        for (int q = 0; q < (K & 7); q++) { s.slot[q] = q < ncs ? 0 : TINF; s.occ_e[q] = 0; s.occ_n[q] = -1; }
-        s.head_s = s.head_e = 0; s.head_node = 0; s.head_alloc = 0;
+        for (int q = 0; q < (K & 7); q++) {
+            if constexpr ((K & 7) > 1) s.slot[q] = q < ncs ? 0 : TINF;
+            s.occ_e[q] = 0;
+            s.occ_n[q] = -1;
+        }
+        s.head_s = s.head_e = 0; s.head_alloc = 0;
         s.ring_head = s.ring_seen = 0;
-        s.alloc_t = active ? g.s_init_alloc[g.rank_struct[L.r]] : 0;
-        s.free_t = 0;
-        s.cpmax = 0;
+        F64(F_ALLOC, tid) = active ? g.s_init_alloc[g.rank_struct[L.r]] : 0;
         s.commcum = 0;
-        s.comp_a = 0;
-        s.done_cnt = 0;
         s.pop_seq = 0;
         constexpr bool MSG = (K & 8) != 0;
 
@@ -1114,7 +1202,7 @@ __global__ void __launch_bounds__(1024, 1)
                     dispatch(g, c, L, s, f, tr.y, rec_b(g, L.nb + tr.y), 0, tr.z, 0);
                 }
                 if (prev >= 0) start_phase(g, o, c, L, s, 0, cfg);
-                s.done_cnt += g.s_nstatic[st];
+                F32(Q_DONE, tid) += g.s_nstatic[st];
                 if (o.ev_start)
                     for (int q = g.static_off[st]; q < g.static_off[st + 1]; q++)
                         record(g, o, cfg, L.r, g.static_list[q], 0, 0);
@@ -1159,8 +1247,9 @@ __global__ void __launch_bounds__(1024, 1)
                     if (L.r > rmin) start_phase(g, o, c, L, s, t, cfg);
                     s.pop_seq = 0;
                     while (s.due.head >= 0) {
-                        const int x = ms_pop(s.due, c.due, R, L.r);
-                        pop_event(g, c, L, s, f, x, t);
+                        int64_t fx;
+                        const int x = ms_pop_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, fx);
+                        pop_event(g, c, L, s, f, x, fx, t);
                         start_phase(g, o, c, L, s, t, cfg);
                     }
                 }
@@ -1168,15 +1257,16 @@ __global__ void __launch_bounds__(1024, 1)
                 // serial mode: the reference loop verbatim, one pop per iteration
                 if (active) gather_due(g, c, L, s, t);
                 for (;;) {
-                    const uint64_t k2 = (active && s.due.head >= 0) ? (((uint64_t)L.r << 13) | (uint64_t)s.due.head)
+                    const uint64_t k2 = (active && s.due.head >= 0) ? (((uint64_t)L.r << 13) | (uint64_t)ms_min(s.due))
                                                                      : KINF;
                     const uint64_t m2 = gmin_key<CL>(k2, sh, par);
                     if (m2 == KINF) break;
                     f.step++;
                     if (active && (int)(m2 >> 13) == L.r) {
                         s.pop_seq = 0;
-                        const int x = ms_pop(s.due, c.due, R, L.r);
-                        pop_event(g, c, L, s, f, x, t);
+                        int64_t fx;
+                        const int x = ms_pop_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, fx);
+                        pop_event(g, c, L, s, f, x, fx, t);
                     }
                     if (active) start_phase(g, o, c, L, s, t, cfg);
                     const int64_t v = reserve<MSG, CL>(g, o, c, sh, par, t, false, cfg, f.epoch, topo,
@@ -1192,23 +1282,24 @@ __global__ void __launch_bounds__(1024, 1)
         if (active) advance(g, c, L, s, tcur, TINF);
 
         // ---- row: reductions over ranks (cli.py:336-341) ----
-        int dead = active && s.done_cnt != my_n;
+        int dead = active && F32(Q_DONE, tid) != my_n;
         dead = gor<CL>(dead | overflow, sh, par);
         dirty = dead != 0;
         int64_t vals[6] = {0, 0, 0, 0, 0, 0};
         if (active) {
-            const int64_t comm = s.commcum;
-            vals[0] = stat_ref<KK>(c, L, R, ST_FIN);
-            vals[1] = s.cpmax > cpm ? s.cpmax : cpm;
-            vals[2] = stat_ref<KK>(c, L, R, ST_COMP);
+            const int64_t comm = s.commcum, cpx = F64(F_CPMAX, tid);
+            vals[0] = F64(F_FIN, tid);
+            vals[1] = cpx > cpm ? cpx : cpm;
+            vals[2] = F64(F_COMP, tid);
             vals[3] = comm;
-            vals[4] = comm - stat_ref<KK>(c, L, R, ST_OVL);
-            vals[5] = stat_ref<KK>(c, L, R, ST_PEAK);
+            vals[4] = comm - F64(F_OVL, tid);
+            vals[5] = F64(F_PEAK, tid);
             if (o.rank_stats) {
                 int64_t *rs = o.rank_stats + ((size_t)cfg * R + L.r) * 5;
                 rs[0] = vals[0]; rs[1] = vals[2]; rs[2] = vals[3]; rs[3] = vals[4]; rs[4] = vals[5];
             }
         }
+#pragma unroll
         for (int k = 0; k < 6; k++) {
             const int64_t v = gmax_i64<CL>(vals[k], sh, par);
             if (is_leader) o.rows[(size_t)cfg * 6 + k] = v;
@@ -1330,10 +1421,23 @@ cudaError_t sweep_set_smem(size_t smem) {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<T, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     FL_SET(1) FL_SET(2) FL_SET(4) FL_SET(9) FL_SET(10) FL_SET(12)
 #undef FL_SET
+#ifdef FL_CARVEOUT
+    // leave the rest of the SM's SRAM to L1 (register spills live there)
+    int pct = (int)((smem + 8192) * 100 / (228 * 1024)) + 1;
+    pct = pct > 100 ? 100 : pct;
+#define FL_CO(T) \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<T, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct); \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<T, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    FL_CO(1) FL_CO(2) FL_CO(4) FL_CO(9) FL_CO(10) FL_CO(12)
+#undef FL_CO
+#endif
     return e;
 }
 
-size_t sweep_shared_header_bytes() { return (sizeof(Shared) + 15) / 16 * 16; }
+size_t sweep_shared_header_bytes() { return SM_HDR; }
+size_t sweep_shared_bytes_per_rank() { return 8 * F_NSM + 4 * Q_N32; }   // x FL_SR lanes
+size_t sweep_global_bytes_per_rank() { return 8 * (F_N64 - F_NSM); }
+int sweep_plane_lanes() { return FL_SR; }
 
 cudaError_t launch_cp(const DevGraph &g, const DevPoints &p, int nv, const int32_t *order, const int32_t *vkind,
                       const int32_t *va, const int32_t *vb, const int32_t *vsend, const int32_t *vmsg,

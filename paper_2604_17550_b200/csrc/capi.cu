@@ -191,6 +191,13 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
         // When one consumer depends (transitively) on all the others it is always the
         // last to finish, so the free can be attributed to it statically.
         std::vector<int32_t> last_cons((size_t)(total_t > 0 ? total_t : 1), -1);
+        // Dependency-edge classes (engine.cu pop_event), with static hosts folded away:
+        // when a node's remaining predecessors are totally ordered by ancestry, the order
+        // in which they complete is the same in every schedule, so its readiness needs no
+        // counting -- the first only writes the critical-path accumulator, the middle ones
+        // max into it without reading it back, and the last reads it and dispatches.
+        std::vector<int32_t> succ_ent((size_t)(ne_succ > 0 ? ne_succ : 1));
+        for (int q = 0; q < ne_succ; q++) succ_ent[q] = d->succ_idx[q];      // class 0: counted
         for (int s = 0; s < S; s++) {
             const int nb = d->s_node_off[s], n = d->s_node_off[s + 1] - nb;
             const int tb = d->s_tens_off[s], nt = d->s_tens_off[s + 1] - tb;
@@ -214,6 +221,35 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
                 }
             }
             if ((int)order.size() != n) continue;   // cyclic: leave every free to the run-time check
+            {
+                auto is_anc = [&](int a, int b) { return (anc[(size_t)b * W + (a >> 6)] >> (a & 63)) & 1ull; };
+                std::vector<int> P;
+                for (int x = 0; x < n; x++) {
+                    if (is_static[nb + x]) continue;
+                    for (int q = d->succ_off[nb + x]; q < d->succ_off[nb + x + 1]; q++) {
+                        const int w = d->succ_idx[q];
+                        P.clear();
+                        for (int u = d->pred_off[nb + w]; u < d->pred_off[nb + w + 1]; u++)
+                            if (!is_static[nb + d->pred_idx[u]]) P.push_back(d->pred_idx[u]);
+                        int cls = 0;
+                        if (P.size() == 1) {
+                            cls = fl::FL_EDGE_SINGLE;
+                        } else {
+                            bool ordered = true, first = true, last = true;
+                            for (size_t i = 0; i < P.size() && ordered; i++)
+                                for (size_t j = i + 1; j < P.size() && ordered; j++)
+                                    ordered = is_anc(P[i], P[j]) || is_anc(P[j], P[i]);
+                            for (int p : P) {
+                                if (p == x) continue;
+                                first &= is_anc(x, p);
+                                last &= is_anc(p, x);
+                            }
+                            if (ordered) cls = first ? fl::FL_EDGE_FIRST : last ? fl::FL_EDGE_LAST : fl::FL_EDGE_MID;
+                        }
+                        succ_ent[q] = w | (cls << 16);
+                    }
+                }
+            }
             for (int t = 0; t < nt; t++) {
                 const int c0 = d->tens_cons_off[tb + t], c1 = d->tens_cons_off[tb + t + 1];
                 if (c1 - c0 < 2) continue;
@@ -286,6 +322,7 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
         if (!rc) rc = upload(g, tc.data(), tc.size(), &dg.tens_rng);
         if (!rc) rc = upload(g, mfree.data(), mfree.size(), &dg.free_tens);
         if (!rc) rc = upload(g, s_nstatic.data(), s_nstatic.size(), &dg.s_nstatic);
+        if (!rc) rc = upload(g, succ_ent.data(), succ_ent.size(), &dg.succ_ent);
         if (!rc) rc = upload(g, trig_off.data(), trig_off.size(), &dg.trig_off);
         if (!rc) rc = upload(g, trig.data(), trig.size(), &dg.trig);
         if (!rc) rc = upload(g, static_off.data(), static_off.size(), &dg.static_off);

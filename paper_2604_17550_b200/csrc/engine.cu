@@ -37,6 +37,7 @@
 // contraction.  Times are int64 ns.
 
 #include <cooperative_groups.h>
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -231,6 +232,20 @@ __device__ __forceinline__ int gor(int v, Shared &sh, int &par) {
 }
 
 // ---------------------------------------------------------- rank state
+
+#ifdef FL_PROFILE     // development only: per-segment cycle counts of warp 0 of CTA 0
+__device__ unsigned long long fl_prof[16];
+#define PROF_MARK(k)                                                                      \
+    do {                                                                                  \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                                        \
+            const long long now_ = clock64();                                             \
+            atomicAdd(&fl_prof[k], (unsigned long long)(now_ - prof_t));                  \
+            prof_t = now_;                                                                \
+        }                                                                                 \
+    } while (0)
+#else
+#define PROF_MARK(k) do {} while (0)
+#endif
 
 // Node record built by capi.cu, three 16-byte words per node so that one
 // broadcast load per word serves the 32 ranks of a warp visiting the node:
@@ -586,10 +601,31 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
     const uint64_t fx = (uint64_t)fx64;     // this node's critical-path finish
     int seq = 0;
     for (uint32_t q = xa.x; q < xa.y; q++, seq++) {
-        const int d = g.succ_idx[q];
+        const uint32_t ent = (uint32_t)g.succ_ent[q];
+        const int d = (int)(ent & 0xffffu);
+        const int cls = f.fold ? (int)(ent >> 16) : FL_EDGE_COUNTED;
+        int64_t *slot = c.cp + (d * R + L.r);
+        // Statically ordered predecessors (capi.cu): no counting, and only the last one
+        // reads the accumulator.  A node that waits on a missing one is never dispatched.
+        if (cls == FL_EDGE_FIRST) {
+            *slot = (int64_t)(f.epoch | fx);
+            continue;
+        }
+        if (cls == FL_EDGE_MID) {
+            atomicMax(reinterpret_cast<unsigned long long *>(slot), (unsigned long long)(f.epoch | fx));
+            continue;
+        }
         const uint4 db = rec_b(g, L.nb + d);
         if (rec_never(db)) continue;
-        int64_t *slot = c.cp + (d * R + L.r);
+        if (cls == FL_EDGE_SINGLE) {
+            dispatch(g, c, L, s, f, d, db, (int64_t)fx, seq, t);
+            continue;
+        }
+        if (cls == FL_EDGE_LAST) {
+            const uint64_t a = (uint64_t)__ldcg(slot) & VAL48;    // the first/middle ones' max (at L2)
+            dispatch(g, c, L, s, f, d, db, (int64_t)(a > fx ? a : fx), seq, t);
+            continue;
+        }
         // first dependency to complete: the word holds nothing of this design point,
         // so skip reading it (a DRAM round trip on the critical chain)
         uint64_t a;
@@ -1216,10 +1252,16 @@ __global__ void __launch_bounds__(1024, 1)
 
         // ---- event loop ----
         const int64_t TCAP = (int64_t)1 << 48;   // 48-bit accumulators; keys pack (t, rank)
+#ifdef FL_PROFILE
+        long long prof_t = clock64();
+#endif
         for (;;) {
+            PROF_MARK(0);                                   // loop back-edge
             int64_t nt = active ? next_time(g, c, L, s, tcur) : TINF;
             uint64_t key = nt == TINF ? KINF : ((uint64_t)(nt < TCAP ? nt : TCAP) << 14) | (uint64_t)L.r;
+            PROF_MARK(1);                                   // next_time + key
             uint64_t kmin = gmin_key<CL>(key, sh, par);
+            PROF_MARK(2);                                   // step reduction (incl. barrier wait)
             // collectives completed by the previous step's pops: reserve them now (the
             // reduction's barrier made every arrival visible), then re-derive the next time
             const int nc = CL ? *c.ncomp : sh.ncomp, nmc = MSG ? (CL ? *c.nmcomp : sh.nmcomp) : 0;
@@ -1236,21 +1278,27 @@ __global__ void __launch_bounds__(1024, 1)
             const int64_t t = (int64_t)(kmin >> 14);
             const int rmin = (int)(kmin & 0x3fff);
             if (t >= TCAP || f.step >= (1ull << 25) - 2) { overflow = true; break; }
+            PROF_MARK(3);                                   // reservations
             if (t > tcur) {
                 if (active) advance(g, c, L, s, tcur, t);
                 tcur = t;
             }
             f.step++;
+            PROF_MARK(4);                                   // advance
             if (!zero) {
                 if (active) {
                     gather_due(g, c, L, s, t);
+                    PROF_MARK(5);                           // gather_due
                     if (L.r > rmin) start_phase(g, o, c, L, s, t, cfg);
+                    PROF_MARK(6);                           // tie start phase
                     s.pop_seq = 0;
                     while (s.due.head >= 0) {
                         int64_t fx;
                         const int x = ms_pop_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, fx);
                         pop_event(g, c, L, s, f, x, fx, t);
+                        PROF_MARK(7);                       // pop_event
                         start_phase(g, o, c, L, s, t, cfg);
+                        PROF_MARK(8);                       // start phase after a pop
                     }
                 }
             } else {
@@ -1280,6 +1328,14 @@ __global__ void __launch_bounds__(1024, 1)
             }
         }
         if (active) advance(g, c, L, s, tcur, TINF);
+#ifdef FL_PROFILE
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&fl_prof[15], 1ull);
+        if (blockIdx.x == 0 && threadIdx.x == 0 && cfg + ncl >= p.n) {
+            printf("FLPROF points %llu", fl_prof[15]);
+            for (int k = 0; k < 9; k++) printf(" s%d %llu", k, fl_prof[k]);
+            printf("\n");
+        }
+#endif
 
         // ---- row: reductions over ranks (cli.py:336-341) ----
         int dead = active && F32(Q_DONE, tid) != my_n;

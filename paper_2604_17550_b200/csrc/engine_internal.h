@@ -5,6 +5,8 @@
 
 namespace fl {
 
+enum { FL_EDGE_COUNTED = 0, FL_EDGE_SINGLE = 1, FL_EDGE_FIRST = 2, FL_EDGE_MID = 3, FL_EDGE_LAST = 4 };
+
 // Device copy of fl_graph_desc (pointers are device pointers).
 struct DevGraph {
     int R, S, n_inst, coll_stride, max_nodes, max_words, total_nodes, total_tens;
@@ -29,6 +31,7 @@ struct DevGraph {
     int needs_done;              // some tensor's last consumer is only known at run time
     const int32_t *s_nstatic, *trig_off, *static_off, *static_list;
     const int4 *trig;            // {trigger host, node, position in the host's dependents, -}
+    const int32_t *succ_ent;     // succ_idx | edge class << 16 (FL_EDGE_*, valid when static hosts are folded)
     // messages
     const int64_t *rank_value;
     int n_msg, p2p_stride;

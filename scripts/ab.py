@@ -28,7 +28,17 @@ def child(name, workload, points, reps):
     import torch
     from paper_2604_17550_b200 import sweep as S
     from paper_2604_17550_b200.engine import Engine
+    ranks = 0
+    if ":" in workload:                 # e.g. c3:512 -- the C3 grid on fsdp:512 (scaling probes)
+        workload, ranks = workload.split(":")[0], int(workload.split(":")[1])
     w = {"c3": S.c3_workload, "c2": S.c2_workload, "c4": S.c4_workload}[workload]()
+    if ranks:
+        w.parallel = f"fsdp:{ranks}"
+        side = int(round(ranks ** 0.5))
+        while ranks % side:
+            side -= 1
+        w.points.rows[:] = np.where(w.points.rows > 0, side, 0)
+        w.points.cols[:] = np.where(w.points.cols > 0, ranks // side, 0)
     graphs = S.workload_graphs(w)
     n_all = len(w.points)
     if points and points < n_all:

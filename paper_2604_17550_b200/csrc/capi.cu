@@ -309,6 +309,17 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
             }
             trig_off[s + 1] = (int32_t)trig.size();
         }
+        // the initial dispatch list without static hosts (what the folded t = 0 visits)
+        std::vector<int32_t> init_ns_off(S + 1, 0), init_ns;
+        for (int s = 0; s < S; s++) {
+            const int nb = d->s_node_off[s];
+            for (int q = d->s_init_off[s]; q < d->s_init_off[s + 1]; q++) {
+                const int v = d->init_list[q];
+                if (!is_static[nb + v] && !(d->node_flags[nb + v] & 1)) init_ns.push_back(v);
+            }
+            init_ns_off[s + 1] = (int32_t)init_ns.size();
+        }
+        if (init_ns.empty()) init_ns.push_back(0);
         int fold_ok = 1;
         for (int s = 0; s < S; s++) fold_ok &= s_fold[s];
         dg.fold_ok = fold_ok;
@@ -323,6 +334,8 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
         if (!rc) rc = upload(g, mfree.data(), mfree.size(), &dg.free_tens);
         if (!rc) rc = upload(g, s_nstatic.data(), s_nstatic.size(), &dg.s_nstatic);
         if (!rc) rc = upload(g, succ_ent.data(), succ_ent.size(), &dg.succ_ent);
+        if (!rc) rc = upload(g, init_ns_off.data(), init_ns_off.size(), &dg.s_init_ns_off);
+        if (!rc) rc = upload(g, init_ns.data(), init_ns.size(), &dg.init_ns);
         if (!rc) rc = upload(g, trig_off.data(), trig_off.size(), &dg.trig_off);
         if (!rc) rc = upload(g, trig.data(), trig.size(), &dg.trig);
         if (!rc) rc = upload(g, static_off.data(), static_off.size(), &dg.static_off);

@@ -536,6 +536,14 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
     }
 }
 
+// max of a 64-bit value over the lanes of `grp` (all of which call this)
+__device__ __forceinline__ unsigned long long group_max_u64(unsigned grp, unsigned long long v) {
+    const unsigned hi = (unsigned)(v >> 32), lo = (unsigned)v;
+    const unsigned mh = __reduce_max_sync(grp, hi);
+    const unsigned ml = __reduce_max_sync(grp, hi == mh ? lo : 0u);
+    return ((unsigned long long)mh << 32) | ml;
+}
+
 // A node whose every dependency has completed (simulator.py:247-268); `cps`
 // is its contention-free critical-path start (simulator.py:449).
 template <int K>
@@ -557,13 +565,18 @@ __device__ __forceinline__ void dispatch(const DevGraph &g, const Ctx &c, const 
     }
     if (kind == FL_COLL) {
         const int i = g.rank_coll_inst[L.r * g.coll_stride + (int)rb.y];
-        atomicMax((unsigned long long *)&c.inst_cpmax[i], (unsigned long long)cps);
-        if (!f.init) {
-            const unsigned long long key = (f.step << 39) | ((unsigned long long)L.r << 25) |
-                                           ((unsigned long long)s.pop_seq << 12) | (unsigned long long)seq;
-            atomicMax(&c.inst_ckey[i], key);
+        // warp-aggregated: the lanes arriving at the same instance together update it once
+        const unsigned grp = __match_any_sync(__activemask(), i);
+        const unsigned long long cm = group_max_u64(grp, (unsigned long long)cps);
+        const unsigned long long key = (f.step << 39) | ((unsigned long long)L.r << 25) |
+                                       ((unsigned long long)s.pop_seq << 12) | (unsigned long long)seq;
+        const unsigned long long km = f.init ? 0ull : group_max_u64(grp, key);
+        if ((int)(threadIdx.x & 31) == __ffs(grp) - 1) {
+            atomicMax((unsigned long long *)&c.inst_cpmax[i], cm);
+            if (!f.init) atomicMax(&c.inst_ckey[i], km);
+            const int cnt = __popc(grp);
+            if (atomicSub(&c.inst_wait[i], cnt) == cnt) c.complist[atomicAdd(c.ncomp, 1)] = i;
         }
-        if (atomicSub(&c.inst_wait[i], 1) == 1) c.complist[atomicAdd(c.ncomp, 1)] = i;
         return;
     }
     const int64_t fin = cps + c.dur[L.nb + d];
@@ -1203,11 +1216,18 @@ __global__ void __launch_bounds__(1024, 1)
         // ---- t = 0: initial dispatch + start phase (simulator.py:275-277) ----
         if (active) {
             const int st = g.rank_struct[L.r];
-            for (int q = g.s_init_off[st]; q < g.s_init_off[st + 1]; q++) {
-                const int d = g.init_list[q];
-                const uint4 db = rec_b(g, L.nb + d);
-                if (rec_never(db) || (f.fold && rec_static(db))) continue;
-                dispatch(g, c, L, s, f, d, db, 0, 0, 0);
+            if (f.fold) {
+                for (int q = g.s_init_ns_off[st]; q < g.s_init_ns_off[st + 1]; q++) {
+                    const int d = g.init_ns[q];
+                    dispatch(g, c, L, s, f, d, rec_b(g, L.nb + d), 0, 0, 0);
+                }
+            } else {
+                for (int q = g.s_init_off[st]; q < g.s_init_off[st + 1]; q++) {
+                    const int d = g.init_list[q];
+                    const uint4 db = rec_b(g, L.nb + d);
+                    if (rec_never(db)) continue;
+                    dispatch(g, c, L, s, f, d, db, 0, 0, 0);
+                }
             }
             start_phase(g, o, c, L, s, 0, cfg);
         }

@@ -31,6 +31,7 @@ struct DevGraph {
     int needs_done;              // some tensor's last consumer is only known at run time
     const int32_t *s_nstatic, *trig_off, *static_off, *static_list;
     const int4 *trig;            // {trigger host, node, position in the host's dependents, -}
+    const int32_t *s_init_ns_off, *init_ns;   // initial dispatch list without static hosts
     const int32_t *succ_ent;     // succ_idx | edge class << 16 (FL_EDGE_*, valid when static hosts are folded)
     // messages
     const int64_t *rank_value;

@@ -303,7 +303,7 @@ enum {
 #endif
 constexpr int F_NSM = FL_NSM;
 constexpr int FL_SR = 1024;                         // plane stride (lanes)
-enum { Q_RING_TAIL = 0, Q_HEAD_NODE, Q_HEAD_INST, Q_DONE, Q_N32 };
+enum { Q_RING_TAIL = 0, Q_RING_HEAD, Q_RING_SEEN, Q_HEAD_NODE, Q_HEAD_INST, Q_DONE, Q_N32 };
 
 extern __shared__ __align__(16) unsigned char fl_smem[];
 constexpr unsigned SM_HDR = (sizeof(Shared) + 15) / 16 * 16;
@@ -387,12 +387,11 @@ struct Rank {
     int64_t slot[K & 7];            // compute stream free-at times (K > 1 only: with one stream
                                     // the stream is busy at t iff it has an occupant)
     int64_t occ_e[K & 7];           // end of the node running on each compute stream
-    int64_t head_s, head_e;         // comm-FIFO head (valid iff ring_head < ring_seen)
+    int64_t head_s, head_e;         // comm-FIFO head: start (HS_ALLOC once its outputs are allocated),
+                                    // end (TINF when the FIFO is empty); FIFO indices in Q_RING_*
     int64_t commcum;                // integral of "comm stream busy" up to the current step (= comm busy)
     int host_n;                     // node running on the host stream (end in F_HOST_E), or -1
     int occ_n[K & 7];
-    int head_alloc;
-    int ring_head, ring_seen;
     int pop_seq;
 };
 
@@ -473,7 +472,7 @@ __device__ __forceinline__ void record(const DevGraph &g, const DevOut &o, int c
 // One rank's start phase at time t (simulator.py:282-297 restricted to this rank).
 template <int K>
 __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, const Ctx &c, const Lane &L,
-                                            Rank<K> &s, int64_t t, int cfg) {
+                                            Rank<K> &s, const Step &f, int64_t t, int cfg) {
     const int R = c.R;
     while (s.rh.head >= 0 && s.host_n < 0) {      // the host stream is free at t (gather_due ran at t)
         int64_t v;
@@ -510,6 +509,7 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
             F64(F_COMP, L.lr) += e - t;
             F64(F_COMP_A, L.lr) = s.commcum;
         }
+
 #ifdef FL_PREFETCH
         if (e > t && !c.touch) {          // the successors' accumulator words are read when x completes
             const uint4 xa = rec_a(g, L.nb + x);
@@ -662,15 +662,19 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
     }
 }
 
+constexpr int64_t HS_ALLOC = INT64_MIN;   // head_s once the head's outputs are allocated (it started)
+
 template <int K>
 __device__ __forceinline__ void load_head(const Ctx &c, const Lane &L, Rank<K> &s) {
-    if (s.ring_head < s.ring_seen) {
-        const int i = c.ring_inst[s.ring_head * c.R + L.r];
-        F32(Q_HEAD_NODE, L.lr) = c.ring_node[s.ring_head * c.R + L.r];
+    const int h = F32(Q_RING_HEAD, L.lr);
+    if (h < F32(Q_RING_SEEN, L.lr)) {
+        const int i = c.ring_inst[h * c.R + L.r];
+        F32(Q_HEAD_NODE, L.lr) = c.ring_node[h * c.R + L.r];
         F32(Q_HEAD_INST, L.lr) = i;
         s.head_s = c.inst_s[i];
         s.head_e = c.inst_e[i];
-        s.head_alloc = 0;
+    } else {
+        s.head_e = TINF;
     }
 }
 
@@ -678,10 +682,10 @@ __device__ __forceinline__ void load_head(const Ctx &c, const Lane &L, Rank<K> &
 template <int K>
 __device__ __forceinline__ void refresh_ring(const Ctx &c, const Lane &L, Rank<K> &s) {
     const int tail = F32(Q_RING_TAIL, L.lr);
-    if (tail != s.ring_seen) {
-        const bool was_empty = s.ring_head == s.ring_seen;
-        s.ring_seen = tail;
-        if (was_empty) load_head(c, L, s);
+    const int seen = F32(Q_RING_SEEN, L.lr);
+    if (tail != seen) {
+        F32(Q_RING_SEEN, L.lr) = tail;
+        if (s.head_e == TINF) load_head(c, L, s);
     }
 }
 
@@ -692,7 +696,7 @@ __device__ __forceinline__ int64_t next_time(const DevGraph &g, const Ctx &c, co
     int64_t nt = s.host_n >= 0 ? F64(F_HOST_E, L.lr) : TINF;
 #pragma unroll
     for (int q = 0; q < (K & 7); q++) if (s.occ_n[q] >= 0 && s.occ_e[q] < nt) nt = s.occ_e[q];
-    if (s.ring_head < s.ring_seen && s.head_e < nt) nt = s.head_e;
+    if (s.head_e < nt) nt = s.head_e;
     if ((K & 8) && c.mcount[L.r] > 0) {          // in-flight messages, sorted by end time
         const int64_t e = c.msg_e[c.mlist[L.r] & ~MSG_ALLOC];
         nt = e < nt ? e : nt;
@@ -717,13 +721,13 @@ __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, cons
             s.occ_n[q] = -1;
             if ((K & 7) == 1) F64(F_OVL, L.lr) += s.commcum - F64(F_COMP_A, L.lr);   // comm time under [start, t)
         }
-    while (s.ring_head < s.ring_seen && s.head_e == t) {
+    while (s.head_e == t) {
         const int hn = F32(Q_HEAD_NODE, L.lr), hi = F32(Q_HEAD_INST, L.lr);
-        if (!s.head_alloc) { const uint4 hb = rec_b(g, L.nb + hn); F64(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }  // zero-length: starts now
+        if (s.head_s != HS_ALLOC) { const uint4 hb = rec_b(g, L.nb + hn); F64(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }  // zero-length: starts now
         // every member of an instance finishes at max over members' critical-path starts + duration
         // (simulator.py:419-428)
         ms_insert_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, hn, c.inst_cpmax[hi] + c.inst_dur[hi]);
-        s.ring_head++;
+        F32(Q_RING_HEAD, L.lr)++;
         load_head(c, L, s);
     }
     if (K & 8) {
@@ -751,11 +755,11 @@ template <int K>
 __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const Lane &L, Rank<K> &s,
                                         int64_t tcur, int64_t tnew) {
     const int R = c.R;
-    const bool head = s.ring_head < s.ring_seen;
-    if (head && !s.head_alloc && s.head_s <= tcur) {   // a collective that started by tcur
+    const bool head = s.head_e != TINF;
+    if (head && s.head_s != HS_ALLOC && s.head_s <= tcur) {   // a collective that started by tcur
         const uint4 hb = rec_b(g, L.nb + F32(Q_HEAD_NODE, L.lr));
         F64(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w);
-        s.head_alloc = 1;
+        s.head_s = HS_ALLOC;
     }
     bool msg_on = false;            // a message of this rank is on the wire during [tcur, tnew)
     if (K & 8) {
@@ -980,7 +984,9 @@ __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, co
         if (MSG && nmc) reserve_msgs(g, o, c, nmc, init, topo, cols, cfg, epoch, cpm);
         if (MSG) { if (CL) *c.nmcomp = 0; else sh.nmcomp = 0; }
     }
-    gsync<CL>();
+    // Without messages nothing written above is read before the caller's next barrier
+    // (its step reduction, or reserve()'s own); the message phase fills other ranks' lists.
+    if (MSG) gsync<CL>();
     return cpm;
 }
 
@@ -1206,8 +1212,8 @@ __global__ void __launch_bounds__(1024, 1)
             s.occ_e[q] = 0;
             s.occ_n[q] = -1;
         }
-        s.head_s = s.head_e = 0; s.head_alloc = 0;
-        s.ring_head = s.ring_seen = 0;
+        s.head_s = 0;
+        s.head_e = TINF;
         F64(F_ALLOC, tid) = active ? g.s_init_alloc[g.rank_struct[L.r]] : 0;
         s.commcum = 0;
         s.pop_seq = 0;
@@ -1229,9 +1235,11 @@ __global__ void __launch_bounds__(1024, 1)
                     dispatch(g, c, L, s, f, d, db, 0, 0, 0);
                 }
             }
-            start_phase(g, o, c, L, s, 0, cfg);
+            start_phase(g, o, c, L, s, f, 0, cfg);
         }
-        int64_t cpm = reserve<MSG, CL>(g, o, c, sh, par, 0, true, cfg, f.epoch, topo, p.cols[cfg]);
+        // (reservations also return their instances' critical-path finishes; every member's
+        // pop folds the same value into F_CPMAX, so the row needs only that)
+        reserve<MSG, CL>(g, o, c, sh, par, 0, true, cfg, f.epoch, topo, p.cols[cfg]);
         if (active) refresh_ring(c, L, s);
         f.init = 0;
         if (f.fold) {
@@ -1251,20 +1259,19 @@ __global__ void __launch_bounds__(1024, 1)
                 for (int q = g.trig_off[st]; q < g.trig_off[st + 1]; q++) {
                     const int4 tr = g.trig[q];
                     if (tr.x != prev) {
-                        if (prev >= 0) start_phase(g, o, c, L, s, 0, cfg);
+                        if (prev >= 0) start_phase(g, o, c, L, s, f, 0, cfg);
                         s.pop_seq++;
                         prev = tr.x;
                     }
                     dispatch(g, c, L, s, f, tr.y, rec_b(g, L.nb + tr.y), 0, tr.z, 0);
                 }
-                if (prev >= 0) start_phase(g, o, c, L, s, 0, cfg);
+                if (prev >= 0) start_phase(g, o, c, L, s, f, 0, cfg);
                 F32(Q_DONE, tid) += g.s_nstatic[st];
                 if (o.ev_start)
                     for (int q = g.static_off[st]; q < g.static_off[st + 1]; q++)
                         record(g, o, cfg, L.r, g.static_list[q], 0, 0);
             }
-            const int64_t v = reserve<MSG, CL>(g, o, c, sh, par, 0, false, cfg, f.epoch, topo, p.cols[cfg]);
-            cpm = v > cpm ? v : cpm;
+            reserve<MSG, CL>(g, o, c, sh, par, 0, false, cfg, f.epoch, topo, p.cols[cfg]);
             if (active) refresh_ring(c, L, s);
         }
         int64_t tcur = 0;
@@ -1286,10 +1293,9 @@ __global__ void __launch_bounds__(1024, 1)
             // reduction's barrier made every arrival visible), then re-derive the next time
             const int nc = CL ? *c.ncomp : sh.ncomp, nmc = MSG ? (CL ? *c.nmcomp : sh.nmcomp) : 0;
             if (nc | nmc) {
-                const int64_t v = reserve_n<MSG, CL>(g, o, c, sh, par, tcur, false, cfg, f.epoch, nc, nmc,
+                reserve_n<MSG, CL>(g, o, c, sh, par, tcur, false, cfg, f.epoch, nc, nmc,
                                                      topo, p.cols[cfg]);
-                cpm = v > cpm ? v : cpm;
-                if (active) refresh_ring(c, L, s);
+                    if (active) refresh_ring(c, L, s);
                 nt = active ? next_time(g, c, L, s, tcur) : TINF;
                 key = nt == TINF ? KINF : ((uint64_t)(nt < TCAP ? nt : TCAP) << 14) | (uint64_t)L.r;
                 kmin = gmin_key<CL>(key, sh, par);
@@ -1309,7 +1315,7 @@ __global__ void __launch_bounds__(1024, 1)
                 if (active) {
                     gather_due(g, c, L, s, t);
                     PROF_MARK(5);                           // gather_due
-                    if (L.r > rmin) start_phase(g, o, c, L, s, t, cfg);
+                    if (L.r > rmin) start_phase(g, o, c, L, s, f, t, cfg);
                     PROF_MARK(6);                           // tie start phase
                     s.pop_seq = 0;
                     while (s.due.head >= 0) {
@@ -1317,7 +1323,7 @@ __global__ void __launch_bounds__(1024, 1)
                         const int x = ms_pop_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, fx);
                         pop_event(g, c, L, s, f, x, fx, t);
                         PROF_MARK(7);                       // pop_event
-                        start_phase(g, o, c, L, s, t, cfg);
+                        start_phase(g, o, c, L, s, f, t, cfg);
                         PROF_MARK(8);                       // start phase after a pop
                     }
                 }
@@ -1336,11 +1342,10 @@ __global__ void __launch_bounds__(1024, 1)
                         const int x = ms_pop_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, fx);
                         pop_event(g, c, L, s, f, x, fx, t);
                     }
-                    if (active) start_phase(g, o, c, L, s, t, cfg);
-                    const int64_t v = reserve<MSG, CL>(g, o, c, sh, par, t, false, cfg, f.epoch, topo,
+                    if (active) start_phase(g, o, c, L, s, f, t, cfg);
+                    reserve<MSG, CL>(g, o, c, sh, par, t, false, cfg, f.epoch, topo,
                                                        p.cols[cfg]);
-                    cpm = v > cpm ? v : cpm;
-                    if (active) {
+                            if (active) {
                         refresh_ring(c, L, s);
                         gather_due(g, c, L, s, t);
                     }
@@ -1365,7 +1370,7 @@ __global__ void __launch_bounds__(1024, 1)
         if (active) {
             const int64_t comm = s.commcum, cpx = F64(F_CPMAX, tid);
             vals[0] = F64(F_FIN, tid);
-            vals[1] = cpx > cpm ? cpx : cpm;
+            vals[1] = cpx;
             vals[2] = F64(F_COMP, tid);
             vals[3] = comm;
             vals[4] = comm - F64(F_OVL, tid);

@@ -104,6 +104,7 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     dg.max_words = (dg.max_nodes + 63) / 64;
     dg.total_nodes = total;
     dg.total_tens = total_t;
+    dg.n_succ = d->succ_off[total];
     const int ne_pred = d->pred_off[total], ne_succ = d->succ_off[total], ne_free = d->free_off[total];
     const int ne_cons = d->tens_cons_off[total_t], ne_init = d->s_init_off[S];
     const int64_t ne_mem = d->inst_mem_off[d->n_inst];
@@ -168,7 +169,8 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
 
     // packed node records and tensor consumer ranges (engine.cu node record layout)
     {
-        std::vector<uint4> rec(3 * (size_t)(total > 0 ? total : 1));
+        std::vector<uint4> rec(2 * (size_t)(total > 0 ? total : 1));
+        std::vector<int32_t> mfree_off((size_t)(total > 0 ? total : 1), 0);
         std::vector<int32_t> mfree;
         mfree.reserve((size_t)ne_free + 1);
         // static hosts: zero in-degree, zero duration, no tensors (all start and end at t=0)
@@ -283,10 +285,13 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
             const uint64_t alloc = (uint64_t)d->node_alloc[i];
             const unsigned meta = (unsigned)d->node_kind[i] | ((unsigned)(d->node_flags[i] & 1) << 4) |
                                   ((unsigned)is_static[i] << 5) | ((unsigned)indeg_nh << 6) | ((unsigned)indeg << 16);
-            rec[3 * i] = make_uint4((unsigned)d->succ_off[i], (unsigned)d->succ_off[i + 1], m0, (uint32_t)mfree.size());
-            rec[3 * i + 1] = make_uint4(meta, (unsigned)(d->node_coll_ord[i] < 0 ? 0 : d->node_coll_ord[i]),
+            const uint32_t nmf = (uint32_t)mfree.size() - m0;
+            if (nmf > 0xffff) return fail(FL_ERR_CAPACITY, "a node frees more than 65535 shared tensors");
+            mfree_off[i] = (int32_t)m0;
+            rec[2 * i] = make_uint4((unsigned)d->succ_off[i], (unsigned)(d->succ_off[i + 1] - d->succ_off[i]) | (nmf << 16),
+                                    (uint32_t)ufree, (uint32_t)(ufree >> 32));
+            rec[2 * i + 1] = make_uint4(meta, (unsigned)(d->node_coll_ord[i] < 0 ? 0 : d->node_coll_ord[i]),
                                         (uint32_t)alloc, (uint32_t)(alloc >> 32));
-            rec[3 * i + 2] = make_uint4((uint32_t)ufree, (uint32_t)(ufree >> 32), 0u, 0u);
         }
         // nodes whose every dependency is a static host become ready during the t=0 pops of
         // those hosts, right after the highest-id one (the trigger); listed by (trigger, position)
@@ -334,6 +339,7 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
         if (!rc) rc = upload(g, mfree.data(), mfree.size(), &dg.free_tens);
         if (!rc) rc = upload(g, s_nstatic.data(), s_nstatic.size(), &dg.s_nstatic);
         if (!rc) rc = upload(g, succ_ent.data(), succ_ent.size(), &dg.succ_ent);
+        if (!rc) rc = upload(g, mfree_off.data(), mfree_off.size(), &dg.mfree_off);
         if (!rc) rc = upload(g, init_ns_off.data(), init_ns_off.size(), &dg.s_init_ns_off);
         if (!rc) rc = upload(g, init_ns.data(), init_ns.size(), &dg.init_ns);
         if (!rc) rc = upload(g, trig_off.data(), trig_off.size(), &dg.trig_off);

@@ -48,6 +48,8 @@ namespace fl {
 
 namespace cg = cooperative_groups;
 
+extern __shared__ __align__(16) unsigned char fl_smem[];   // the sweep kernel's dynamic shared memory
+
 // ------------------------------------------------------------------ costs
 
 __device__ __forceinline__ int64_t rhu(double x) {          // traceio.py:68-70
@@ -235,34 +237,35 @@ __device__ __forceinline__ int gor(int v, Shared &sh, int &par) {
 
 #ifdef FL_PROFILE     // development only: per-segment cycle counts of warp 0 of CTA 0
 __device__ unsigned long long fl_prof[16];
+__shared__ long long fl_prof_t;
 #define PROF_MARK(k)                                                                      \
     do {                                                                                  \
         if (blockIdx.x == 0 && threadIdx.x == 0) {                                        \
             const long long now_ = clock64();                                             \
-            atomicAdd(&fl_prof[k], (unsigned long long)(now_ - prof_t));                  \
-            prof_t = now_;                                                                \
+            atomicAdd(&fl_prof[k], (unsigned long long)(now_ - fl_prof_t));               \
+            fl_prof_t = now_;                                                             \
         }                                                                                 \
     } while (0)
 #else
 #define PROF_MARK(k) do {} while (0)
 #endif
 
-// Node record built by capi.cu, three 16-byte words per node so that one
-// broadcast load per word serves the 32 ranks of a warp visiting the node:
-//   a = {succ_off, succ_end, mfree_off, mfree_end}  dependents; tensors with >1 consumer
+// Node record built by capi.cu, two 16-byte words per node so that one
+// broadcast load per word serves the 32 ranks of a warp visiting the node (an L1
+// hit: the records of a graph set are a few tens of KB):
+//   a = {succ_off, succ_cnt | mfree_cnt << 16, ufree_lo, ufree_hi}
+//       dependents; tensors with more than one consumer it may free (from g.mfree_off);
+//       bytes of tensors it is the only (or statically last) consumer of
 //   b = {meta, coll_ord, alloc_lo, alloc_hi}        bytes allocated when the node starts
-//   c = {ufree_lo, ufree_hi, -, -}                  bytes of tensors it is the only consumer of
-//   meta bits: 0-3 kind, 4 never-ready (waits on a missing node), 8-19 in-degree
-//   meta bits: 0-3 kind, 4 never-ready, 5 static host, 6-15 in-degree from
-//   non-static nodes, 16-25 in-degree
+//   meta bits: 0-3 kind, 4 never-ready (waits on a missing node), 5 static host,
+//   6-15 in-degree from non-static nodes, 16-25 in-degree
 __device__ __forceinline__ int rec_kind(const uint4 &b) { return (int)(b.x & 15u); }
 __device__ __forceinline__ bool rec_never(const uint4 &b) { return (b.x >> 4) & 1u; }
 __device__ __forceinline__ bool rec_static(const uint4 &b) { return (b.x >> 5) & 1u; }
 __device__ __forceinline__ uint64_t rec_indeg(const uint4 &b, bool fold) { return (b.x >> (fold ? 6 : 16)) & 0x3ffu; }
 __device__ __forceinline__ int64_t rec_u64(uint32_t lo, uint32_t hi) { return (int64_t)(((uint64_t)hi << 32) | lo); }
-__device__ __forceinline__ uint4 rec_a(const DevGraph &g, int gn) { return g.node_rec[3 * gn]; }
-__device__ __forceinline__ uint4 rec_b(const DevGraph &g, int gn) { return g.node_rec[3 * gn + 1]; }
-__device__ __forceinline__ uint4 rec_c(const DevGraph &g, int gn) { return g.node_rec[3 * gn + 2]; }
+__device__ __forceinline__ uint4 rec_a(const DevGraph &g, int gn) { return g.node_rec[2 * gn]; }
+__device__ __forceinline__ uint4 rec_b(const DevGraph &g, int gn) { return g.node_rec[2 * gn + 1]; }
 
 // Per-(node, rank) accumulator word, one int64 in global memory ([node][rank]):
 //   bits 58-63  epoch of the design point that wrote it (stale words read as empty)
@@ -295,9 +298,9 @@ enum {
     F_COMP, F_OVL, F_COMP_A,                        // compute busy, compute-under-comm, commcum at compute start
     F_ALLOC, F_FREE, F_CUR, F_PEAK,                 // bytes allocated / freed at this step; memory in use, peak
     F_RH_CP, F_HOST_E, F_HOST_CP,                   // host stream (its slot is free at t iff host_n < 0)
-    F_DUE_SUM, F_RC_SUM, F_RH_SUM,                  // non-empty-word summaries of the sets' bitmaps
     F_N64
 };
+enum { F_DUE_SUM = -1, F_RC_SUM = -1, F_RH_SUM = -1 };   // (sets keep no summaries: see MinSet)
 #ifndef FL_NSM
 #define FL_NSM F_N64
 #endif
@@ -305,7 +308,6 @@ constexpr int F_NSM = FL_NSM;
 constexpr int FL_SR = 1024;                         // plane stride (lanes)
 enum { Q_RING_TAIL = 0, Q_RING_HEAD, Q_RING_SEEN, Q_HEAD_NODE, Q_HEAD_INST, Q_DONE, Q_N32 };
 
-extern __shared__ __align__(16) unsigned char fl_smem[];
 constexpr unsigned SM_HDR = (sizeof(Shared) + 15) / 16 * 16;
 __device__ __forceinline__ int64_t &F64(int k, int lr) {
     if (k < F_NSM) return reinterpret_cast<int64_t *>(fl_smem + SM_HDR)[k * FL_SR + lr];
@@ -371,10 +373,10 @@ template <int K> __device__ __forceinline__ uint64_t &touch_ref(const Ctx &c, co
 }
 
 // A node set with its minimum cached in a register and the rest in a global
-// bitmap ([word][rank]) with a summary of its non-empty words in shared field FS.
-// head < 0: empty; else bits 0-15 = the minimum, bit 16 = the bitmap is non-empty
-// (invariant: the minimum < every bitmap member).  The due / ready sets rarely hold
-// more than one node, so most inserts and pops are register operations.
+// bitmap ([word][rank]).  head < 0: empty; else bits 0-15 = the minimum, bit 16 =
+// the bitmap may be non-empty (invariant: the minimum < every bitmap member).  The
+// due / ready sets rarely hold more than one node, so most inserts and pops are
+// register operations; a pop after an overflow scans the words above the minimum.
 struct MinSet {
     int head;
 };
@@ -403,24 +405,21 @@ struct Step {                       // block-uniform per-step context
     int touch;                      // first-dependency bitmap in shared memory (else epoch tags)
 };
 
-__device__ __forceinline__ void bm_set(uint64_t *b, int R, int r, int64_t &sum, int idx) {
-    const int w = idx >> 6;
-    b[w * R + r] |= 1ull << (idx & 63);
-    sum |= 1ll << w;
+__device__ __forceinline__ void bm_set(uint64_t *b, int R, int r, int idx) {
+    b[(idx >> 6) * R + r] |= 1ull << (idx & 63);
 }
 
-// pops the smallest member; returns it, and whether the bitmap is still non-empty
-__device__ __forceinline__ int bm_pop(uint64_t *b, int R, int r, int64_t &sum, bool &more) {
-    int64_t sm = sum;
-    const int w = __ffsll((long long)sm) - 1;
-    uint64_t *p = b + (w * R + r);
-    uint64_t word = *p;
-    const int bit = __ffsll((long long)word) - 1;
-    word &= word - 1;
-    *p = word;
-    if (!word) { sm &= sm - 1; sum = sm; }
-    more = sm != 0;
-    return (w << 6) | bit;
+// pops the smallest member above `from`, or returns -1 when there is none
+__device__ __forceinline__ int bm_pop(uint64_t *b, int R, int r, int from, int nwords) {
+    for (int w = from >> 6; w < nwords; w++) {
+        uint64_t *p = b + (w * R + r);
+        const uint64_t word = *p;
+        if (word) {
+            *p = word & (word - 1);
+            return (w << 6) | (__ffsll((long long)word) - 1);
+        }
+    }
+    return -1;
 }
 
 // Sets carrying each member's critical-path finish: the minimum's in shared field F,
@@ -434,26 +433,29 @@ __device__ __forceinline__ void ms_insert_cp(MinSet &m, uint64_t *b, int64_t *cp
     } else if (idx < ms_min(m)) {
         const int h = ms_min(m);
         cp[h * R + L.r] = F64(F, L.lr);
-        bm_set(b, R, L.r, F64(FS, L.lr), h);
+        bm_set(b, R, L.r, h);
         m.head = idx | MS_MORE;
         F64(F, L.lr) = v;
     } else {
         cp[idx * R + L.r] = v;
-        bm_set(b, R, L.r, F64(FS, L.lr), idx);
+        bm_set(b, R, L.r, idx);
         m.head |= MS_MORE;
     }
 }
 
 template <int F, int FS>
 __device__ __forceinline__ int ms_pop_cp(MinSet &m, uint64_t *b, const int64_t *cp, int R, const Lane &L,
-                                         int64_t &v) {
+                                         int64_t &v, int nwords) {
     const int x = ms_min(m);
     v = F64(F, L.lr);
     if (m.head & MS_MORE) {
-        bool more;
-        const int h = bm_pop(b, R, L.r, F64(FS, L.lr), more);
-        m.head = h | (more ? MS_MORE : 0);
-        F64(F, L.lr) = cp[h * R + L.r] & (int64_t)VAL48;
+        const int h = bm_pop(b, R, L.r, x, nwords);
+        if (h >= 0) {
+            m.head = h | MS_MORE;
+            F64(F, L.lr) = cp[h * R + L.r] & (int64_t)VAL48;
+        } else {
+            m.head = -1;
+        }
     } else {
         m.head = -1;
     }
@@ -476,7 +478,7 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
     const int R = c.R;
     while (s.rh.head >= 0 && s.host_n < 0) {      // the host stream is free at t (gather_due ran at t)
         int64_t v;
-        const int h = ms_pop_cp<F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, v);
+        const int h = ms_pop_cp<F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, v, g.max_words);
         const int64_t e = t + c.dur[L.nb + h];
         { const uint4 hb = rec_b(g, L.nb + h); F64(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
         record(g, o, cfg, L.r, h, t, e);
@@ -501,7 +503,7 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
             if (sk > t) break;
         }
         int64_t v;
-        const int x = ms_pop_cp<F_RC_CP, F_RC_SUM>(s.rc, c.rdyc, c.cp, R, L, v);
+        const int x = ms_pop_cp<F_RC_CP, F_RC_SUM>(s.rc, c.rdyc, c.cp, R, L, v, g.max_words);
         const int64_t e = t + c.dur[L.nb + x];
         { const uint4 xb = rec_b(g, L.nb + x); F64(F_ALLOC, L.lr) += rec_u64(xb.z, xb.w); }
         record(g, o, cfg, L.r, x, t, e);
@@ -510,15 +512,6 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
             F64(F_COMP_A, L.lr) = s.commcum;
         }
 
-#ifdef FL_PREFETCH
-        if (e > t && !c.touch) {          // the successors' accumulator words are read when x completes
-            const uint4 xa = rec_a(g, L.nb + x);
-            for (uint32_t q = xa.x; q < xa.y; q++) {
-                const int64_t *w = c.cp + (g.succ_idx[q] * R + L.r);
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(w));
-            }
-        }
-#endif
 #pragma unroll
         for (int q = 0; q < (K & 7); q++) {
             if (q == k) {
@@ -590,7 +583,7 @@ template <int K>
 __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const Lane &L, Rank<K> &s,
                                           const Step &f, int x, int64_t fx64, int64_t t) {
     const int R = c.R;
-    const uint4 xa = rec_a(g, L.nb + x), xc = rec_c(g, L.nb + x);
+    const uint4 xa = rec_a(g, L.nb + x);
     if (g.needs_done) done_ref<K>(c, L, R, x >> 6) |= 1ull << (x & 63);
     F32(Q_DONE, L.lr)++;
     s.pop_seq++;
@@ -599,8 +592,8 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
         const int64_t cm = F64(F_CPMAX, L.lr);
         if (fx64 > cm) F64(F_CPMAX, L.lr) = fx64;
     }
-    int64_t freed = rec_u64(xc.x, xc.y);
-    for (uint32_t q = xa.z; q < xa.w; q++) {
+    int64_t freed = rec_u64(xa.z, xa.w);
+    if (xa.y >> 16) for (uint32_t q = (uint32_t)g.mfree_off[L.nb + x], qe = q + (xa.y >> 16); q < qe; q++) {
         const int tt = L.tb + g.free_tens[q];
         const int2 cr = g.tens_rng[tt];
         bool all = true;
@@ -611,10 +604,12 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
         if (all) freed += g.tens_bytes[tt];
     }
     if (freed) F64(F_FREE, L.lr) += freed;
+    PROF_MARK(9);                           // pop: records, statistics
     const uint64_t fx = (uint64_t)fx64;     // this node's critical-path finish
     int seq = 0;
-    for (uint32_t q = xa.x; q < xa.y; q++, seq++) {
-        const uint32_t ent = (uint32_t)g.succ_ent[q];
+    const int32_t *sl = g.succ_ent;
+    for (uint32_t q = xa.x, qe = xa.x + (xa.y & 0xffffu); q < qe; q++, seq++) {
+        const uint32_t ent = (uint32_t)sl[q];
         const int d = (int)(ent & 0xffffu);
         const int cls = f.fold ? (int)(ent >> 16) : FL_EDGE_COUNTED;
         int64_t *slot = c.cp + (d * R + L.r);
@@ -635,8 +630,10 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
             continue;
         }
         if (cls == FL_EDGE_LAST) {
+            PROF_MARK(10);                  // edges before a "last" one
             const uint64_t a = (uint64_t)__ldcg(slot) & VAL48;    // the first/middle ones' max (at L2)
             dispatch(g, c, L, s, f, d, db, (int64_t)(a > fx ? a : fx), seq, t);
+            PROF_MARK(11);                  // "last" edge: accumulator read + dispatch
             continue;
         }
         // first dependency to complete: the word holds nothing of this design point,
@@ -1280,7 +1277,7 @@ __global__ void __launch_bounds__(1024, 1)
         // ---- event loop ----
         const int64_t TCAP = (int64_t)1 << 48;   // 48-bit accumulators; keys pack (t, rank)
 #ifdef FL_PROFILE
-        long long prof_t = clock64();
+        if (blockIdx.x == 0 && threadIdx.x == 0) fl_prof_t = clock64();
 #endif
         for (;;) {
             PROF_MARK(0);                                   // loop back-edge
@@ -1320,7 +1317,7 @@ __global__ void __launch_bounds__(1024, 1)
                     s.pop_seq = 0;
                     while (s.due.head >= 0) {
                         int64_t fx;
-                        const int x = ms_pop_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, fx);
+                        const int x = ms_pop_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, fx, g.max_words);
                         pop_event(g, c, L, s, f, x, fx, t);
                         PROF_MARK(7);                       // pop_event
                         start_phase(g, o, c, L, s, f, t, cfg);
@@ -1339,7 +1336,7 @@ __global__ void __launch_bounds__(1024, 1)
                     if (active && (int)(m2 >> 13) == L.r) {
                         s.pop_seq = 0;
                         int64_t fx;
-                        const int x = ms_pop_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, fx);
+                        const int x = ms_pop_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, fx, g.max_words);
                         pop_event(g, c, L, s, f, x, fx, t);
                     }
                     if (active) start_phase(g, o, c, L, s, f, t, cfg);
@@ -1357,7 +1354,7 @@ __global__ void __launch_bounds__(1024, 1)
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&fl_prof[15], 1ull);
         if (blockIdx.x == 0 && threadIdx.x == 0 && cfg + ncl >= p.n) {
             printf("FLPROF points %llu", fl_prof[15]);
-            for (int k = 0; k < 9; k++) printf(" s%d %llu", k, fl_prof[k]);
+            for (int k = 0; k < 12; k++) printf(" s%d %llu", k, fl_prof[k]);
             printf("\n");
         }
 #endif
@@ -1431,7 +1428,7 @@ __global__ void cp_kernel(const __grid_constant__ DevGraph g, const __grid_const
             }
             int64_t d = g.node_dur[gn];
             if (p.peak_flops && g.node_flops[gn] >= 0) d = flops_to_ns(g.node_flops[gn], p.peak_flops[cfg], p.efficiency[cfg]);
-            if ((g.node_rec[3 * gn + 1].x & 15u) <= FL_COMP) x += d;   // `duration_ns or 0`
+            if ((g.node_rec[2 * gn + 1].x & 15u) <= FL_COMP) x += d;   // `duration_ns or 0`
         }
         cv[v] = x;
         best = x > best ? x : best;

@@ -9,7 +9,7 @@ enum { FL_EDGE_COUNTED = 0, FL_EDGE_SINGLE = 1, FL_EDGE_FIRST = 2, FL_EDGE_MID =
 
 // Device copy of fl_graph_desc (pointers are device pointers).
 struct DevGraph {
-    int R, S, n_inst, coll_stride, max_nodes, max_words, total_nodes, total_tens;
+    int R, S, n_inst, coll_stride, max_nodes, max_words, total_nodes, total_tens, n_succ;
     const int32_t *rank_struct;
     const int32_t *s_node_off, *s_tens_off, *s_init_off, *s_ncoll;
     const int64_t *s_init_alloc;
@@ -24,7 +24,8 @@ struct DevGraph {
     const int32_t *inst_mem_rank, *inst_mem_node, *rank_coll_inst;
     const int32_t *inst_full_node;   // >= 0 when members are ranks 0..R-1 in order, all at this local node
     // derived on upload (capi.cu): packed per-node records and tensor consumer ranges
-    const uint4 *node_rec;       // [2 * total_nodes]
+    const uint4 *node_rec;       // [2 * total_nodes] (engine.cu "Node record")
+    const int32_t *mfree_off;    // [total_nodes] first entry in free_tens of a node's shared-tensor frees
     const int2 *tens_rng;        // [total_tens] {first, end} into tens_cons
     // static-host folding (engine.cu "t = 0 host pops")
     int fold_ok;

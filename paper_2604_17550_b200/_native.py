@@ -26,8 +26,11 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-fmad=false",                 # no FMA contraction: bit-exact fp64 cost model
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
 ]
+# engine.cu is compiled once per kernel-variant group (compute streams | 8 with messages,
+# engine.cu FL_BASE) so the groups build in parallel
+ENGINE_PARTS = (1, 2, 4, 9, 10, 12)
 
 
 def nvcc() -> str:
@@ -37,16 +40,39 @@ def nvcc() -> str:
     return "nvcc"
 
 
+def _compile(out: Path, defines=(), verbose: bool = False) -> str:
+    """nvcc every translation unit to an object (in parallel), then link `out`."""
+    tmp = out.parent / (out.name + ".objs")
+    tmp.mkdir(parents=True, exist_ok=True)
+    inc = ["-I", str(ROOT / "include"), "-I", str(PKG / "csrc")]
+    dflags = [f"-D{d}" for d in defines]
+    jobs = [(PKG / "csrc" / "engine.cu", tmp / f"engine_{b}.o", [f"-DFL_BASE={b}"]) for b in ENGINE_PARTS]
+    jobs.append((PKG / "csrc" / "capi.cu", tmp / "capi.o", []))
+    procs = []
+    for src, obj, extra in jobs:
+        cmd = [nvcc(), *NVCC_FLAGS, *dflags, *extra, *inc, "-c", str(src), "-o", str(obj)]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+    err = ""
+    failed = False
+    for p in procs:
+        _, e = p.communicate()
+        err += e
+        failed |= p.returncode != 0
+    if failed:
+        raise EngineError("nvcc failed:\n" + err[-4000:])
+    link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *[str(o) for _, o, _ in jobs],
+            "-o", str(out)]
+    res = subprocess.run(link, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise EngineError("nvcc link failed:\n" + res.stderr[-4000:])
+    return err
+
+
 def build_variant(out: Path, defines=(), verbose: bool = False) -> str:
     """Compile the engine with extra -D flags into `out` (A/B experiments)."""
-    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(ROOT / "include"), "-I", str(PKG / "csrc"),
-           *map(str, SOURCES), "-o", str(out)]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise EngineError("nvcc failed:\n" + res.stderr[-4000:])
-    return res.stderr
+    return _compile(out, defines, verbose)
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
@@ -54,13 +80,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     newest = max(p.stat().st_mtime for p in SOURCES + HEADERS)
     if not force and LIB.exists() and LIB.stat().st_mtime >= newest:
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-I", str(PKG / "csrc"),
-           *map(str, SOURCES), "-o", str(LIB) + ".tmp"]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise EngineError("nvcc failed:\n" + res.stderr[-4000:])
+    _compile(Path(str(LIB) + ".tmp"), verbose=verbose)
     os.replace(str(LIB) + ".tmp", LIB)
     return LIB
 

@@ -377,14 +377,14 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     off = align_up(off + (size_t)d->n_msg * 8 * 8 + (size_t)sc.link_cap * 16 + (size_t)d->n_msg * 8 +
                        (size_t)R * 4 + 2 * (size_t)dg.p2p_stride * R * 4 + 64, 256);
     sc.off_ctr = off;  off = align_up(off + 64, 256);
-    sc.off_prf = off;  off = align_up(off + fl::sweep_global_bytes_per_rank() * (size_t)fl::sweep_plane_lanes() * CS, 256);
+    sc.off_prf = off;  off = align_up(off + fl::sweep_global_bytes_per_rank() * (size_t)fl::sweep_plane_lanes(g->block, CS) * CS, 256);
     sc.slot_bytes = off;
 
     // shared memory: header | comm_end, stats, ring tails | [instances] | [durations] | [done bitmap]
     size_t sm = fl::sweep_shared_header_bytes();
     sc.sm_off_dyn = (unsigned)sm;
     const size_t B = (size_t)g->block;              // shared per-rank arrays have blockDim stride
-    sm = align_up(sm + (size_t)fl::sweep_plane_lanes() * fl::sweep_shared_bytes_per_rank(), 16);   // per-rank fields (engine.cu F_*, Q_*)
+    sm = align_up(sm + (size_t)fl::sweep_plane_lanes(g->block, CS) * fl::sweep_shared_bytes_per_rank(), 16);   // per-rank fields (engine.cu F_*, Q_*)
     const size_t budget = (size_t)optin - 1024;   // the kernel's static shared memory (Ctx) comes off the top
     const size_t sbits = (size_t)dg.max_words * B * 8;   // a bitmap over this CTA's ranks
     sc.inst_in_smem = CS == 1 && sm + inst_bytes <= budget;   // clusters share instance state in HBM

@@ -73,7 +73,7 @@ __device__ __forceinline__ double ring_ar(int64_t n, double s, double a, double 
 }
 
 // collectives.py:251-293.  Returns -1 for UnsupportedAlgoTopologyError.
-__device__ int64_t analytical_time(int kind, int64_t size, int64_t n, int algo, double a,
+static __device__ int64_t analytical_time(int kind, int64_t size, int64_t n, int algo, double a,
                                    double b, int64_t rows, int64_t cols) {
     if (n <= 1) return 0;
     double s = (double)size, t;
@@ -111,6 +111,12 @@ __device__ __forceinline__ int64_t coll_time(const DevGraph &g, int i, int algo,
                            mesh ? rows : 0, mesh ? cols : 0);
 }
 
+#ifndef FL_BASE
+#define FL_BASE 0       // 0: this translation unit instantiates every kernel variant
+#endif
+#define FL_COMMON (FL_BASE == 0 || FL_BASE == 1)   // non-template kernels and the dispatchers
+
+#if FL_COMMON
 __global__ void cost_only_kernel(int n, const uint8_t *kind, const int64_t *size, const int64_t *gn,
                                  const uint8_t *algo, const double *alpha, const double *beta,
                                  const int32_t *rows, const int32_t *cols, int64_t *out,
@@ -124,6 +130,7 @@ __global__ void cost_only_kernel(int n, const uint8_t *kind, const int64_t *size
     }
     if (i < m) out_comp[i] = flops_to_ns(flops[i], peak[i], eff[i]);
 }
+#endif
 
 // ------------------------------------------------------- block primitives
 
@@ -236,8 +243,8 @@ __device__ __forceinline__ int gor(int v, Shared &sh, int &par) {
 // ---------------------------------------------------------- rank state
 
 #ifdef FL_PROFILE     // development only: per-segment cycle counts of warp 0 of CTA 0
-__device__ unsigned long long fl_prof[16];
-__shared__ long long fl_prof_t;
+static __device__ unsigned long long fl_prof[16];
+static __shared__ long long fl_prof_t;
 #define PROF_MARK(k)                                                                      \
     do {                                                                                  \
         if (blockIdx.x == 0 && threadIdx.x == 0) {                                        \
@@ -305,16 +312,24 @@ enum { F_DUE_SUM = -1, F_RC_SUM = -1, F_RH_SUM = -1 };   // (sets keep no summar
 #define FL_NSM F_N64
 #endif
 constexpr int F_NSM = FL_NSM;
-constexpr int FL_SR = 1024;                         // plane stride (lanes)
+// Plane stride (lanes), a compile-time constant per kernel variant: bits 5-6 of the
+// variant word K select 1024 (0), 256 (1) or 64 (2), the smallest that holds the block,
+// so small design points keep many CTAs per SM.
+template <int K> __host__ __device__ constexpr int plane_lanes() { return ((K >> 5) & 3) == 0 ? 1024 : ((K >> 5) & 3) == 1 ? 256 : 64; }
+constexpr int FL_SR = 1024;                         // widest plane (HBM fallback fields, capacity)
 enum { Q_RING_TAIL = 0, Q_RING_HEAD, Q_RING_SEEN, Q_HEAD_NODE, Q_HEAD_INST, Q_DONE, Q_N32 };
 
 constexpr unsigned SM_HDR = (sizeof(Shared) + 15) / 16 * 16;
+template <int K>
 __device__ __forceinline__ int64_t &F64(int k, int lr) {
-    if (k < F_NSM) return reinterpret_cast<int64_t *>(fl_smem + SM_HDR)[k * FL_SR + lr];
-    return reinterpret_cast<Shared *>(fl_smem)->prg[(k - F_NSM) * FL_SR + lr];
+    constexpr int SR = plane_lanes<K>();
+    if (k < F_NSM) return reinterpret_cast<int64_t *>(fl_smem + SM_HDR)[k * SR + lr];
+    return reinterpret_cast<Shared *>(fl_smem)->prg[(k - F_NSM) * SR + lr];
 }
+template <int K>
 __device__ __forceinline__ int32_t &F32(int k, int lr) {
-    return reinterpret_cast<int32_t *>(fl_smem + SM_HDR + (size_t)F_NSM * 8 * FL_SR)[k * FL_SR + lr];
+    constexpr int SR = plane_lanes<K>();
+    return reinterpret_cast<int32_t *>(fl_smem + SM_HDR + (size_t)F_NSM * 8 * SR)[k * SR + lr];
 }
 
 // Per-CTA (block-uniform) state pointers.  Bitmaps are word-major,
@@ -424,18 +439,18 @@ __device__ __forceinline__ int bm_pop(uint64_t *b, int R, int r, int from, int n
 
 // Sets carrying each member's critical-path finish: the minimum's in shared field F,
 // bitmap members' in their accumulator word cp[node][rank].
-template <int F, int FS>
+template <int K, int F, int FS>
 __device__ __forceinline__ void ms_insert_cp(MinSet &m, uint64_t *b, int64_t *cp, int R, const Lane &L, int idx,
                                              int64_t v) {
     if (m.head < 0) {
         m.head = idx;
-        F64(F, L.lr) = v;
+        F64<K>(F, L.lr) = v;
     } else if (idx < ms_min(m)) {
         const int h = ms_min(m);
-        cp[h * R + L.r] = F64(F, L.lr);
+        cp[h * R + L.r] = F64<K>(F, L.lr);
         bm_set(b, R, L.r, h);
         m.head = idx | MS_MORE;
-        F64(F, L.lr) = v;
+        F64<K>(F, L.lr) = v;
     } else {
         cp[idx * R + L.r] = v;
         bm_set(b, R, L.r, idx);
@@ -443,16 +458,16 @@ __device__ __forceinline__ void ms_insert_cp(MinSet &m, uint64_t *b, int64_t *cp
     }
 }
 
-template <int F, int FS>
+template <int K, int F, int FS>
 __device__ __forceinline__ int ms_pop_cp(MinSet &m, uint64_t *b, const int64_t *cp, int R, const Lane &L,
                                          int64_t &v, int nwords) {
     const int x = ms_min(m);
-    v = F64(F, L.lr);
+    v = F64<K>(F, L.lr);
     if (m.head & MS_MORE) {
         const int h = bm_pop(b, R, L.r, x, nwords);
         if (h >= 0) {
             m.head = h | MS_MORE;
-            F64(F, L.lr) = cp[h * R + L.r] & (int64_t)VAL48;
+            F64<K>(F, L.lr) = cp[h * R + L.r] & (int64_t)VAL48;
         } else {
             m.head = -1;
         }
@@ -478,15 +493,15 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
     const int R = c.R;
     while (s.rh.head >= 0 && s.host_n < 0) {      // the host stream is free at t (gather_due ran at t)
         int64_t v;
-        const int h = ms_pop_cp<F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, v, g.max_words);
+        const int h = ms_pop_cp<K, F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, v, g.max_words);
         const int64_t e = t + c.dur[L.nb + h];
-        { const uint4 hb = rec_b(g, L.nb + h); F64(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
+        { const uint4 hb = rec_b(g, L.nb + h); F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
         record(g, o, cfg, L.r, h, t, e);
         if (e == t) {
-            ms_insert_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, h, v);
+            ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, h, v);
         } else {
-            F64(F_HOST_E, L.lr) = e;
-            F64(F_HOST_CP, L.lr) = v;
+            F64<K>(F_HOST_E, L.lr) = e;
+            F64<K>(F_HOST_CP, L.lr) = v;
             s.host_n = h;
         }
     }
@@ -503,13 +518,13 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
             if (sk > t) break;
         }
         int64_t v;
-        const int x = ms_pop_cp<F_RC_CP, F_RC_SUM>(s.rc, c.rdyc, c.cp, R, L, v, g.max_words);
+        const int x = ms_pop_cp<K, F_RC_CP, F_RC_SUM>(s.rc, c.rdyc, c.cp, R, L, v, g.max_words);
         const int64_t e = t + c.dur[L.nb + x];
-        { const uint4 xb = rec_b(g, L.nb + x); F64(F_ALLOC, L.lr) += rec_u64(xb.z, xb.w); }
+        { const uint4 xb = rec_b(g, L.nb + x); F64<K>(F_ALLOC, L.lr) += rec_u64(xb.z, xb.w); }
         record(g, o, cfg, L.r, x, t, e);
         if ((K & 7) == 1 && e > t) {      // one compute stream: its busy intervals are disjoint
-            F64(F_COMP, L.lr) += e - t;
-            F64(F_COMP_A, L.lr) = s.commcum;
+            F64<K>(F_COMP, L.lr) += e - t;
+            F64<K>(F_COMP_A, L.lr) = s.commcum;
         }
 
 #pragma unroll
@@ -517,11 +532,11 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
             if (q == k) {
                 if constexpr ((K & 7) > 1) s.slot[q] = e;
                 if (e == t) {
-                    ms_insert_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, x, v);
+                    ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, x, v);
                 } else {
                     s.occ_e[q] = e;
                     s.occ_n[q] = x;
-                    if (q == 0) F64(F_OCC_CP, L.lr) = v;
+                    if (q == 0) F64<K>(F_OCC_CP, L.lr) = v;
                     else c.cp[x * R + L.r] = v;      // streams 1..3: the running node's own accumulator word
                 }
             }
@@ -573,8 +588,8 @@ __device__ __forceinline__ void dispatch(const DevGraph &g, const Ctx &c, const 
         return;
     }
     const int64_t fin = cps + c.dur[L.nb + d];
-    if (kind == FL_COMP) ms_insert_cp<F_RC_CP, F_RC_SUM>(s.rc, c.rdyc, c.cp, R, L, d, fin);
-    else ms_insert_cp<F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, d, fin);
+    if (kind == FL_COMP) ms_insert_cp<K, F_RC_CP, F_RC_SUM>(s.rc, c.rdyc, c.cp, R, L, d, fin);
+    else ms_insert_cp<K, F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, d, fin);
 }
 
 // Pop one completion event (simulator.py:335-340) and free tensors whose last
@@ -585,12 +600,12 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
     const int R = c.R;
     const uint4 xa = rec_a(g, L.nb + x);
     if (g.needs_done) done_ref<K>(c, L, R, x >> 6) |= 1ull << (x & 63);
-    F32(Q_DONE, L.lr)++;
+    F32<K>(Q_DONE, L.lr)++;
     s.pop_seq++;
-    F64(F_FIN, L.lr) = t;
+    F64<K>(F_FIN, L.lr) = t;
     {
-        const int64_t cm = F64(F_CPMAX, L.lr);
-        if (fx64 > cm) F64(F_CPMAX, L.lr) = fx64;
+        const int64_t cm = F64<K>(F_CPMAX, L.lr);
+        if (fx64 > cm) F64<K>(F_CPMAX, L.lr) = fx64;
     }
     int64_t freed = rec_u64(xa.z, xa.w);
     if (xa.y >> 16) for (uint32_t q = (uint32_t)g.mfree_off[L.nb + x], qe = q + (xa.y >> 16); q < qe; q++) {
@@ -603,7 +618,7 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
         }
         if (all) freed += g.tens_bytes[tt];
     }
-    if (freed) F64(F_FREE, L.lr) += freed;
+    if (freed) F64<K>(F_FREE, L.lr) += freed;
     PROF_MARK(9);                           // pop: records, statistics
     const uint64_t fx = (uint64_t)fx64;     // this node's critical-path finish
     int seq = 0;
@@ -663,11 +678,11 @@ constexpr int64_t HS_ALLOC = INT64_MIN;   // head_s once the head's outputs are 
 
 template <int K>
 __device__ __forceinline__ void load_head(const Ctx &c, const Lane &L, Rank<K> &s) {
-    const int h = F32(Q_RING_HEAD, L.lr);
-    if (h < F32(Q_RING_SEEN, L.lr)) {
+    const int h = F32<K>(Q_RING_HEAD, L.lr);
+    if (h < F32<K>(Q_RING_SEEN, L.lr)) {
         const int i = c.ring_inst[h * c.R + L.r];
-        F32(Q_HEAD_NODE, L.lr) = c.ring_node[h * c.R + L.r];
-        F32(Q_HEAD_INST, L.lr) = i;
+        F32<K>(Q_HEAD_NODE, L.lr) = c.ring_node[h * c.R + L.r];
+        F32<K>(Q_HEAD_INST, L.lr) = i;
         s.head_s = c.inst_s[i];
         s.head_e = c.inst_e[i];
     } else {
@@ -678,10 +693,10 @@ __device__ __forceinline__ void load_head(const Ctx &c, const Lane &L, Rank<K> &
 // After reservations: pick up comm-FIFO entries appended for this rank.
 template <int K>
 __device__ __forceinline__ void refresh_ring(const Ctx &c, const Lane &L, Rank<K> &s) {
-    const int tail = F32(Q_RING_TAIL, L.lr);
-    const int seen = F32(Q_RING_SEEN, L.lr);
+    const int tail = F32<K>(Q_RING_TAIL, L.lr);
+    const int seen = F32<K>(Q_RING_SEEN, L.lr);
     if (tail != seen) {
-        F32(Q_RING_SEEN, L.lr) = tail;
+        F32<K>(Q_RING_SEEN, L.lr) = tail;
         if (s.head_e == TINF) load_head(c, L, s);
     }
 }
@@ -690,7 +705,7 @@ template <int K>
 __device__ __forceinline__ int64_t next_time(const DevGraph &g, const Ctx &c, const Lane &L, const Rank<K> &s,
                                              int64_t tcur) {
     if (s.due.head >= 0) return tcur;
-    int64_t nt = s.host_n >= 0 ? F64(F_HOST_E, L.lr) : TINF;
+    int64_t nt = s.host_n >= 0 ? F64<K>(F_HOST_E, L.lr) : TINF;
 #pragma unroll
     for (int q = 0; q < (K & 7); q++) if (s.occ_n[q] >= 0 && s.occ_e[q] < nt) nt = s.occ_e[q];
     if (s.head_e < nt) nt = s.head_e;
@@ -706,25 +721,25 @@ template <int K>
 __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, const Lane &L, Rank<K> &s,
                                            int64_t t) {
     const int R = c.R;
-    if (s.host_n >= 0 && F64(F_HOST_E, L.lr) == t) {
-        ms_insert_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, s.host_n, F64(F_HOST_CP, L.lr));
+    if (s.host_n >= 0 && F64<K>(F_HOST_E, L.lr) == t) {
+        ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, s.host_n, F64<K>(F_HOST_CP, L.lr));
         s.host_n = -1;
     }
 #pragma unroll
     for (int q = 0; q < (K & 7); q++)
         if (s.occ_n[q] >= 0 && s.occ_e[q] == t) {
-            const int64_t v = q == 0 ? F64(F_OCC_CP, L.lr) : c.cp[s.occ_n[q] * R + L.r];
-            ms_insert_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, s.occ_n[q], v);
+            const int64_t v = q == 0 ? F64<K>(F_OCC_CP, L.lr) : c.cp[s.occ_n[q] * R + L.r];
+            ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, s.occ_n[q], v);
             s.occ_n[q] = -1;
-            if ((K & 7) == 1) F64(F_OVL, L.lr) += s.commcum - F64(F_COMP_A, L.lr);   // comm time under [start, t)
+            if ((K & 7) == 1) F64<K>(F_OVL, L.lr) += s.commcum - F64<K>(F_COMP_A, L.lr);   // comm time under [start, t)
         }
     while (s.head_e == t) {
-        const int hn = F32(Q_HEAD_NODE, L.lr), hi = F32(Q_HEAD_INST, L.lr);
-        if (s.head_s != HS_ALLOC) { const uint4 hb = rec_b(g, L.nb + hn); F64(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }  // zero-length: starts now
+        const int hn = F32<K>(Q_HEAD_NODE, L.lr), hi = F32<K>(Q_HEAD_INST, L.lr);
+        if (s.head_s != HS_ALLOC) { const uint4 hb = rec_b(g, L.nb + hn); F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }  // zero-length: starts now
         // every member of an instance finishes at max over members' critical-path starts + duration
         // (simulator.py:419-428)
-        ms_insert_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, hn, c.inst_cpmax[hi] + c.inst_dur[hi]);
-        F32(Q_RING_HEAD, L.lr)++;
+        ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, hn, c.inst_cpmax[hi] + c.inst_dur[hi]);
+        F32<K>(Q_RING_HEAD, L.lr)++;
         load_head(c, L, s);
     }
     if (K & 8) {
@@ -733,8 +748,8 @@ __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, cons
             const int ent = c.mlist[k * R + L.r];
             if (c.msg_e[ent & ~MSG_ALLOC] != t) break;
             const int node = c.mlist_node[k * R + L.r];
-            if (!(ent & MSG_ALLOC)) { const uint4 hb = rec_b(g, L.nb + node); F64(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
-            ms_insert_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, node, c.cp[node * R + L.r] & (int64_t)VAL48);
+            if (!(ent & MSG_ALLOC)) { const uint4 hb = rec_b(g, L.nb + node); F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
+            ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, node, c.cp[node * R + L.r] & (int64_t)VAL48);
         }
         if (k) {
             for (int q = k; q < n; q++) {
@@ -754,8 +769,8 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
     const int R = c.R;
     const bool head = s.head_e != TINF;
     if (head && s.head_s != HS_ALLOC && s.head_s <= tcur) {   // a collective that started by tcur
-        const uint4 hb = rec_b(g, L.nb + F32(Q_HEAD_NODE, L.lr));
-        F64(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w);
+        const uint4 hb = rec_b(g, L.nb + F32<K>(Q_HEAD_NODE, L.lr));
+        F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w);
         s.head_s = HS_ALLOC;
     }
     bool msg_on = false;            // a message of this rank is on the wire during [tcur, tnew)
@@ -767,20 +782,20 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
                 msg_on = true;
                 if (!(ent & MSG_ALLOC)) {
                     const uint4 hb = rec_b(g, L.nb + c.mlist_node[k * R + L.r]);
-                    F64(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w);
+                    F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w);
                     c.mlist[k * R + L.r] = ent | MSG_ALLOC;
                 }
             }
         }
     }
     {
-        const int64_t at = F64(F_ALLOC, L.lr), ft = F64(F_FREE, L.lr);
+        const int64_t at = F64<K>(F_ALLOC, L.lr), ft = F64<K>(F_FREE, L.lr);
         if (at | ft) {
-            const int64_t cur = F64(F_CUR, L.lr) + at;
-            if (cur > F64(F_PEAK, L.lr)) F64(F_PEAK, L.lr) = cur;
-            F64(F_CUR, L.lr) = cur - ft;
-            F64(F_ALLOC, L.lr) = 0;
-            F64(F_FREE, L.lr) = 0;
+            const int64_t cur = F64<K>(F_CUR, L.lr) + at;
+            if (cur > F64<K>(F_PEAK, L.lr)) F64<K>(F_PEAK, L.lr) = cur;
+            F64<K>(F_CUR, L.lr) = cur - ft;
+            F64<K>(F_ALLOC, L.lr) = 0;
+            F64<K>(F_FREE, L.lr) = 0;
         }
     }
     if (tnew == TINF) return;
@@ -792,8 +807,8 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
 #pragma unroll
         for (int q = 0; q < (K & 7); q++) comp_on |= s.occ_n[q] >= 0;
         if (comp_on) {
-            F64(F_COMP, L.lr) += dt;
-            if (comm_on) F64(F_OVL, L.lr) += dt;
+            F64<K>(F_COMP, L.lr) += dt;
+            if (comm_on) F64<K>(F_OVL, L.lr) += dt;
         }
     }
 }
@@ -851,7 +866,7 @@ __device__ __forceinline__ int64_t transfer_ns(const DevGraph &g, int topo, int 
 
 // Message phase (simulator.py:310-327), one thread: FIFO per link, a message holds
 // every link on its route for the whole transfer.
-__device__ void reserve_msgs(const DevGraph &g, const DevOut &o, const Ctx &c, int nm, bool init, int topo,
+static __device__ void reserve_msgs(const DevGraph &g, const DevOut &o, const Ctx &c, int nm, bool init, int topo,
                              int cols, int cfg, uint64_t epoch, int64_t &cpm) {
     const int R = c.R;
     for (int a = 1; a < nm; a++) {
@@ -902,7 +917,7 @@ __device__ void reserve_msgs(const DevGraph &g, const DevOut &o, const Ctx &c, i
 // reference's order (simulator.py:298-309), block- (or cluster-) wide; then the
 // step's messages (simulator.py:310-327).  Returns the largest critical-path
 // finish among them.
-template <bool MSG, bool CL>
+template <bool MSG, bool CL, int K>
 __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, const Ctx &c, Shared &sh, int &par,
                                           int64_t t, bool init, int cfg, uint64_t epoch,
                                           int nc, int nmc, int topo, int cols) {
@@ -936,7 +951,7 @@ __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, co
             for (int64_t j = threadIdx.x; j < nm; j += blockDim.x) {
                 const int lm = g.inst_mem_rank[m0 + j] - base;
                 if (lm < 0 || lm >= RL) continue;       // another CTA's rank
-                const int64_t ce = F64(F_COMM_END, lm);
+                const int64_t ce = F64<K>(F_COMM_END, lm);
                 local = ce > local ? ce : local;
             }
             s = gmax_i64<CL>(local, sh, par);
@@ -948,8 +963,8 @@ __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, co
         if (full_node >= 0) {
             for (int lm = threadIdx.x; lm < RL; lm += blockDim.x) {
                 const int m = base + lm;
-                F64(F_COMM_END, lm) = e;
-                const int slot = F32(Q_RING_TAIL, lm)++;
+                F64<K>(F_COMM_END, lm) = e;
+                const int slot = F32<K>(Q_RING_TAIL, lm)++;
                 c.ring_inst[slot * R + m] = i;
                 c.ring_node[slot * R + m] = full_node;
                 record(g, o, cfg, m, full_node, s, e);
@@ -961,8 +976,8 @@ __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, co
                 const int m = g.inst_mem_rank[m0 + j], node = g.inst_mem_node[m0 + j];
                 const int lm = m - base;
                 if (lm < 0 || lm >= RL) continue;
-                F64(F_COMM_END, lm) = e;
-                const int slot = F32(Q_RING_TAIL, lm)++;
+                F64<K>(F_COMM_END, lm) = e;
+                const int slot = F32<K>(Q_RING_TAIL, lm)++;
                 c.ring_inst[slot * R + m] = i;
                 c.ring_node[slot * R + m] = node;
                 record(g, o, cfg, m, node, s, e);
@@ -988,13 +1003,13 @@ __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, co
 }
 
 // Barrier, then reserve whatever completed since the last reservation.
-template <bool MSG, bool CL>
+template <bool MSG, bool CL, int K>
 __device__ __forceinline__ int64_t reserve(const DevGraph &g, const DevOut &o, const Ctx &c, Shared &sh, int &par,
                                            int64_t t, bool init, int cfg, uint64_t epoch,
                                            int topo, int cols) {
     gsync<CL>();
     const int nc = CL ? *c.ncomp : sh.ncomp, nmc = MSG ? (CL ? *c.nmcomp : sh.nmcomp) : 0;
-    return (nc | nmc) ? reserve_n<MSG, CL>(g, o, c, sh, par, t, init, cfg, epoch, nc, nmc, topo, cols) : 0;
+    return (nc | nmc) ? reserve_n<MSG, CL, K>(g, o, c, sh, par, t, init, cfg, epoch, nc, nmc, topo, cols) : 0;
 }
 
 // Zero this CTA's ranks' columns of a [rows][R] array (clusters split a point's ranks).
@@ -1062,7 +1077,7 @@ __global__ void __launch_bounds__(1024, 1)
         c.nmcomp = CL ? ctr + 1 : &sh.nmcomp;
         c.lead_cta = crank == 0;
         c.touch = sc.touch_in_smem;
-        sh.prg = reinterpret_cast<int64_t *>(base + sc.off_prf) + (size_t)crank * (F_N64 - F_NSM) * FL_SR;
+        sh.prg = reinterpret_cast<int64_t *>(base + sc.off_prf) + (size_t)crank * (F_N64 - F_NSM) * plane_lanes<K>();
         const int M = g.n_msg;
         int64_t *mb = reinterpret_cast<int64_t *>(base + sc.off_msg);
         c.msg_sendt = mb;
@@ -1171,9 +1186,9 @@ __global__ void __launch_bounds__(1024, 1)
         if (sc.touch_in_smem) for (size_t i = tid; i < (size_t)g.max_words * bd; i += bd) c.touched[i] = 0;
         if (tid == 0) { sh.cend_all = 0; sh.cend_uniform = 1; }
 #pragma unroll
-        for (int k = 0; k < F_N64; k++) F64(k, tid) = 0;
+        for (int k = 0; k < F_N64; k++) F64<K>(k, tid) = 0;
 #pragma unroll
-        for (int k = 0; k < Q_N32; k++) F32(k, tid) = 0;
+        for (int k = 0; k < Q_N32; k++) F32<K>(k, tid) = 0;
         bad = gor<CL>(bad, sh, par);
         cap_bad = gor<CL>(cap_bad, sh, par);
         if (cap_bad) bad = 2;
@@ -1211,7 +1226,7 @@ __global__ void __launch_bounds__(1024, 1)
         }
         s.head_s = 0;
         s.head_e = TINF;
-        F64(F_ALLOC, tid) = active ? g.s_init_alloc[g.rank_struct[L.r]] : 0;
+        F64<K>(F_ALLOC, tid) = active ? g.s_init_alloc[g.rank_struct[L.r]] : 0;
         s.commcum = 0;
         s.pop_seq = 0;
         constexpr bool MSG = (K & 8) != 0;
@@ -1236,7 +1251,7 @@ __global__ void __launch_bounds__(1024, 1)
         }
         // (reservations also return their instances' critical-path finishes; every member's
         // pop folds the same value into F_CPMAX, so the row needs only that)
-        reserve<MSG, CL>(g, o, c, sh, par, 0, true, cfg, f.epoch, topo, p.cols[cfg]);
+        reserve<MSG, CL, KK>(g, o, c, sh, par, 0, true, cfg, f.epoch, topo, p.cols[cfg]);
         if (active) refresh_ring(c, L, s);
         f.init = 0;
         if (f.fold) {
@@ -1263,12 +1278,12 @@ __global__ void __launch_bounds__(1024, 1)
                     dispatch(g, c, L, s, f, tr.y, rec_b(g, L.nb + tr.y), 0, tr.z, 0);
                 }
                 if (prev >= 0) start_phase(g, o, c, L, s, f, 0, cfg);
-                F32(Q_DONE, tid) += g.s_nstatic[st];
+                F32<K>(Q_DONE, tid) += g.s_nstatic[st];
                 if (o.ev_start)
                     for (int q = g.static_off[st]; q < g.static_off[st + 1]; q++)
                         record(g, o, cfg, L.r, g.static_list[q], 0, 0);
             }
-            reserve<MSG, CL>(g, o, c, sh, par, 0, false, cfg, f.epoch, topo, p.cols[cfg]);
+            reserve<MSG, CL, KK>(g, o, c, sh, par, 0, false, cfg, f.epoch, topo, p.cols[cfg]);
             if (active) refresh_ring(c, L, s);
         }
         int64_t tcur = 0;
@@ -1290,7 +1305,7 @@ __global__ void __launch_bounds__(1024, 1)
             // reduction's barrier made every arrival visible), then re-derive the next time
             const int nc = CL ? *c.ncomp : sh.ncomp, nmc = MSG ? (CL ? *c.nmcomp : sh.nmcomp) : 0;
             if (nc | nmc) {
-                reserve_n<MSG, CL>(g, o, c, sh, par, tcur, false, cfg, f.epoch, nc, nmc,
+                reserve_n<MSG, CL, K>(g, o, c, sh, par, tcur, false, cfg, f.epoch, nc, nmc,
                                                      topo, p.cols[cfg]);
                     if (active) refresh_ring(c, L, s);
                 nt = active ? next_time(g, c, L, s, tcur) : TINF;
@@ -1317,7 +1332,7 @@ __global__ void __launch_bounds__(1024, 1)
                     s.pop_seq = 0;
                     while (s.due.head >= 0) {
                         int64_t fx;
-                        const int x = ms_pop_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, fx, g.max_words);
+                        const int x = ms_pop_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, fx, g.max_words);
                         pop_event(g, c, L, s, f, x, fx, t);
                         PROF_MARK(7);                       // pop_event
                         start_phase(g, o, c, L, s, f, t, cfg);
@@ -1336,11 +1351,11 @@ __global__ void __launch_bounds__(1024, 1)
                     if (active && (int)(m2 >> 13) == L.r) {
                         s.pop_seq = 0;
                         int64_t fx;
-                        const int x = ms_pop_cp<F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, fx, g.max_words);
+                        const int x = ms_pop_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, fx, g.max_words);
                         pop_event(g, c, L, s, f, x, fx, t);
                     }
                     if (active) start_phase(g, o, c, L, s, f, t, cfg);
-                    reserve<MSG, CL>(g, o, c, sh, par, t, false, cfg, f.epoch, topo,
+                    reserve<MSG, CL, KK>(g, o, c, sh, par, t, false, cfg, f.epoch, topo,
                                                        p.cols[cfg]);
                             if (active) {
                         refresh_ring(c, L, s);
@@ -1360,18 +1375,18 @@ __global__ void __launch_bounds__(1024, 1)
 #endif
 
         // ---- row: reductions over ranks (cli.py:336-341) ----
-        int dead = active && F32(Q_DONE, tid) != my_n;
+        int dead = active && F32<K>(Q_DONE, tid) != my_n;
         dead = gor<CL>(dead | overflow, sh, par);
         dirty = dead != 0;
         int64_t vals[6] = {0, 0, 0, 0, 0, 0};
         if (active) {
-            const int64_t comm = s.commcum, cpx = F64(F_CPMAX, tid);
-            vals[0] = F64(F_FIN, tid);
+            const int64_t comm = s.commcum, cpx = F64<K>(F_CPMAX, tid);
+            vals[0] = F64<K>(F_FIN, tid);
             vals[1] = cpx;
-            vals[2] = F64(F_COMP, tid);
+            vals[2] = F64<K>(F_COMP, tid);
             vals[3] = comm;
-            vals[4] = comm - F64(F_OVL, tid);
-            vals[5] = F64(F_PEAK, tid);
+            vals[4] = comm - F64<K>(F_OVL, tid);
+            vals[5] = F64<K>(F_PEAK, tid);
             if (o.rank_stats) {
                 int64_t *rs = o.rank_stats + ((size_t)cfg * R + L.r) * 5;
                 rs[0] = vals[0]; rs[1] = vals[2]; rs[2] = vals[3]; rs[3] = vals[4]; rs[4] = vals[5];
@@ -1399,6 +1414,7 @@ __global__ void __launch_bounds__(1024, 1)
 // contention-free bound does not have.  One thread per design point.
 //   vertex v: vkind 0 = (rank va, local node vb), 1 = collective instance va;
 //   vsend[v] >= 0 for a RECV: the vertex of its SEND, vmsg[v] the message.
+#if FL_COMMON
 __global__ void cp_kernel(const __grid_constant__ DevGraph g, const __grid_constant__ DevPoints p, int nv,
                           const int32_t *order, const int32_t *vkind, const int32_t *va, const int32_t *vb,
                           const int32_t *vsend, const int32_t *vmsg, const int32_t *poff, const int32_t *pidx,
@@ -1436,13 +1452,14 @@ __global__ void cp_kernel(const __grid_constant__ DevGraph g, const __grid_const
     out[cfg] = best;
     status[cfg] = st;
 }
+#endif
 
 // ------------------------------------------------------------ host side
 
 template <int T>
 static cudaError_t launch_t(int grid, int block, size_t smem, cudaStream_t st, int cluster, const DevGraph &g,
                             const DevPoints &p, const DevOut &o, const DevScratch &sc) {
-    if (cluster <= 1) {
+    if (cluster <= 1 || (T >> 5)) {     // narrow planes: single-CTA design points only
         sweep_kernel<T, false><<<grid, block, smem, st>>>(g, p, o, sc);
         return cudaGetLastError();
     }
@@ -1461,22 +1478,82 @@ static cudaError_t launch_t(int grid, int block, size_t smem, cudaStream_t st, i
     return cudaLaunchKernelEx(&cfg, sweep_kernel<T, true>, g, p, o, sc);
 }
 
+static inline int plane_class(int block) { return block > 256 ? 0 : block > 64 ? 1 : 2; }
+static inline int plane_lanes_for(int block) { return block > 256 ? 1024 : block > 64 ? 256 : 64; }
+
+// The variants are compiled in six translation units (-DFL_BASE = compute streams | 8 with
+// messages), each holding its three plane widths and its cluster variant.
+#define FL_PART_DECL(B)                                                                                     \
+    cudaError_t launch_sweep_b##B(int T, int grid, int block, size_t smem, cudaStream_t st, int cluster,   \
+                                  const DevGraph &g, const DevPoints &p, const DevOut &o, const DevScratch &sc); \
+    cudaError_t set_smem_b##B(size_t smem);
+FL_PART_DECL(1) FL_PART_DECL(2) FL_PART_DECL(4) FL_PART_DECL(9) FL_PART_DECL(10) FL_PART_DECL(12)
+
+#define FL_PART_DEF(B)                                                                                      \
+    cudaError_t launch_sweep_b##B(int T, int grid, int block, size_t smem, cudaStream_t st, int cluster,   \
+                                  const DevGraph &g, const DevPoints &p, const DevOut &o, const DevScratch &sc) { \
+        switch (T) {                                                                                        \
+            case B: return launch_t<B>(grid, block, smem, st, cluster, g, p, o, sc);                        \
+            case B + 32: return launch_t<B + 32>(grid, block, smem, st, cluster, g, p, o, sc);              \
+            case B + 64: return launch_t<B + 64>(grid, block, smem, st, cluster, g, p, o, sc);              \
+            default: return cudaErrorInvalidValue;                                                          \
+        }                                                                                                   \
+    }                                                                                                       \
+    cudaError_t set_smem_b##B(size_t smem) {                                                                \
+        cudaError_t e = cudaSuccess;                                                                        \
+        const cudaFuncAttribute A = cudaFuncAttributeMaxDynamicSharedMemorySize;                            \
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<B, false>, A, (int)smem);               \
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<B + 32, false>, A, (int)smem);          \
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<B + 64, false>, A, (int)smem);          \
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<B, true>, A, (int)smem);                \
+        if (e == cudaSuccess)                                                                               \
+            e = cudaFuncSetAttribute(sweep_kernel<B, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
+        return e;                                                                                           \
+    }
+
+#if FL_BASE == 0 || FL_BASE == 1
+FL_PART_DEF(1)
+#endif
+#if FL_BASE == 0 || FL_BASE == 2
+FL_PART_DEF(2)
+#endif
+#if FL_BASE == 0 || FL_BASE == 4
+FL_PART_DEF(4)
+#endif
+#if FL_BASE == 0 || FL_BASE == 9
+FL_PART_DEF(9)
+#endif
+#if FL_BASE == 0 || FL_BASE == 10
+FL_PART_DEF(10)
+#endif
+#if FL_BASE == 0 || FL_BASE == 12
+FL_PART_DEF(12)
+#endif
+
+#if FL_COMMON
 cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t st, int cluster, const DevGraph &g,
                          const DevPoints &p, const DevOut &o, const DevScratch &sc) {
-    // template argument: compute streams (1, 2, 4) | 8 when the graphs carry SEND/RECV
-    const int T = K | (g.n_msg > 0 ? 8 : 0);
-    switch (T) {
-        case 1: return launch_t<1>(grid, block, smem, st, cluster, g, p, o, sc);
-        case 2: return launch_t<2>(grid, block, smem, st, cluster, g, p, o, sc);
-        case 4: return launch_t<4>(grid, block, smem, st, cluster, g, p, o, sc);
-        case 9: return launch_t<9>(grid, block, smem, st, cluster, g, p, o, sc);
-        case 10: return launch_t<10>(grid, block, smem, st, cluster, g, p, o, sc);
-        default: return launch_t<12>(grid, block, smem, st, cluster, g, p, o, sc);
+    // variant word: compute streams (1, 2, 4) | 8 when the graphs carry SEND/RECV | plane class << 5
+    const int B = K | (g.n_msg > 0 ? 8 : 0);
+    const int T = B | (cluster > 1 ? 0 : plane_class(block) << 5);
+    switch (B) {
+        case 1: return launch_sweep_b1(T, grid, block, smem, st, cluster, g, p, o, sc);
+        case 2: return launch_sweep_b2(T, grid, block, smem, st, cluster, g, p, o, sc);
+        case 4: return launch_sweep_b4(T, grid, block, smem, st, cluster, g, p, o, sc);
+        case 9: return launch_sweep_b9(T, grid, block, smem, st, cluster, g, p, o, sc);
+        case 10: return launch_sweep_b10(T, grid, block, smem, st, cluster, g, p, o, sc);
+        case 12: return launch_sweep_b12(T, grid, block, smem, st, cluster, g, p, o, sc);
+        default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t sweep_occupancy(int block, size_t smem, int cluster, int *occ) {
-    if (cluster <= 1) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, sweep_kernel<1, false>, block, smem);
+    if (cluster <= 1) {
+        const int pc = plane_class(block);
+        return pc == 0 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, sweep_kernel<1, false>, block, smem)
+             : pc == 1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, sweep_kernel<33, false>, block, smem)
+                       : cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, sweep_kernel<65, false>, block, smem);
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cluster);
     cfg.blockDim = dim3(block);
@@ -1492,30 +1569,19 @@ cudaError_t sweep_occupancy(int block, size_t smem, int cluster, int *occ) {
 }
 
 cudaError_t sweep_set_smem(size_t smem) {
-    cudaError_t e = cudaSuccess;
-#define FL_SET(T)                                                                                               \
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<T, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    FL_SET(1) FL_SET(2) FL_SET(4) FL_SET(9) FL_SET(10) FL_SET(12)
-#undef FL_SET
-#ifdef FL_CARVEOUT
-    // leave the rest of the SM's SRAM to L1 (register spills live there)
-    int pct = (int)((smem + 8192) * 100 / (228 * 1024)) + 1;
-    pct = pct > 100 ? 100 : pct;
-#define FL_CO(T) \
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<T, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct); \
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<T, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    FL_CO(1) FL_CO(2) FL_CO(4) FL_CO(9) FL_CO(10) FL_CO(12)
-#undef FL_CO
-#endif
+    cudaError_t e = set_smem_b1(smem);
+    if (e == cudaSuccess) e = set_smem_b2(smem);
+    if (e == cudaSuccess) e = set_smem_b4(smem);
+    if (e == cudaSuccess) e = set_smem_b9(smem);
+    if (e == cudaSuccess) e = set_smem_b10(smem);
+    if (e == cudaSuccess) e = set_smem_b12(smem);
     return e;
 }
 
 size_t sweep_shared_header_bytes() { return SM_HDR; }
-size_t sweep_shared_bytes_per_rank() { return 8 * F_NSM + 4 * Q_N32; }   // x FL_SR lanes
+size_t sweep_shared_bytes_per_rank() { return 8 * F_NSM + 4 * Q_N32; }   // x plane lanes
 size_t sweep_global_bytes_per_rank() { return 8 * (F_N64 - F_NSM); }
-int sweep_plane_lanes() { return FL_SR; }
+int sweep_plane_lanes(int block, int cluster) { return cluster > 1 ? 1024 : plane_lanes_for(block); }
 
 cudaError_t launch_cp(const DevGraph &g, const DevPoints &p, int nv, const int32_t *order, const int32_t *vkind,
                       const int32_t *va, const int32_t *vb, const int32_t *vsend, const int32_t *vmsg,
@@ -1535,5 +1601,6 @@ cudaError_t launch_cost_only(int n, const uint8_t *kind, const int64_t *size, co
                                                    status, m, flops, peak, eff, out_comp);
     return cudaGetLastError();
 }
+#endif  // FL_COMMON
 
 }  // namespace fl

@@ -77,7 +77,7 @@ cudaError_t sweep_set_smem(size_t smem);
 size_t sweep_shared_header_bytes();
 size_t sweep_shared_bytes_per_rank();   // the [field][blockDim] per-rank planes
 size_t sweep_global_bytes_per_rank();
-int sweep_plane_lanes();               // per-rank planes are this many lanes wide
+int sweep_plane_lanes(int block, int cluster);   // per-rank planes are this many lanes wide
 cudaError_t launch_cp(const DevGraph &g, const DevPoints &p, int nv, const int32_t *order, const int32_t *vkind,
                       const int32_t *va, const int32_t *vb, const int32_t *vsend, const int32_t *vmsg,
                       const int32_t *poff, const int32_t *pidx, int64_t *vals, int64_t *out, int32_t *status);

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import shutil
 import subprocess
 from pathlib import Path
 
@@ -65,6 +66,7 @@ def _compile(out: Path, defines=(), verbose: bool = False) -> str:
     link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *[str(o) for _, o, _ in jobs],
             "-o", str(out)]
     res = subprocess.run(link, capture_output=True, text=True)
+    shutil.rmtree(tmp, ignore_errors=True)
     if res.returncode != 0:
         raise EngineError("nvcc link failed:\n" + res.stderr[-4000:])
     return err

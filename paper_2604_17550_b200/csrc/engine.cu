@@ -690,6 +690,20 @@ __device__ __forceinline__ void load_head(const Ctx &c, const Lane &L, Rank<K> &
     }
 }
 
+// Append to lane lm's comm FIFO (rank m).  An entry appended to an empty FIFO is the
+// head: it goes straight to the head fields in shared memory, the rest to HBM.
+template <int K>
+__device__ __forceinline__ void append_ring(const Ctx &c, int lm, int m, int R, int inst, int node) {
+    const int slot = F32<K>(Q_RING_TAIL, lm)++;
+    if (slot == F32<K>(Q_RING_HEAD, lm)) {
+        F32<K>(Q_HEAD_NODE, lm) = node;
+        F32<K>(Q_HEAD_INST, lm) = inst;
+    } else {
+        c.ring_inst[slot * R + m] = inst;
+        c.ring_node[slot * R + m] = node;
+    }
+}
+
 // After reservations: pick up comm-FIFO entries appended for this rank.
 template <int K>
 __device__ __forceinline__ void refresh_ring(const Ctx &c, const Lane &L, Rank<K> &s) {
@@ -697,7 +711,11 @@ __device__ __forceinline__ void refresh_ring(const Ctx &c, const Lane &L, Rank<K
     const int seen = F32<K>(Q_RING_SEEN, L.lr);
     if (tail != seen) {
         F32<K>(Q_RING_SEEN, L.lr) = tail;
-        if (s.head_e == TINF) load_head(c, L, s);
+        if (s.head_e == TINF) {     // the FIFO was empty: append_ring installed the new head
+            const int i = F32<K>(Q_HEAD_INST, L.lr);
+            s.head_s = c.inst_s[i];
+            s.head_e = c.inst_e[i];
+        }
     }
 }
 
@@ -917,8 +935,9 @@ static __device__ void reserve_msgs(const DevGraph &g, const DevOut &o, const Ct
 // reference's order (simulator.py:298-309), block- (or cluster-) wide; then the
 // step's messages (simulator.py:310-327).  Returns the largest critical-path
 // finish among them.
+// (inlined: as a real call the ABI spilled the caller's live registers around it)
 template <bool MSG, bool CL, int K>
-__device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, const Ctx &c, Shared &sh, int &par,
+__device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, const Ctx &c, Shared &sh, int &par,
                                           int64_t t, bool init, int cfg, uint64_t epoch,
                                           int nc, int nmc, int topo, int cols) {
     int64_t cpm = 0;
@@ -964,9 +983,7 @@ __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, co
             for (int lm = threadIdx.x; lm < RL; lm += blockDim.x) {
                 const int m = base + lm;
                 F64<K>(F_COMM_END, lm) = e;
-                const int slot = F32<K>(Q_RING_TAIL, lm)++;
-                c.ring_inst[slot * R + m] = i;
-                c.ring_node[slot * R + m] = full_node;
+                append_ring<K>(c, lm, m, R, i, full_node);
                 record(g, o, cfg, m, full_node, s, e);
             }
             uni = true;
@@ -977,9 +994,7 @@ __device__ __noinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, co
                 const int lm = m - base;
                 if (lm < 0 || lm >= RL) continue;
                 F64<K>(F_COMM_END, lm) = e;
-                const int slot = F32<K>(Q_RING_TAIL, lm)++;
-                c.ring_inst[slot * R + m] = i;
-                c.ring_node[slot * R + m] = node;
+                append_ring<K>(c, lm, m, R, i, node);
                 record(g, o, cfg, m, node, s, e);
             }
             uni = false;

@@ -165,7 +165,8 @@ int fl_sweep_run_device(fl_graph *g, const fl_points *dev_points, fl_outputs *de
 
 /* Contention-free critical path alone (simulator.py:400-460) for host design
  * points, over the merged multi-rank graph given as vertices in topological
- * order (vkind 0: rank va's node vb; 1: collective instance va; RECVs carry
+ * order (n_vert entries, padded with -1 after the live vertices;
+ * vkind 0: rank va's node vb; 1: collective instance va; RECVs carry
  * their SEND's vertex in vsend and the message in vmsg) with predecessor CSR.
  * fl_sweep_run computes the same value as a by-product of the simulation; this
  * entry point serves critical_path() when the simulation itself deadlocks. */
@@ -173,6 +174,16 @@ int fl_critical_path(fl_graph *g, const fl_points *host_points, int32_t n_vert, 
                      const int32_t *vkind, const int32_t *va, const int32_t *vb, const int32_t *vsend,
                      const int32_t *vmsg, const int32_t *pred_off, const int32_t *pred_idx,
                      int64_t *out_cp, int32_t *out_status);
+
+/* fl_critical_path plus every vertex's contention-free finish and start times
+ * (out_vals[point * n_vert + vertex] finishes, then out_vals[(n_points + point) * n_vert
+ * + vertex] starts; host buffer of 2 * n_points * n_vert), from which the host derives the
+ * critical-path node trace ("duration_ns and node path"; the reference
+ * implementation returns only the length, simulator.py:400-460). */
+int fl_critical_path_values(fl_graph *g, const fl_points *host_points, int32_t n_vert, const int32_t *order,
+                            const int32_t *vkind, const int32_t *va, const int32_t *vb, const int32_t *vsend,
+                            const int32_t *vmsg, const int32_t *pred_off, const int32_t *pred_idx,
+                            int64_t *out_cp, int32_t *out_status, int64_t *out_vals);
 
 /* Cost stage alone (K1 parity hook): alpha-beta time of n collectives and
  * flops->ns of m compute nodes, evaluated by the device code path. Host buffers. */

@@ -765,7 +765,11 @@ cleanup:
 
 /* ------------------------------------------------------- critical path */
 
-int or_critical_path(const or_graphs *G, const or_config *cfg, int64_t *result, char *err, int errlen) {
+/* critical_path, optionally with every node's finish and start, its collective
+ * instance (-1: none) and, for a RECV, its SEND (-1: none) -- the inputs of the
+ * node-trace rule in pyoracle.critical_path_trace.  Flat node order. */
+int or_critical_path_ex(const or_graphs *G, const or_config *cfg, int64_t *result, int64_t *node_fin,
+                        int64_t *node_start, int64_t *node_inst, int64_t *node_send, char *err, int errlen) {
     int64_t nr = G->n_ranks, total = G->node_off[nr];
     lookup L;
     if (build_lookup(G, &L)) { free_lookup(&L); set_err(err, errlen, "duplicate rank in graphs"); return OR_INVALID; }
@@ -847,6 +851,7 @@ int or_critical_path(const or_graphs *G, const or_config *cfg, int64_t *result, 
             if (wire > start) start = wire;
         }
         vfin[w] = start + vdur[w];
+        vstart[w] = start;
         seen += w < total ? 1 : (I.mem_off[w - total + 1] - I.mem_off[w - total]);
         /* successors of every node that maps to this vertex */
         if (w < total) {
@@ -872,6 +877,13 @@ int or_critical_path(const or_graphs *G, const or_config *cfg, int64_t *result, 
         int64_t best = 0;
         for (int64_t w = 0; w < nv; w++) if (live[w] && vfin[w] > best) best = vfin[w];
         *result = best;
+        if (node_fin)
+            for (int64_t v = 0; v < total; v++) {
+                node_fin[v] = vfin[vert_of[v]];
+                node_start[v] = vstart[vert_of[v]];
+                node_inst[v] = inst_of[v];
+                node_send[v] = (G->node_kind[v] == K_RECV && msg_of[v] >= 0) ? msgs[msg_of[v]].send : -1;
+            }
     }
     free(vstart); free(queue); free(live);
 cleanup:
@@ -882,4 +894,8 @@ cleanup:
     free(inst_of); free(rank_of);
     free_lookup(&L);
     return rc;
+}
+
+int or_critical_path(const or_graphs *G, const or_config *cfg, int64_t *result, char *err, int errlen) {
+    return or_critical_path_ex(G, cfg, result, NULL, NULL, NULL, NULL, err, errlen);
 }

@@ -80,6 +80,8 @@ def lib():
         _lib = C.CDLL(str(LIB_PATH))
         _lib.or_simulate.argtypes = [C.POINTER(OrGraphs), C.POINTER(OrConfig), C.POINTER(OrSimOut), C.c_char_p, C.c_int]
         _lib.or_critical_path.argtypes = [C.POINTER(OrGraphs), C.POINTER(OrConfig), P, C.c_char_p, C.c_int]
+        _lib.or_critical_path_ex.argtypes = [C.POINTER(OrGraphs), C.POINTER(OrConfig), P, P, P, P, P,
+                                             C.c_char_p, C.c_int]
         _lib.or_analytical_time.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int, C.c_double, C.c_double,
                                             C.c_int64, C.c_int64, C.POINTER(C.c_int)]
         _lib.or_analytical_time.restype = C.c_int64
@@ -239,6 +241,57 @@ def critical_path(graphs, topo, algo="ring", flat=None) -> int:
     if rc:
         raise OracleError(rc, err.value.decode())
     return int(res.value)
+
+
+def critical_path_trace(graphs, topo, algo="ring", flat=None):
+    """(length, [(rank, node_id), ...]) -- the node-trace rule documented at
+    paper_2604_17550_b200.engine.critical_path_trace, over the C restatement's
+    per-node finish/start times (or_critical_path_ex, simulator.py:400-460)."""
+    flat = flat if flat is not None else flatten(graphs)
+    g = _struct(flat)
+    cfg = _config(topo, algo)
+    total = int(flat["node_off"][-1])
+    fin, start, inst, send = (np.zeros(max(1, total), np.int64) for _ in range(4))
+    res = C.c_int64(0)
+    err = C.create_string_buffer(512)
+    rc = lib().or_critical_path_ex(C.byref(g), C.byref(cfg), C.byref(res), fin.ctypes.data_as(P),
+                                   start.ctypes.data_as(P), inst.ctypes.data_as(P), send.ctypes.data_as(P), err, 512)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    if total == 0:
+        return int(res.value), []
+    node_off, node_id, rank_value = flat["node_off"], flat["node_id"], flat["rank_value"]
+    rank_of = np.repeat(np.arange(len(rank_value)), np.diff(node_off))
+    index = {(int(rank_of[v]), int(node_id[v])): v for v in range(total)}
+    members = {}
+    for v in range(total):
+        if inst[v] >= 0:
+            members.setdefault(int(inst[v]), []).append(v)
+    dep_off, dep_ids = flat["dep_off"], flat["dep_ids"]
+
+    def key(v):
+        return int(rank_value[rank_of[v]]), int(node_id[v])
+
+    def deps(v):
+        out = set()
+        for m in (members[int(inst[v])] if inst[v] >= 0 else [v]):
+            r = int(rank_of[m])
+            for q in range(int(dep_off[m]), int(dep_off[m + 1])):
+                out.add(index[(r, int(dep_ids[q]))])
+        return out
+
+    v = min(range(total), key=lambda u: (-int(fin[u]), key(u)))
+    path = [v]
+    while True:
+        hit = [d for d in deps(v) if fin[d] == start[v]]
+        if hit:
+            v = min(hit, key=key)
+        elif send[v] >= 0:
+            v = int(send[v])
+        else:
+            break
+        path.append(v)
+    return int(res.value), [key(u) for u in reversed(path)]
 
 
 def analytical_time(kind: str, size_bytes: int, n: int, algo: str, alpha: float, beta: float,

@@ -11,7 +11,7 @@ and specs can be handed over unchanged.
 from .costs import (DEFAULT_DEVICE, CollectiveAlgo, DeviceSpec, ProfileTable, analytical_duration,
                     analytical_time, load_profile, op_flops, round_half_up_ns)
 from .engine import (ROW_FIELDS, DesignPoints, Engine, RankStats, SimOptions, SimReport, TraceEvent,
-                     cost_only, critical_path, simulate, simulate_batch)
+                     cost_only, critical_path, critical_path_trace, simulate, simulate_batch)
 from .errors import (DeadlockError, EngineError, FormatError, InconsistentGroupsError, TrainsimError,
                      UnsupportedAlgoTopologyError, UnsupportedComboError)
 from .expansion import (P2pPlan, PlanOp, check_plan, collective_instances, dataflow_check, expand,

@@ -159,6 +159,8 @@ def _bind(L):
     L.fl_sweep_run_device.argtypes = [C.c_void_p, C.POINTER(Points), C.POINTER(Outputs), C.c_void_p, P32]
     L.fl_critical_path.argtypes = [C.c_void_p, C.POINTER(Points), C.c_int32, P32, P32, P32, P32, P32, P32, P32,
                                    P32, P64, P32]
+    L.fl_critical_path_values.argtypes = [C.c_void_p, C.POINTER(Points), C.c_int32, P32, P32, P32, P32, P32, P32,
+                                          P32, P32, P64, P32, P64]
     L.fl_cost_only.argtypes = [C.c_int32, PU8, P64, P64, PU8, PF64, PF64, P32, P32, P64, P32,
                                C.c_int32, P64, PF64, PF64, P64]
     return L
@@ -169,4 +171,5 @@ def last_error() -> str:
 
 
 EXPORTED = ["fl_version", "fl_last_error", "fl_device_count", "fl_graph_create", "fl_graph_destroy",
-            "fl_graph_max_nodes", "fl_sweep_run", "fl_sweep_run_device", "fl_critical_path", "fl_cost_only"]
+            "fl_graph_max_nodes", "fl_sweep_run", "fl_sweep_run_device", "fl_critical_path",
+            "fl_critical_path_values", "fl_cost_only"]

@@ -580,9 +580,10 @@ int fl_sweep_run(fl_graph *g, const fl_points *hp, fl_outputs *ho) {
     return FL_OK;
 }
 
-int fl_critical_path(fl_graph *g, const fl_points *hp, int32_t nv, const int32_t *order, const int32_t *vkind,
-                     const int32_t *va, const int32_t *vb, const int32_t *vsend, const int32_t *vmsg,
-                     const int32_t *pred_off, const int32_t *pred_idx, int64_t *out_cp, int32_t *out_status) {
+static int critical_path_impl(fl_graph *g, const fl_points *hp, int32_t nv, const int32_t *order,
+                              const int32_t *vkind, const int32_t *va, const int32_t *vb, const int32_t *vsend,
+                              const int32_t *vmsg, const int32_t *pred_off, const int32_t *pred_idx,
+                              int64_t *out_cp, int32_t *out_status, int64_t *out_vals) {
     if (!g || !hp || nv < 0) return fail(FL_ERR_INVALID, "bad argument");
     CK(cudaSetDevice(g->device));
     const size_t n = (size_t)hp->n_points;
@@ -606,19 +607,37 @@ int fl_critical_path(fl_graph *g, const fl_points *hp, int32_t nv, const int32_t
         return rc;
     }
     void *pv = nullptr;
-    if (cudaMalloc(&pv, n * V * 8) != cudaSuccess) { free_all(tmp); return fail(FL_ERR_CUDA, "cp scratch"); }
+    if (cudaMalloc(&pv, n * V * 8 * (out_vals ? 2 : 1)) != cudaSuccess) { free_all(tmp); return fail(FL_ERR_CUDA, "cp scratch"); }
     tmp.push_back(pv);
     vals = static_cast<int64_t *>(pv);
+    int64_t *starts = out_vals ? vals + n * V : nullptr;
     fl::DevPoints dp;
     dp.n = (int)n; dp.algo = algo; dp.topo_kind = topo; dp.bw = bw; dp.latency = lat; dp.rows = rows;
     dp.cols = cols; dp.peak_flops = peak; dp.efficiency = eff; dp.compute_streams = 1;
-    cudaError_t e = fl::launch_cp(g->dg, dp, nv, dorder, dk, da, db, ds, dm, dpo, dpi, vals, dout, dst);
+    cudaError_t e = fl::launch_cp(g->dg, dp, nv, dorder, dk, da, db, ds, dm, dpo, dpi, vals, starts, dout, dst);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e == cudaSuccess) e = cudaMemcpy(out_cp, dout, n * 8, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) e = cudaMemcpy(out_status, dst, n * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && out_vals) e = cudaMemcpy(out_vals, vals, 2 * n * V * 8, cudaMemcpyDeviceToHost);
     free_all(tmp);
     if (e != cudaSuccess) return fail(FL_ERR_CUDA, cudaGetErrorString(e));
     return FL_OK;
+}
+
+int fl_critical_path(fl_graph *g, const fl_points *hp, int32_t nv, const int32_t *order, const int32_t *vkind,
+                     const int32_t *va, const int32_t *vb, const int32_t *vsend, const int32_t *vmsg,
+                     const int32_t *pred_off, const int32_t *pred_idx, int64_t *out_cp, int32_t *out_status) {
+    return critical_path_impl(g, hp, nv, order, vkind, va, vb, vsend, vmsg, pred_off, pred_idx, out_cp, out_status,
+                              nullptr);
+}
+
+int fl_critical_path_values(fl_graph *g, const fl_points *hp, int32_t nv, const int32_t *order,
+                            const int32_t *vkind, const int32_t *va, const int32_t *vb, const int32_t *vsend,
+                            const int32_t *vmsg, const int32_t *pred_off, const int32_t *pred_idx,
+                            int64_t *out_cp, int32_t *out_status, int64_t *out_vals) {
+    if (!out_vals) return fail(FL_ERR_INVALID, "out_vals is required");
+    return critical_path_impl(g, hp, nv, order, vkind, va, vb, vsend, vmsg, pred_off, pred_idx, out_cp, out_status,
+                              out_vals);
 }
 
 int fl_cost_only(int32_t n, const uint8_t *kind, const int64_t *size_bytes, const int64_t *group_n,

@@ -1433,21 +1433,24 @@ __global__ void __launch_bounds__(1024, 1)
 __global__ void cp_kernel(const __grid_constant__ DevGraph g, const __grid_constant__ DevPoints p, int nv,
                           const int32_t *order, const int32_t *vkind, const int32_t *va, const int32_t *vb,
                           const int32_t *vsend, const int32_t *vmsg, const int32_t *poff, const int32_t *pidx,
-                          int64_t *vals, int64_t *out, int32_t *status) {
+                          int64_t *vals, int64_t *starts, int64_t *out, int32_t *status) {
     const int cfg = blockIdx.x * blockDim.x + threadIdx.x;
     if (cfg >= p.n) return;
     int64_t *cv = vals + (size_t)cfg * nv;
+    int64_t *sv = starts ? starts + (size_t)cfg * nv : nullptr;   // start times, for the node trace
     const int topo = p.topo_kind[cfg], cols = p.cols[cfg];
     const double beta = __ddiv_rn(1e9, p.bw[cfg]);
     int64_t best = 0;
     int st = FL_OK;
     for (int q = 0; q < nv; q++) {
         const int v = order[q];
+        if (v < 0) break;                           // order is padded with -1 past the live vertices
         int64_t x = 0;
         for (int u = poff[v]; u < poff[v + 1]; u++) x = cv[pidx[u]] > x ? cv[pidx[u]] : x;   // :449
         if (vkind[v] == 1) {                        // collective: union of the members' deps (:419-428)
             const int64_t d = coll_time(g, va[v], p.algo[cfg], topo, p.bw[cfg], p.latency[cfg], p.rows[cfg], cols);
             if (d < 0) { st = FL_ERR_UNSUPPORTED_ALGO; break; }
+            if (sv) sv[v] = x;
             x += d;
         } else {
             const int gn = g.s_node_off[g.rank_struct[va[v]]] + vb[v];
@@ -1459,6 +1462,7 @@ __global__ void cp_kernel(const __grid_constant__ DevGraph g, const __grid_const
             }
             int64_t d = g.node_dur[gn];
             if (p.peak_flops && g.node_flops[gn] >= 0) d = flops_to_ns(g.node_flops[gn], p.peak_flops[cfg], p.efficiency[cfg]);
+            if (sv) sv[v] = x;
             if ((g.node_rec[2 * gn + 1].x & 15u) <= FL_COMP) x += d;   // `duration_ns or 0`
         }
         cv[v] = x;
@@ -1600,8 +1604,10 @@ int sweep_plane_lanes(int block, int cluster) { return cluster > 1 ? 1024 : plan
 
 cudaError_t launch_cp(const DevGraph &g, const DevPoints &p, int nv, const int32_t *order, const int32_t *vkind,
                       const int32_t *va, const int32_t *vb, const int32_t *vsend, const int32_t *vmsg,
-                      const int32_t *poff, const int32_t *pidx, int64_t *vals, int64_t *out, int32_t *status) {
-    cp_kernel<<<(p.n + 127) / 128, 128>>>(g, p, nv, order, vkind, va, vb, vsend, vmsg, poff, pidx, vals, out, status);
+                      const int32_t *poff, const int32_t *pidx, int64_t *vals, int64_t *starts, int64_t *out,
+                      int32_t *status) {
+    cp_kernel<<<(p.n + 127) / 128, 128>>>(g, p, nv, order, vkind, va, vb, vsend, vmsg, poff, pidx, vals, starts, out,
+                                          status);
     return cudaGetLastError();
 }
 

@@ -80,7 +80,8 @@ size_t sweep_global_bytes_per_rank();
 int sweep_plane_lanes(int block, int cluster);   // per-rank planes are this many lanes wide
 cudaError_t launch_cp(const DevGraph &g, const DevPoints &p, int nv, const int32_t *order, const int32_t *vkind,
                       const int32_t *va, const int32_t *vb, const int32_t *vsend, const int32_t *vmsg,
-                      const int32_t *poff, const int32_t *pidx, int64_t *vals, int64_t *out, int32_t *status);
+                      const int32_t *poff, const int32_t *pidx, int64_t *vals, int64_t *starts, int64_t *out,
+                      int32_t *status);
 cudaError_t launch_cost_only(int n, const uint8_t *kind, const int64_t *size, const int64_t *gn,
                              const uint8_t *algo, const double *alpha, const double *beta,
                              const int32_t *rows, const int32_t *cols, int64_t *out, int32_t *status,

@@ -364,6 +364,98 @@ def critical_path(graphs, topo, algo=CollectiveAlgo.RING, device: int = 0) -> in
     return int(out["rows"][0, 1])
 
 
+def critical_path_trace(graphs, topo, algo=CollectiveAlgo.RING, device: int = 0):
+    """Critical path with its node trace: ``(length_ns, [(rank, node_id), ...])``.
+
+    SPEC.md:460 defines ``critical_path`` as "duration_ns and node path"; the reference
+    implementation returns only the length (simulator.py:400-460), so the path rule is
+    this package's, restated in oracle/pyoracle.py:critical_path_trace:
+
+    * the sink is the (rank, node_id) with the largest contention-free finish, the
+      lowest (rank, node_id) on ties;
+    * a node's predecessor on the path is its lowest (rank, node_id) dependency whose
+      finish equals the node's start (a collective member's dependencies are the union
+      over its group, simulator.py:419-428); when no dependency does, the start was
+      set by a RECV's SEND plus the wire time (simulator.py:430-435, :450-452) and the
+      path continues at the SEND; a node whose start no predecessor sets is the source.
+
+    Every finish and start comes from the GPU (fl_critical_path_values); the host only
+    walks back through them.
+    """
+    from .store import merged_cp_graph
+    gs = compile_graphs(graphs)
+    if gs.pair_error:
+        _raise_pair_error(gs, topo, algo)
+    mg = merged_cp_graph(gs)
+    eng = Engine(gs, device)
+    try:
+        pts = _single_point(topo, algo)
+        p = _native.Points(1, _ptr(pts.algo, _native.PU8), _ptr(pts.topo_kind, _native.PU8),
+                           _ptr(pts.bw, _native.PF64), _ptr(pts.latency, _native.P64),
+                           _ptr(pts.rows, _native.P32), _ptr(pts.cols, _native.P32),
+                           _ptr(pts.peak_flops, _native.PF64), _ptr(pts.efficiency, _native.PF64), 1)
+        V = int(mg["n_vert"])
+        cp = np.zeros(1, np.int64)
+        st = np.zeros(1, np.int32)
+        vals = np.zeros(2 * max(V, 1), np.int64)
+        arr = {k: np.ascontiguousarray(v if len(v) else np.zeros(1, np.int32)) for k, v in mg.items() if k != "n_vert"}
+        rc = _native.lib().fl_critical_path_values(eng._h, C.byref(p), V, *(
+            _ptr(arr[k], _native.P32) for k in ("order", "vkind", "va", "vb", "vsend", "vmsg", "pred_off", "pred_idx")),
+            _ptr(cp, _native.P64), _ptr(st, _native.P32), _ptr(vals, _native.P64))
+        if rc:
+            raise EngineError(f"fl_critical_path_values: {_native.last_error()} (status {rc})")
+    finally:
+        eng.close()
+    raise_for_status(int(st[0]))
+    finish, start = vals[:V], vals[V:2 * V]
+    R = gs.n_ranks
+    base = np.zeros(R + 1, np.int64)
+    for r in range(R):
+        base[r + 1] = base[r] + gs.structs[gs.rank_struct[r]].n
+    total = int(base[-1])
+    vid = np.arange(total, dtype=np.int64)
+    inst_of = np.full(total, -1, np.int64)
+    for i in range(gs.n_inst):
+        for j in range(int(gs.inst_mem_off[i]), int(gs.inst_mem_off[i + 1])):
+            g_ = base[gs.inst_mem_rank[j]] + gs.inst_mem_node[j]
+            vid[g_], inst_of[g_] = total + i, i
+    send_of = {}
+    for m in range(len(gs.msg_bytes) if gs.msg_bytes is not None else 0):
+        send_of[int(base[gs.msg_recv_rank[m]] + gs.msg_recv_node[m])] = int(base[gs.msg_send_rank[m]] + gs.msg_send_node[m])
+    rank_of = np.repeat(np.arange(R), np.diff(base))
+    key = lambda g_: (int(gs.rank_values[rank_of[g_]]), int(gs.structs[gs.rank_struct[rank_of[g_]]].node_id[g_ - base[rank_of[g_]]]))
+
+    def deps(g_):
+        r = int(rank_of[g_])
+        members = ([int(base[gs.inst_mem_rank[j]] + gs.inst_mem_node[j])
+                    for j in range(int(gs.inst_mem_off[inst_of[g_]]), int(gs.inst_mem_off[inst_of[g_] + 1]))]
+                   if inst_of[g_] >= 0 else [g_])
+        out = []
+        for m_ in members:
+            rm = int(rank_of[m_])
+            st_ = gs.structs[gs.rank_struct[rm]]
+            k = m_ - int(base[rm])
+            out.extend(int(base[rm]) + int(q) for q in st_.pred_idx[st_.pred_off[k]:st_.pred_off[k + 1]])
+        return out
+
+    cand = [g_ for g_ in range(total)]
+    if not cand:
+        return 0, []
+    sink = min(cand, key=lambda g_: (-int(finish[vid[g_]]), key(g_)))
+    path = [sink]
+    while True:
+        cur = path[-1]
+        s0 = int(start[vid[cur]])
+        hit = [d for d in deps(cur) if int(finish[vid[d]]) == s0]
+        if hit:
+            path.append(min(hit, key=key))
+        elif cur in send_of:
+            path.append(send_of[cur])
+        else:
+            break
+    return int(cp[0]), [key(g_) for g_ in reversed(path)]
+
+
 def simulate_batch(graphs, points: DesignPoints, device: int = 0, engine: Optional[Engine] = None) -> dict:
     """One graph set x N design points -> sweep rows (cli.py:319-342, batched).
 

@@ -463,5 +463,7 @@ def merged_cp_graph(gs: GraphSet):
     poff = np.zeros(V + 1, np.int32)
     poff[1:] = np.cumsum([len(p) for p in preds])
     pidx = np.fromiter((u for p in preds for u in sorted(p)), np.int32, count=int(poff[-1]))
-    return dict(n_vert=V, order=np.asarray(order, np.int32), vkind=vkind, va=va, vb=vb, vsend=vsend,
+    # n_vert entries: vertices of collective members' own (rank, node) slots are unused, -1 pads
+    order = np.asarray(order + [-1] * (V - len(order)), np.int32)
+    return dict(n_vert=V, order=order, vkind=vkind, va=va, vb=vb, vsend=vsend,
                 vmsg=vmsg, pred_off=poff, pred_idx=pidx)

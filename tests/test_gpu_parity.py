@@ -294,3 +294,44 @@ def test_engine_cluster_8192_ranks_vs_oracle():
     flat = O.flatten(gs)
     for i, (spec, algo) in enumerate(specs):
         assert {k: int(out[k][i]) for k in ROW_KEYS} == O.sweep_row(gs, parse_topology(spec), algo, flat=flat), spec
+
+
+# ---- critical-path node trace (the path rule is documented at engine.critical_path_trace) ----
+
+def _trace_both(gs, topo, algo):
+    try:
+        want = O.critical_path_trace(gs, topo, algo)
+    except O.OracleError as e:
+        want = e.kind
+    try:
+        got = E.critical_path_trace(gs, topo, algo)
+    except EngineError:
+        raise
+    except Exception as e:
+        got = type(e).__name__
+    return got, want
+
+
+@pytest.mark.parametrize("seed", range(120))
+def test_critical_path_trace_random_vs_oracle(seed):
+    gs, topo = random_graphs(seed)
+    for algo in ("ring", "tree"):
+        got, want = _trace_both(gs, topo, algo)
+        assert got == want, (seed, algo)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_critical_path_trace_p2p_vs_oracle(seed):
+    from randgraphs import random_p2p_graphs
+    gs, topo = random_p2p_graphs(seed, mesh=seed % 2 == 1)
+    got, want = _trace_both(gs, topo, "ring")
+    assert got == want, seed
+
+
+@pytest.mark.parametrize("spec,algo", [("switch:64:50GB:2us", "ring"), ("mesh:8x8:100GB:500ns", "mesh-hier")])
+def test_critical_path_trace_fsdp_vs_oracle(spec, algo):
+    gs = synth.synth_transformer(synth.PRESETS["llama-8b-like"], synth.ParallelConfig(synth.Strategy.FSDP, 64), 64)
+    got, want = _trace_both(gs, parse_topology(spec), algo)
+    assert got == want
+    length, path = got
+    assert length == E.critical_path(gs, parse_topology(spec), algo) and len(path) > 1

@@ -90,3 +90,22 @@ def test_oracle_c3_north_star_points(row):
     gs = synth.synth_transformer(synth.PRESETS["llama-8b-like"], synth.ParallelConfig(synth.Strategy.FSDP, 1024), 1024)
     got = O.sweep_row(gs, parse_topology(row["spec"]), row["algo"])
     assert {k: got[k] for k in ROW_KEYS} == {k: row[k] for k in ROW_KEYS}
+
+
+def test_critical_path_trace_is_a_tight_chain():
+    """The oracle's node trace: a dependency chain whose finishes add up to the length
+    (each step's start is its predecessor's finish, or a SEND's finish plus the wire)."""
+    from oracle import pyoracle as O
+    from paper_2604_17550_b200 import synth
+    from paper_2604_17550_b200.topology import parse_topology
+    gs = synth.synth_transformer(synth.PRESETS["tiny"], synth.ParallelConfig(synth.Strategy.FSDP, 8), 8)
+    for spec, algo in [("switch:8:25GB:2us", "ring"), ("mesh:2x4:100GB:1us", "mesh-hier")]:
+        topo = parse_topology(spec)
+        length, path = O.critical_path_trace(gs, topo, algo)
+        assert length == O.critical_path(gs, topo, algo)
+        nodes = {(g.rank, n.node_id): n for g in gs for n in g.nodes}
+        for (ra, a), (rb, b) in zip(path, path[1:]):
+            nb = nodes[(rb, b)]
+            same_rank_dep = ra == rb and a in set(nb.dep_ids())
+            coll_dep = nb.coll is not None and ra in nb.coll.group
+            assert same_rank_dep or coll_dep, ((ra, a), (rb, b))

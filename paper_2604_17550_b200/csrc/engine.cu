@@ -139,6 +139,9 @@ constexpr int64_t TINF = INT64_MAX;
 constexpr uint64_t KINF = ~0ull;
 
 struct Shared {
+    alignas(16) uint64_t xbuf[2][16][2];   // cluster step exchange: {min key, completions} per CTA (st.async)
+    unsigned long long xmbar[2];    // their mbarriers
+    int cflag;                      // a rank of this CTA completed a collective / message since the last exchange
     uint64_t red[2][32];
     int64_t redi[2][32];
     int64_t cend_all;               // every rank's comm stream ends here (valid iff cend_uniform)
@@ -237,6 +240,52 @@ __device__ __forceinline__ int gor(int v, Shared &sh, int &par) {
     cl.sync();
     int m = 0;
     for (int j = 0; j < n; j++) m |= sh.xvor[q][j];
+    return m;
+}
+
+// The per-step reduction of a cluster without cluster.sync: cluster.sync is a
+// MEMBAR.ALL.GPU + CCTL.IVALL (it invalidates L1, so every step would re-read the node
+// records from L2).  Each CTA st.async's its {block min, completion flag} into every
+// CTA's exchange slot, which completes a transaction count on that CTA's mbarrier;
+// waiting on the local mbarrier (acquire, CTA scope) makes all slots visible.  Steps
+// in which some rank completed a collective or message then take a full cluster
+// barrier before the reservation reads the shared instance state in HBM.
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint64_t cl_step_min(uint64_t v, int &any, Shared &sh, int &par, unsigned &xk) {
+    v = block_min_u64(v, sh, par);              // (its barrier also orders this CTA's pops before cflag)
+    const int p = xk & 1;
+    const unsigned ph = (xk >> 1) & 1;
+    xk++;
+    cg::cluster_group cl = cg::this_cluster();
+    const unsigned n = cl.num_blocks(), me = cl.block_rank();
+    const unsigned mb = smem_u32(&sh.xmbar[p]);
+    if (threadIdx.x == 0) {
+        const unsigned long long f = (unsigned long long)sh.cflag;
+        sh.cflag = 0;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(16u * n) : "memory");
+        const unsigned slot = smem_u32(&sh.xbuf[p][me][0]);
+        for (unsigned j = 0; j < n; j++) {
+            unsigned ra, rmb;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(slot), "r"(j));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rmb) : "r"(mb), "r"(j));
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];"
+                         ::"r"(ra), "l"(v), "l"(f), "r"(rmb) : "memory");
+        }
+    }
+    unsigned done;
+    do {
+        asm volatile("{ .reg .pred q; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 q, [%1], %2; "
+                     "selp.u32 %0, 1, 0, q; }" : "=r"(done) : "r"(mb), "r"(ph) : "memory");
+    } while (!done);
+    uint64_t m = KINF;
+    int a = 0;
+    for (unsigned j = 0; j < n; j++) {
+        const uint64_t x = sh.xbuf[p][j][0];
+        m = x < m ? x : m;
+        a |= (int)sh.xbuf[p][j][1];
+    }
+    any = a;
     return m;
 }
 
@@ -568,7 +617,10 @@ __device__ __forceinline__ void dispatch(const DevGraph &g, const Ctx &c, const 
                                            ((unsigned long long)s.pop_seq << 12) | (unsigned long long)seq;
             atomicMax(&c.msg_ckey[m], key);
         }
-        if (atomicSub(&c.msg_wait[m], 1) == 1) c.mcomplist[atomicAdd(c.nmcomp, 1)] = m;
+        if (atomicSub(&c.msg_wait[m], 1) == 1) {
+            c.mcomplist[atomicAdd(c.nmcomp, 1)] = m;
+            if (K & 16) reinterpret_cast<Shared *>(fl_smem)->cflag = 1;
+        }
         return;
     }
     if (kind == FL_COLL) {
@@ -583,7 +635,10 @@ __device__ __forceinline__ void dispatch(const DevGraph &g, const Ctx &c, const 
             atomicMax((unsigned long long *)&c.inst_cpmax[i], cm);
             if (!f.init) atomicMax(&c.inst_ckey[i], km);
             const int cnt = __popc(grp);
-            if (atomicSub(&c.inst_wait[i], cnt) == cnt) c.complist[atomicAdd(c.ncomp, 1)] = i;
+            if (atomicSub(&c.inst_wait[i], cnt) == cnt) {
+                c.complist[atomicAdd(c.ncomp, 1)] = i;
+                if (K & 16) reinterpret_cast<Shared *>(fl_smem)->cflag = 1;
+            }
         }
         return;
     }
@@ -941,7 +996,7 @@ __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o,
                                           int64_t t, bool init, int cfg, uint64_t epoch,
                                           int nc, int nmc, int topo, int cols) {
     int64_t cpm = 0;
-    if (nc > 1 || CL) {             // one thread orders the list (shared by the cluster's CTAs)
+    if (nc > 1) {                   // one thread orders the list (shared by the cluster's CTAs)
         if ((!CL || c.lead_cta) && threadIdx.x == 0) {
             for (int a = 1; a < nc; a++) {
                 const int x = c.complist[a];
@@ -1005,6 +1060,7 @@ __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o,
     if (threadIdx.x == 0) {
         sh.cend_uniform = uni;
         sh.cend_all = cend;
+        sh.cflag = 0;
     }
     if ((!CL || c.lead_cta) && threadIdx.x == 0) {
         if (CL) *c.ncomp = 0; else sh.ncomp = 0;
@@ -1131,7 +1187,13 @@ __global__ void __launch_bounds__(1024, 1)
     const int my_n = active ? g.s_node_off[g.rank_struct[L.r] + 1] - L.nb : 0;
 
     int par = 0;
-    if (tid == 0) { sh.parity = 0; sh.ncomp = 0; sh.nmcomp = 0; sh.flag = 0; }
+    unsigned xk = 0;                // cluster step exchanges done (cl_step_min)
+    if (tid == 0) { sh.parity = 0; sh.ncomp = 0; sh.nmcomp = 0; sh.flag = 0; sh.cflag = 0; }
+    if (CL && tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sh.xmbar[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sh.xmbar[1])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     if (CL && is_leader) { c.ncomp[0] = 0; c.nmcomp[0] = 0; }
     // the global bitmaps are all-zero after a point that ran to completion;
     // clear them once up front and again only after a point that did not
@@ -1314,18 +1376,22 @@ __global__ void __launch_bounds__(1024, 1)
             int64_t nt = active ? next_time(g, c, L, s, tcur) : TINF;
             uint64_t key = nt == TINF ? KINF : ((uint64_t)(nt < TCAP ? nt : TCAP) << 14) | (uint64_t)L.r;
             PROF_MARK(1);                                   // next_time + key
-            uint64_t kmin = gmin_key<CL>(key, sh, par);
+            int any = 0;
+            uint64_t kmin = CL ? cl_step_min(key, any, sh, par, xk) : gmin_key<CL>(key, sh, par);
             PROF_MARK(2);                                   // step reduction (incl. barrier wait)
             // collectives completed by the previous step's pops: reserve them now (the
-            // reduction's barrier made every arrival visible), then re-derive the next time
-            const int nc = CL ? *c.ncomp : sh.ncomp, nmc = MSG ? (CL ? *c.nmcomp : sh.nmcomp) : 0;
+            // reduction's barrier made every arrival visible -- in a cluster, the full
+            // barrier taken here), then re-derive the next time
+            if (CL && any) gsync<CL>();
+            const int nc = CL ? (any ? *c.ncomp : 0) : sh.ncomp;
+            const int nmc = MSG ? (CL ? (any ? *c.nmcomp : 0) : sh.nmcomp) : 0;
             if (nc | nmc) {
                 reserve_n<MSG, CL, K>(g, o, c, sh, par, tcur, false, cfg, f.epoch, nc, nmc,
                                                      topo, p.cols[cfg]);
                     if (active) refresh_ring(c, L, s);
                 nt = active ? next_time(g, c, L, s, tcur) : TINF;
                 key = nt == TINF ? KINF : ((uint64_t)(nt < TCAP ? nt : TCAP) << 14) | (uint64_t)L.r;
-                kmin = gmin_key<CL>(key, sh, par);
+                kmin = CL ? cl_step_min(key, any, sh, par, xk) : gmin_key<CL>(key, sh, par);
             }
             if (kmin == KINF) break;
             const int64_t t = (int64_t)(kmin >> 14);

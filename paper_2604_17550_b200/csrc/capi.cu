@@ -377,7 +377,6 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     off = align_up(off + (size_t)d->n_msg * 8 * 8 + (size_t)sc.link_cap * 16 + (size_t)d->n_msg * 8 +
                        (size_t)R * 4 + 2 * (size_t)dg.p2p_stride * R * 4 + 64, 256);
     sc.off_ctr = off;  off = align_up(off + 64, 256);
-    sc.off_prf = off;  off = align_up(off + fl::sweep_global_bytes_per_rank() * (size_t)fl::sweep_plane_lanes(g->block, CS) * CS, 256);
     sc.slot_bytes = off;
 
     // shared memory: header | comm_end, stats, ring tails | [instances] | [durations] | [done bitmap]

@@ -154,7 +154,6 @@ struct Shared {
     uint64_t xkmin[2][16];
     int64_t xvmax[2][16];
     int xvor[2][16];
-    int64_t *prg;                   // per-rank fields F_NSM.. in this CTA's HBM scratch
 };
 
 // Warp min of keys (time << 14 | rank).  Ranks step in lockstep most of the
@@ -343,10 +342,9 @@ constexpr uint64_t VAL48 = (1ull << 48) - 1;
 //   on a stream, carried along with it so that popping a node needs no HBM read;
 //   a node that overflows a set's head into its bitmap parks the value in the
 //   node's accumulator word instead (simulator.py:449-453 values, see below).
-// Hottest first: the first F_NSM fields are in shared memory, the rest in this CTA's
-// HBM scratch (same layout, L1-cached).  The plane stride is the compile-time
-// maximum block size, so a field access is one LDS/LD at an immediate offset from
-// the lane's own address.
+// Shared-memory planes, one per field.  The plane stride is a compile-time constant,
+// so a field access is one LDS/STS at an immediate offset from the lane's own address
+// (A/B: keeping the colder fields in HBM instead cost 9%).
 enum {
     F_DUE_CP = 0, F_RC_CP, F_OCC_CP,                // heads of the due / ready-compute sets, running compute node
     F_COMM_END,                                     // end of this rank's comm stream (FIFO tail)
@@ -357,10 +355,6 @@ enum {
     F_N64
 };
 enum { F_DUE_SUM = -1, F_RC_SUM = -1, F_RH_SUM = -1 };   // (sets keep no summaries: see MinSet)
-#ifndef FL_NSM
-#define FL_NSM F_N64
-#endif
-constexpr int F_NSM = FL_NSM;
 // Plane stride (lanes), a compile-time constant per kernel variant: bits 5-6 of the
 // variant word K select 1024 (0), 256 (1) or 64 (2), the smallest that holds the block,
 // so small design points keep many CTAs per SM.
@@ -372,13 +366,12 @@ constexpr unsigned SM_HDR = (sizeof(Shared) + 15) / 16 * 16;
 template <int K>
 __device__ __forceinline__ int64_t &F64(int k, int lr) {
     constexpr int SR = plane_lanes<K>();
-    if (k < F_NSM) return reinterpret_cast<int64_t *>(fl_smem + SM_HDR)[k * SR + lr];
-    return reinterpret_cast<Shared *>(fl_smem)->prg[(k - F_NSM) * SR + lr];
+    return reinterpret_cast<int64_t *>(fl_smem + SM_HDR)[k * SR + lr];
 }
 template <int K>
 __device__ __forceinline__ int32_t &F32(int k, int lr) {
     constexpr int SR = plane_lanes<K>();
-    return reinterpret_cast<int32_t *>(fl_smem + SM_HDR + (size_t)F_NSM * 8 * SR)[k * SR + lr];
+    return reinterpret_cast<int32_t *>(fl_smem + SM_HDR + (size_t)F_N64 * 8 * SR)[k * SR + lr];
 }
 
 // Per-CTA (block-uniform) state pointers.  Bitmaps are word-major,
@@ -1148,7 +1141,6 @@ __global__ void __launch_bounds__(1024, 1)
         c.nmcomp = CL ? ctr + 1 : &sh.nmcomp;
         c.lead_cta = crank == 0;
         c.touch = sc.touch_in_smem;
-        sh.prg = reinterpret_cast<int64_t *>(base + sc.off_prf) + (size_t)crank * (F_N64 - F_NSM) * plane_lanes<K>();
         const int M = g.n_msg;
         int64_t *mb = reinterpret_cast<int64_t *>(base + sc.off_msg);
         c.msg_sendt = mb;
@@ -1664,8 +1656,7 @@ cudaError_t sweep_set_smem(size_t smem) {
 }
 
 size_t sweep_shared_header_bytes() { return SM_HDR; }
-size_t sweep_shared_bytes_per_rank() { return 8 * F_NSM + 4 * Q_N32; }   // x plane lanes
-size_t sweep_global_bytes_per_rank() { return 8 * (F_N64 - F_NSM); }
+size_t sweep_shared_bytes_per_rank() { return 8 * F_N64 + 4 * Q_N32; }   // x plane lanes
 int sweep_plane_lanes(int block, int cluster) { return cluster > 1 ? 1024 : plane_lanes_for(block); }
 
 cudaError_t launch_cp(const DevGraph &g, const DevPoints &p, int nv, const int32_t *order, const int32_t *vkind,

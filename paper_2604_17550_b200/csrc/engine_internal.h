@@ -64,7 +64,6 @@ struct DevScratch {
     // dynamic shared-memory layout (bytes from the start of the CTA's smem)
     size_t off_msg;              // message state, link state, per-rank in-flight lists
     size_t off_ctr;              // cluster-wide completion counters
-    size_t off_prf;              // per-rank fields kept in HBM (engine.cu F_NSM..), one block per CTA
     int link_cap;
     unsigned sm_off_dyn, sm_off_done, sm_off_dur, sm_off_inst, sm_off_touch;
     int done_in_smem, dur_in_smem, inst_in_smem, touch_in_smem;
@@ -76,7 +75,6 @@ cudaError_t sweep_occupancy(int block, size_t smem, int cluster, int *occ);
 cudaError_t sweep_set_smem(size_t smem);
 size_t sweep_shared_header_bytes();
 size_t sweep_shared_bytes_per_rank();   // the [field][blockDim] per-rank planes
-size_t sweep_global_bytes_per_rank();
 int sweep_plane_lanes(int block, int cluster);   // per-rank planes are this many lanes wide
 cudaError_t launch_cp(const DevGraph &g, const DevPoints &p, int nv, const int32_t *order, const int32_t *vkind,
                       const int32_t *va, const int32_t *vb, const int32_t *vsend, const int32_t *vmsg,

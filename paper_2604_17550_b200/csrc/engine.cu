@@ -360,7 +360,10 @@ enum { F_DUE_SUM = -1, F_RC_SUM = -1, F_RH_SUM = -1 };   // (sets keep no summar
 // so small design points keep many CTAs per SM.
 template <int K> __host__ __device__ constexpr int plane_lanes() { return ((K >> 5) & 3) == 0 ? 1024 : ((K >> 5) & 3) == 1 ? 256 : 64; }
 constexpr int FL_SR = 1024;                         // widest plane (HBM fallback fields, capacity)
-enum { Q_RING_TAIL = 0, Q_RING_HEAD, Q_RING_SEEN, Q_HEAD_NODE, Q_HEAD_INST, Q_DONE, Q_N32 };
+enum { Q_RING_TAIL = 0, Q_RING_HEAD, Q_RING_SEEN, Q_HEAD_NODE, Q_HEAD_INST, Q_DONE,
+       Q_N32,                       // (the planes above are cleared per design point)
+       Q_NB = Q_N32, Q_TB, Q_MYN,   // per CTA: the rank's first node / tensor in the graph set, its node count
+       Q_ALL };
 
 constexpr unsigned SM_HDR = (sizeof(Shared) + 15) / 16 * 16;
 template <int K>
@@ -1167,16 +1170,20 @@ __global__ void __launch_bounds__(1024, 1)
 
     const bool active = tid < RL;
     Lane L;
-    L.r = active ? base_r + tid : base_r;
+    L.r = base_r + tid;             // (inactive lanes never index per-rank state with it)
     L.lr = tid;
     L.br = sc.touch_in_smem ? tid : L.r;
     L.dr = sc.done_in_smem ? tid : L.r;
     {
-        const int st = g.rank_struct[L.r];
-        L.nb = g.s_node_off[st];
-        L.tb = g.s_tens_off[st];
+        // kept in shared memory: re-reading them there is cheaper than the two dependent
+        // global loads the compiler would otherwise repeat under register pressure
+        const int st = active ? g.rank_struct[L.r] : 0;
+        F32<K>(Q_NB, tid) = g.s_node_off[st];
+        F32<K>(Q_TB, tid) = g.s_tens_off[st];
+        F32<K>(Q_MYN, tid) = active ? g.s_node_off[st + 1] - g.s_node_off[st] : 0;
+        L.nb = F32<K>(Q_NB, tid);
+        L.tb = F32<K>(Q_TB, tid);
     }
-    const int my_n = active ? g.s_node_off[g.rank_struct[L.r] + 1] - L.nb : 0;
 
     int par = 0;
     unsigned xk = 0;                // cluster step exchanges done (cl_step_min)
@@ -1448,7 +1455,7 @@ __global__ void __launch_bounds__(1024, 1)
 #endif
 
         // ---- row: reductions over ranks (cli.py:336-341) ----
-        int dead = active && F32<K>(Q_DONE, tid) != my_n;
+        int dead = active && F32<K>(Q_DONE, tid) != F32<K>(Q_MYN, tid);
         dead = gor<CL>(dead | overflow, sh, par);
         dirty = dead != 0;
         int64_t vals[6] = {0, 0, 0, 0, 0, 0};
@@ -1656,7 +1663,7 @@ cudaError_t sweep_set_smem(size_t smem) {
 }
 
 size_t sweep_shared_header_bytes() { return SM_HDR; }
-size_t sweep_shared_bytes_per_rank() { return 8 * F_N64 + 4 * Q_N32; }   // x plane lanes
+size_t sweep_shared_bytes_per_rank() { return 8 * F_N64 + 4 * Q_ALL; }   // x plane lanes
 int sweep_plane_lanes(int block, int cluster) { return cluster > 1 ? 1024 : plane_lanes_for(block); }
 
 cudaError_t launch_cp(const DevGraph &g, const DevPoints &p, int nv, const int32_t *order, const int32_t *vkind,

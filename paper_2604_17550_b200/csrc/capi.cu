@@ -390,6 +390,7 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     if (sc.inst_in_smem) { sc.sm_off_inst = (unsigned)sm; sm = align_up(sm + inst_bytes, 16); }
     sc.dur_in_smem = sm + dur_bytes <= budget;
     if (sc.dur_in_smem) { sc.sm_off_dur = (unsigned)sm; sm = align_up(sm + dur_bytes, 16); }
+    dg.dur_sm_off = sc.dur_in_smem ? sc.sm_off_dur : 0;
     sc.done_in_smem = dg.needs_done && sm + sbits <= budget;
     if (sc.done_in_smem) { sc.sm_off_done = (unsigned)sm; sm = align_up(sm + sbits, 16); }
 #ifdef FL_NO_TOUCH

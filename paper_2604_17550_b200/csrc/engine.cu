@@ -409,6 +409,12 @@ struct Ctx {
     int32_t *mcount;                // shared [R]
 };
 
+// This design point's duration of node n: an LDS when the durations are in shared memory
+// (g.dur_sm_off), else through the CTA's HBM copy.
+__device__ __forceinline__ int64_t dur_of(const DevGraph &g, const Ctx &c, int n) {
+    return g.dur_sm_off ? reinterpret_cast<const int64_t *>(fl_smem + g.dur_sm_off)[n] : c.dur[n];
+}
+
 constexpr int32_t MSG_ALLOC = 1 << 30;   // mlist entry flag: the endpoint's outputs are allocated
 
 // Per-thread rank identity: element w of rank r in a [w][R] array is at w * R + r.
@@ -535,11 +541,11 @@ __device__ __forceinline__ void record(const DevGraph &g, const DevOut &o, int c
 template <int K>
 __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, const Ctx &c, const Lane &L,
                                             Rank<K> &s, const Step &f, int64_t t, int cfg) {
-    const int R = c.R;
+    const int R = g.R;                      // (a kernel parameter: no shared-memory load)
     while (s.rh.head >= 0 && s.host_n < 0) {      // the host stream is free at t (gather_due ran at t)
         int64_t v;
         const int h = ms_pop_cp<K, F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, v, g.max_words);
-        const int64_t e = t + c.dur[L.nb + h];
+        const int64_t e = t + dur_of(g, c, L.nb + h);
         { const uint4 hb = rec_b(g, L.nb + h); F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
         record(g, o, cfg, L.r, h, t, e);
         if (e == t) {
@@ -564,7 +570,7 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
         }
         int64_t v;
         const int x = ms_pop_cp<K, F_RC_CP, F_RC_SUM>(s.rc, c.rdyc, c.cp, R, L, v, g.max_words);
-        const int64_t e = t + c.dur[L.nb + x];
+        const int64_t e = t + dur_of(g, c, L.nb + x);
         { const uint4 xb = rec_b(g, L.nb + x); F64<K>(F_ALLOC, L.lr) += rec_u64(xb.z, xb.w); }
         record(g, o, cfg, L.r, x, t, e);
         if ((K & 7) == 1 && e > t) {      // one compute stream: its busy intervals are disjoint
@@ -602,7 +608,7 @@ __device__ __forceinline__ unsigned long long group_max_u64(unsigned grp, unsign
 template <int K>
 __device__ __forceinline__ void dispatch(const DevGraph &g, const Ctx &c, const Lane &L, Rank<K> &s,
                                          const Step &f, int d, const uint4 &rb, int64_t cps, int seq, int64_t t) {
-    const int R = c.R;
+    const int R = g.R;                      // (a kernel parameter: no shared-memory load)
     const int kind = rec_kind(rb);
     if ((K & 8) && kind >= FL_SEND) {   // simulator.py:259-268: the message is granted once both ends are ready
         const int m = g.rank_p2p_msg[L.r * g.p2p_stride + (int)rb.y];
@@ -638,7 +644,7 @@ __device__ __forceinline__ void dispatch(const DevGraph &g, const Ctx &c, const 
         }
         return;
     }
-    const int64_t fin = cps + c.dur[L.nb + d];
+    const int64_t fin = cps + dur_of(g, c, L.nb + d);
     if (kind == FL_COMP) ms_insert_cp<K, F_RC_CP, F_RC_SUM>(s.rc, c.rdyc, c.cp, R, L, d, fin);
     else ms_insert_cp<K, F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, d, fin);
 }
@@ -648,7 +654,7 @@ __device__ __forceinline__ void dispatch(const DevGraph &g, const Ctx &c, const 
 template <int K>
 __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const Lane &L, Rank<K> &s,
                                           const Step &f, int x, int64_t fx64, int64_t t) {
-    const int R = c.R;
+    const int R = g.R;                      // (a kernel parameter: no shared-memory load)
     const uint4 xa = rec_a(g, L.nb + x);
     if (g.needs_done) done_ref<K>(c, L, R, x >> 6) |= 1ull << (x & 63);
     F32<K>(Q_DONE, L.lr)++;
@@ -728,11 +734,11 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
 constexpr int64_t HS_ALLOC = INT64_MIN;   // head_s once the head's outputs are allocated (it started)
 
 template <int K>
-__device__ __forceinline__ void load_head(const Ctx &c, const Lane &L, Rank<K> &s) {
+__device__ __forceinline__ void load_head(const Ctx &c, const Lane &L, Rank<K> &s, int R) {
     const int h = F32<K>(Q_RING_HEAD, L.lr);
     if (h < F32<K>(Q_RING_SEEN, L.lr)) {
-        const int i = c.ring_inst[h * c.R + L.r];
-        F32<K>(Q_HEAD_NODE, L.lr) = c.ring_node[h * c.R + L.r];
+        const int i = c.ring_inst[h * R + L.r];
+        F32<K>(Q_HEAD_NODE, L.lr) = c.ring_node[h * R + L.r];
         F32<K>(Q_HEAD_INST, L.lr) = i;
         s.head_s = c.inst_s[i];
         s.head_e = c.inst_e[i];
@@ -789,7 +795,7 @@ __device__ __forceinline__ int64_t next_time(const DevGraph &g, const Ctx &c, co
 template <int K>
 __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, const Lane &L, Rank<K> &s,
                                            int64_t t) {
-    const int R = c.R;
+    const int R = g.R;                      // (a kernel parameter: no shared-memory load)
     if (s.host_n >= 0 && F64<K>(F_HOST_E, L.lr) == t) {
         ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, s.host_n, F64<K>(F_HOST_CP, L.lr));
         s.host_n = -1;
@@ -809,7 +815,7 @@ __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, cons
         // (simulator.py:419-428)
         ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, hn, c.inst_cpmax[hi] + c.inst_dur[hi]);
         F32<K>(Q_RING_HEAD, L.lr)++;
-        load_head(c, L, s);
+        load_head(c, L, s, R);
     }
     if (K & 8) {
         int n = c.mcount[L.r], k = 0;
@@ -835,7 +841,7 @@ __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, cons
 template <int K>
 __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const Lane &L, Rank<K> &s,
                                         int64_t tcur, int64_t tnew) {
-    const int R = c.R;
+    const int R = g.R;                      // (a kernel parameter: no shared-memory load)
     const bool head = s.head_e != TINF;
     if (head && s.head_s != HS_ALLOC && s.head_s <= tcur) {   // a collective that started by tcur
         const uint4 hb = rec_b(g, L.nb + F32<K>(Q_HEAD_NODE, L.lr));
@@ -937,7 +943,7 @@ __device__ __forceinline__ int64_t transfer_ns(const DevGraph &g, int topo, int 
 // every link on its route for the whole transfer.
 static __device__ void reserve_msgs(const DevGraph &g, const DevOut &o, const Ctx &c, int nm, bool init, int topo,
                              int cols, int cfg, uint64_t epoch, int64_t &cpm) {
-    const int R = c.R;
+    const int R = g.R;                      // (a kernel parameter: no shared-memory load)
     for (int a = 1; a < nm; a++) {
         const int x = c.mcomplist[a];
         int b = a - 1;
@@ -1003,7 +1009,7 @@ __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o,
         }
         gsync<CL>();
     }
-    const int R = c.R, RL = CL ? c.RL : c.R, base = CL ? c.base : 0;
+    const int R = g.R, RL = CL ? c.RL : g.R, base = CL ? c.base : 0;
     // While every collective so far spanned all ranks, every comm stream ends at the
     // same time and a full-world reservation needs no reduction (simulator.py:300-303).
     bool uni = sh.cend_uniform;

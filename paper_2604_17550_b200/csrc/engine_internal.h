@@ -32,6 +32,7 @@ struct DevGraph {
     int needs_done;              // some tensor's last consumer is only known at run time
     const int32_t *s_nstatic, *trig_off, *static_off, *static_list;
     const int4 *trig;            // {trigger host, node, position in the host's dependents, -}
+    unsigned dur_sm_off;         // per-point durations in shared memory at this offset (0: HBM, per CTA)
     const int32_t *s_init_ns_off, *init_ns;   // initial dispatch list without static hosts
     const int32_t *succ_ent;     // succ_idx | edge class << 16 (FL_EDGE_*, valid when static hosts are folded)
     // messages

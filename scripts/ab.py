@@ -39,7 +39,13 @@ def child(name, workload, points, reps):
             side -= 1
         w.points.rows[:] = np.where(w.points.rows > 0, side, 0)
         w.points.cols[:] = np.where(w.points.cols > 0, ranks // side, 0)
-    graphs = S.workload_graphs(w)
+    if os.environ.get("AB_FSDP_NONE"):      # the same grid on the fsdp NONE family (counted dependencies)
+        from paper_2604_17550_b200 import synth as SY
+        p = SY.parse_parallel(w.parallel)
+        graphs = SY.synth_transformer(SY.PRESETS[w.model], SY.ParallelConfig(p.strategy, p.degree, SY.FsdpMode.NONE),
+                                      p.degree)
+    else:
+        graphs = S.workload_graphs(w)
     n_all = len(w.points)
     if points and points < n_all:
         w.points = w.points.take(np.linspace(0, n_all - 1, points).round().astype(np.int64))

@@ -335,3 +335,23 @@ def test_critical_path_trace_fsdp_vs_oracle(spec, algo):
     assert got == want
     length, path = got
     assert length == E.critical_path(gs, parse_topology(spec), algo) and len(path) > 1
+
+
+def test_engine_c3_full_grid_vs_oracle():
+    """BASELINE config 3 in full -- 4096 design points x 1024 ranks x 832 nodes in one
+    launch -- every row bit-exact against the CPU oracle's (tests/golden/make_c3_grid.py),
+    plus the reference's own invariants (critical path <= makespan, test_simulator.py:275-295;
+    exposed comm <= comm busy; busy times <= makespan)."""
+    from pathlib import Path
+    from paper_2604_17550_b200 import sweep as S
+    w = S.c3_workload()
+    gs = S.workload_graphs(w)
+    out = E.simulate_batch(gs, w.points)
+    assert (out["status"] == 0).all()
+    got = np.stack([np.asarray(out[k], np.int64) for k in ROW_KEYS], 1)
+    fx = np.load(Path(__file__).parent / "golden" / "c3_grid_rows.npz")
+    assert list(fx["fields"]) == list(ROW_KEYS)
+    bad = np.nonzero((got != fx["rows"]).any(1))[0]
+    assert bad.size == 0, (bad[:5], got[bad[:2]], fx["rows"][bad[:2]])
+    mk, cp = got[:, 0], got[:, 1]
+    assert (cp <= mk).all() and (got[:, 4] <= got[:, 3]).all() and (got[:, 2] <= mk).all() and (got[:, 3] <= mk).all()

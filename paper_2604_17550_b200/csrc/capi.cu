@@ -369,6 +369,7 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     sc.off_ring = off; off = align_up(off + 2 * (size_t)dg.coll_stride * R * 4, 256);
     sc.off_dur = off;  off = align_up(off + dur_bytes * CS, 256);      // one copy per CTA of a cluster
     sc.off_inst = off; off = align_up(off + inst_bytes, 256);
+    sc.off_inst_se = off; off = align_up(off + 16 * (size_t)(d->n_inst > 0 ? d->n_inst : 1) * CS, 256);
     // links: switch eg/in per rank; mesh 4 per position (bounded by the largest rank id)
     int64_t maxv = 0;
     for (int r = 0; r < R; r++) maxv = d->rank_value[r] > maxv ? d->rank_value[r] : maxv;

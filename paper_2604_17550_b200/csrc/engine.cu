@@ -142,6 +142,7 @@ struct Shared {
     alignas(16) uint64_t xbuf[2][16][2];   // cluster step exchange: {min key, completions} per CTA (st.async)
     unsigned long long xmbar[2];    // their mbarriers
     int cflag;                      // a rank of this CTA completed a collective / message since the last exchange
+    int ncons;                      // cluster without messages: completion-list entries reserved so far
     uint64_t red[2][32];
     int64_t redi[2][32];
     int64_t cend_all;               // every rank's comm stream ends here (valid iff cend_uniform)
@@ -997,14 +998,19 @@ template <bool MSG, bool CL, int K>
 __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, const Ctx &c, Shared &sh, int &par,
                                           int64_t t, bool init, int cfg, uint64_t epoch,
                                           int nc, int nmc, int topo, int cols) {
+    // A cluster without messages never rewinds the completion list within a design point:
+    // this reservation's entries start at sh.ncons, so no barrier is needed before the
+    // counter could be reset (the instance times it writes are per-CTA copies).
+    constexpr bool MONO = CL && !MSG;
+    int32_t *const cl = c.complist + (MONO ? sh.ncons : 0);
     int64_t cpm = 0;
     if (nc > 1) {                   // one thread orders the list (shared by the cluster's CTAs)
         if ((!CL || c.lead_cta) && threadIdx.x == 0) {
             for (int a = 1; a < nc; a++) {
-                const int x = c.complist[a];
+                const int x = cl[a];
                 int b = a - 1;
-                while (b >= 0 && comp_before(g, c, x, c.complist[b], init)) { c.complist[b + 1] = c.complist[b]; b--; }
-                c.complist[b + 1] = x;
+                while (b >= 0 && comp_before(g, c, x, cl[b], init)) { cl[b + 1] = cl[b]; b--; }
+                cl[b + 1] = x;
             }
         }
         gsync<CL>();
@@ -1015,7 +1021,7 @@ __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o,
     bool uni = sh.cend_uniform;
     int64_t cend = sh.cend_all;
     for (int q = 0; q < nc; q++) {
-        const int i = c.complist[q];
+        const int i = cl[q];
         const int64_t m0 = g.inst_mem_off[i], nm = g.inst_mem_off[i + 1] - m0;
         const int full_node = g.inst_full_node[i];      // >= 0: members are ranks 0..R-1, all at this node
         int64_t s;
@@ -1035,7 +1041,7 @@ __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o,
         const int64_t e = s + c.inst_dur[i];
         const int64_t cpv = c.inst_cpmax[i] + c.inst_dur[i];
         cpm = cpv > cpm ? cpv : cpm;
-        if ((!CL || c.lead_cta) && threadIdx.x == 0) { c.inst_s[i] = s; c.inst_e[i] = e; }
+        if (threadIdx.x == 0) { c.inst_s[i] = s; c.inst_e[i] = e; }      // (each CTA its own copy)
         if (full_node >= 0) {
             for (int lm = threadIdx.x; lm < RL; lm += blockDim.x) {
                 const int m = base + lm;
@@ -1058,13 +1064,15 @@ __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o,
             gsync<CL>();            // the next reservation reads these comm ends
         }
     }
-    gsync<CL>();                    // every CTA has read the counters and the list
+    if (MONO) __syncthreads();      // this CTA has read sh.cend_* and sh.ncons
+    else gsync<CL>();               // every CTA has read the counters and the list
     if (threadIdx.x == 0) {
         sh.cend_uniform = uni;
         sh.cend_all = cend;
         sh.cflag = 0;
+        if (MONO) sh.ncons += nc;
     }
-    if ((!CL || c.lead_cta) && threadIdx.x == 0) {
+    if (!MONO && (!CL || c.lead_cta) && threadIdx.x == 0) {
         if (CL) *c.ncomp = 0; else sh.ncomp = 0;
         if (MSG && nmc) reserve_msgs(g, o, c, nmc, init, topo, cols, cfg, epoch, cpm);
         if (MSG) { if (CL) *c.nmcomp = 0; else sh.nmcomp = 0; }
@@ -1081,7 +1089,7 @@ __device__ __forceinline__ int64_t reserve(const DevGraph &g, const DevOut &o, c
                                            int64_t t, bool init, int cfg, uint64_t epoch,
                                            int topo, int cols) {
     gsync<CL>();
-    const int nc = CL ? *c.ncomp : sh.ncomp, nmc = MSG ? (CL ? *c.nmcomp : sh.nmcomp) : 0;
+    const int nc = CL ? *c.ncomp - (MSG ? 0 : sh.ncons) : sh.ncomp, nmc = MSG ? (CL ? *c.nmcomp : sh.nmcomp) : 0;
     return (nc | nmc) ? reserve_n<MSG, CL, K>(g, o, c, sh, par, t, init, cfg, epoch, nc, nmc, topo, cols) : 0;
 }
 
@@ -1142,6 +1150,10 @@ __global__ void __launch_bounds__(1024, 1)
         c.inst_s = c.inst_dur + NI;
         c.inst_e = c.inst_s + NI;
         c.inst_cpmax = c.inst_e + NI;
+        if (CL) {                   // reservation times: one copy per CTA, written and read locally
+            c.inst_s = reinterpret_cast<int64_t *>(base + sc.off_inst_se) + (size_t)crank * 2 * NI;
+            c.inst_e = c.inst_s + NI;
+        }
         c.inst_ckey = reinterpret_cast<unsigned long long *>(c.inst_cpmax + NI);
         c.inst_wait = reinterpret_cast<int32_t *>(c.inst_ckey + NI);
         c.complist = c.inst_wait + NI;
@@ -1226,9 +1238,8 @@ __global__ void __launch_bounds__(1024, 1)
             c.inst_cpmax[i] = 0;
             c.inst_ckey[i] = 0ull;
             c.inst_wait[i] = (int32_t)(g.inst_mem_off[i + 1] - g.inst_mem_off[i]);
-            c.inst_s[i] = 0;
-            c.inst_e[i] = 0;
         }
+        for (int i = tid; i < NI; i += bd) { c.inst_s[i] = 0; c.inst_e[i] = 0; }   // (per-CTA copies)
         if (K & 8) {                // messages: wire time per design point, fresh link state
             const double beta = __ddiv_rn(1e9, bwv);
             const int cols = p.cols[cfg];
@@ -1266,7 +1277,8 @@ __global__ void __launch_bounds__(1024, 1)
             else zero_cols<CL>(c.done, (size_t)g.max_words, R, base_r, RL);
         }
         if (sc.touch_in_smem) for (size_t i = tid; i < (size_t)g.max_words * bd; i += bd) c.touched[i] = 0;
-        if (tid == 0) { sh.cend_all = 0; sh.cend_uniform = 1; }
+        if (tid == 0) { sh.cend_all = 0; sh.cend_uniform = 1; sh.ncons = 0; }
+        if (CL && is_leader) *c.ncomp = 0;          // (MONO clusters: the list restarts per point)
 #pragma unroll
         for (int k = 0; k < F_N64; k++) F64<K>(k, tid) = 0;
 #pragma unroll
@@ -1388,7 +1400,7 @@ __global__ void __launch_bounds__(1024, 1)
             // reduction's barrier made every arrival visible -- in a cluster, the full
             // barrier taken here), then re-derive the next time
             if (CL && any) gsync<CL>();
-            const int nc = CL ? (any ? *c.ncomp : 0) : sh.ncomp;
+            const int nc = CL ? (any ? *c.ncomp - (MSG ? 0 : sh.ncons) : 0) : sh.ncomp;
             const int nmc = MSG ? (CL ? (any ? *c.nmcomp : 0) : sh.nmcomp) : 0;
             if (nc | nmc) {
                 reserve_n<MSG, CL, K>(g, o, c, sh, par, tcur, false, cfg, f.epoch, nc, nmc,

@@ -65,6 +65,7 @@ struct DevScratch {
     // dynamic shared-memory layout (bytes from the start of the CTA's smem)
     size_t off_msg;              // message state, link state, per-rank in-flight lists
     size_t off_ctr;              // cluster-wide completion counters
+    size_t off_inst_se;          // clusters: per-CTA copies of the instances' reservation start / end
     int link_cap;
     unsigned sm_off_dyn, sm_off_done, sm_off_dur, sm_off_inst, sm_off_touch;
     int done_in_smem, dur_in_smem, inst_in_smem, touch_in_smem;

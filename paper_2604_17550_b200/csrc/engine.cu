@@ -1238,8 +1238,9 @@ __global__ void __launch_bounds__(1024, 1)
             c.inst_cpmax[i] = 0;
             c.inst_ckey[i] = 0ull;
             c.inst_wait[i] = (int32_t)(g.inst_mem_off[i + 1] - g.inst_mem_off[i]);
+            if (!CL) { c.inst_s[i] = 0; c.inst_e[i] = 0; }
         }
-        for (int i = tid; i < NI; i += bd) { c.inst_s[i] = 0; c.inst_e[i] = 0; }   // (per-CTA copies)
+        if (CL) for (int i = tid; i < NI; i += bd) { c.inst_s[i] = 0; c.inst_e[i] = 0; }   // (per-CTA copies)
         if (K & 8) {                // messages: wire time per design point, fresh link state
             const double beta = __ddiv_rn(1e9, bwv);
             const int cols = p.cols[cfg];

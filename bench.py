@@ -234,10 +234,19 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (the engine has no CPU path)")
+    # FLINT_BENCH_SHARE_GPU=1 (development only): every rank on the visible GPUs modulo their
+    # count, gloo for the result gather -- exercises the multi-rank logic on a 1-GPU box
+    share = os.environ.get("FLINT_BENCH_SHARE_GPU") == "1"
+    if share:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cdev = torch.device("cpu") if share else dev       # where the collectives' tensors live
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     from paper_2604_17550_b200 import sweep as S
     from paper_2604_17550_b200.engine import Engine
@@ -264,8 +273,8 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)       # > L2 (126 MB)
     per = -(-n * world // world)
-    gather_out = torch.empty((n * world, 7), dtype=torch.int64, device=dev) if world > 1 else None
-    gather_in = torch.empty((n, 7), dtype=torch.int64, device=dev) if world > 1 else None
+    gather_out = torch.empty((n * world, 7), dtype=torch.int64, device=cdev) if world > 1 else None
+    gather_in = torch.empty((n, 7), dtype=torch.int64, device=cdev) if world > 1 else None
 
     def step():
         k = eng.run_device(ptrs, stream.cuda_stream, n)
@@ -303,7 +312,7 @@ def run_ours(args):
         torch.cuda.synchronize()
     total_ms = sum(s_ms)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
@@ -329,11 +338,11 @@ def run_ours(args):
         t0 = time.perf_counter()
         out = eng.run(hp)
         if world > 1:
-            S.gather_rows(out["status"], out["rows"], n * world, world, rank, device=dev)
+            S.gather_rows(out["status"], out["rows"], n * world, world, rank, device=cdev)
         e2e_s.append(time.perf_counter() - t0)
     e2e_step = sum(e2e_s) / len(e2e_s)
     if world > 1:
-        t = torch.tensor([e2e_step], dtype=torch.float64, device=dev)
+        t = torch.tensor([e2e_step], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_step = float(t.item())
     h2d = sum(v.nbytes for v in pin.values())
@@ -343,7 +352,7 @@ def run_ours(args):
     bpu = bytes_per_unit(gs)
     peak, peak_src = measured_peak_hbm()
     achieved = bpu * units_step / (kernel_ms / 1e3) / 1e9
-    traffic = profiled_traffic(args.workload)
+    traffic = profiled_traffic(args.workload) if not args.points else None   # (captured on the full grid)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
                 "peak_source": peak_src, "kernel": "fl::sweep_kernel<1>",

@@ -31,6 +31,16 @@
 // Per-rank statistics (compute/comm busy, exposed comm, peak memory,
 // simulator.py:342-393) are accumulated on-line from the step timeline.
 //
+// What makes it fast (with the A/B measurements):
+//   * dependency edges whose order is fixed by ancestry are classed on the host
+//     (capi.cu): first / middle / last writes, maxes and reads of the accumulator
+//     replace per-edge read-modify-writes (pop_event);
+//   * per-rank state lives in registers (what every step reads) and in shared-
+//     memory planes with a compile-time stride (everything else, F_* / Q_*);
+//   * collective arrivals are aggregated per warp (dispatch);
+//   * design points wider than 1024 ranks run on thread-block clusters whose
+//     per-step reduction goes through st.async + mbarrier (cl_step_min).
+//
 // Numerics: every fp64 operation of the cost model uses an explicit
 // round-to-nearest intrinsic and the file is compiled with -fmad=false, so
 // each expression is the reference's Python evaluation order with no FMA

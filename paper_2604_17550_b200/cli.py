@@ -41,6 +41,8 @@ def build_parser() -> _Parser:
     sp.add_argument("--normalize-to", help="parallel token whose makespan is the baseline")
     sp.add_argument("--jobs", type=int, default=1)
     sp.add_argument("--device", type=int, default=0)
+    sp.add_argument("--devices", help="extension: comma list of GPU ids to spread the design points over "
+                    "(one process, one host thread per GPU)")
     sp.add_argument("--pass", dest="passes", help="extension: comma list of graph rewrites to sweep, e.g. "
                     "none,reorder-allgather:1,bucket-allreduce:2097152 (adds a 'pass' column)")
     sp.add_argument("--out", required=True, help="CSV path")
@@ -53,7 +55,8 @@ def cmd_sweep(args) -> int:
     split = lambda s: [t.strip() for t in s.split(",") if t.strip()]
     rows = sweep_rows(args.preset, split(args.parallel), split(args.topo), split(args.algo),
                       args.comm_mode, args.fsdp_mode, args.profile, args.device,
-                      split(args.passes) if args.passes else None)
+                      split(args.passes) if args.passes else None,
+                      [int(x) for x in split(args.devices)] if args.devices else None)
     normalize(rows, args.normalize_to)
     write_csv(rows, args.out)
     print(f"wrote {len(rows)} rows to {args.out}")

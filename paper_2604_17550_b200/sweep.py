@@ -154,7 +154,7 @@ def gather_rows(local_status, local_rows, n_total: int, world: int, rank: int, d
 
 def sweep_rows(preset: str, parallels, topos, algos, comm_mode: str = "analytical",
                fsdp_mode: str = "delayed", profile_path: Optional[str] = None, device: int = 0,
-               passes: Optional[list] = None) -> list:
+               passes: Optional[list] = None, devices: Optional[list] = None) -> list:
     """Rows of ``trainsim sweep`` (cli.py:319-358) computed on the GPU.
 
     Design points that share a graph are evaluated in one engine launch: all
@@ -165,7 +165,11 @@ def sweep_rows(preset: str, parallels, topos, algos, comm_mode: str = "analytica
     ``passes`` (an extension; the reference sweeps one graph per parallel
     token) adds a graph-rewrite axis, e.g. ``["none", "reorder-allgather:1",
     "bucket-allreduce:2097152"]`` (passes.apply_pass); rows then carry a
-    ``pass`` column and each value is another graph structure."""
+    ``pass`` column and each value is another graph structure.
+
+    ``devices`` spreads every group's design points over several GPUs from this
+    one process (contiguous slices, one host thread per GPU; the engine call
+    releases the GIL); the rows do not depend on how they are split."""
     if comm_mode not in ("analytical", "expanded"):
         raise UnsupportedComboError(f"unknown comm mode {comm_mode!r}")
     if not parallels or not topos or not algos:
@@ -206,13 +210,11 @@ def sweep_rows(preset: str, parallels, topos, algos, comm_mode: str = "analytica
             for i in idxs:
                 errors[i] = e
             continue
-        eng = Engine(graphs, device)
-        try:
-            out = eng.run(DesignPoints.from_topologies([parsed[i][0] for i in idxs], [parsed[i][1] for i in idxs]))
-        finally:
-            eng.close()
-        for j, i in enumerate(idxs):
-            results[i] = (int(out["status"][j]), out["rows"][j], p.degree)
+        devs = list(devices) if devices else [device]
+        pts = DesignPoints.from_topologies([parsed[i][0] for i in idxs], [parsed[i][1] for i in idxs])
+        for (a, b), out in zip(*_run_on_devices(graphs, pts, devs)):
+            for j in range(a, b):
+                results[idxs[j]] = (int(out["status"][j - a]), out["rows"][j - a], p.degree)
     rows = []
     for i, (par, ps, spec, algo) in enumerate(tasks):  # first failure in task order, like the pool map
         if i in errors:
@@ -227,6 +229,29 @@ def sweep_rows(preset: str, parallels, topos, algos, comm_mode: str = "analytica
         row.update({k: int(v) for k, v in zip(ROW_FIELDS, vals)})
         rows.append(row)
     return rows
+
+
+def _run_on_devices(graphs, pts: DesignPoints, devices: list):
+    """Evaluate `pts` split into contiguous slices, one per device, concurrently."""
+    from concurrent.futures import ThreadPoolExecutor
+    from .store import compile_graphs
+    gs = compile_graphs(graphs)
+    slices = [shard(len(pts), len(devices), k) for k in range(len(devices))]
+
+    def one(k):
+        a, b = slices[k]
+        if a == b:
+            return {"status": np.zeros(0, np.int32), "rows": np.zeros((0, 6), np.int64)}
+        eng = Engine(gs, devices[k])
+        try:
+            return eng.run(pts.take(np.arange(a, b)))
+        finally:
+            eng.close()
+
+    if len(devices) == 1:
+        return slices, [one(0)]
+    with ThreadPoolExecutor(max_workers=len(devices)) as ex:
+        return slices, list(ex.map(one, range(len(devices))))
 
 
 def normalize(rows: list, normalize_to: Optional[str]) -> None:

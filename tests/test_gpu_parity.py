@@ -355,3 +355,14 @@ def test_engine_c3_full_grid_vs_oracle():
     assert bad.size == 0, (bad[:5], got[bad[:2]], fx["rows"][bad[:2]])
     mk, cp = got[:, 0], got[:, 1]
     assert (cp <= mk).all() and (got[:, 4] <= got[:, 3]).all() and (got[:, 2] <= mk).all() and (got[:, 3] <= mk).all()
+
+
+def test_sweep_rows_split_over_devices_is_identical():
+    """sweep_rows(devices=[...]) evaluates contiguous slices concurrently (one host thread per
+    GPU; here the same GPU twice) and returns exactly the single-launch rows."""
+    from paper_2604_17550_b200.sweep import sweep_rows
+    topos = [f"switch:8:{bw}GB:{lat}us" for bw in (10, 50, 400) for lat in (1, 5)] + ["mesh:2x4:100GB:1us"]
+    args = ("tiny", ["fsdp:8", "dp:8"], topos, ["ring", "mesh-hier"][:1])
+    one = sweep_rows(*args)
+    two = sweep_rows(*args, devices=[0, 0, 0])
+    assert one == two and len(one) == 2 * len(topos)

@@ -60,6 +60,21 @@ namespace cg = cooperative_groups;
 
 extern __shared__ __align__(16) unsigned char fl_smem[];   // the sweep kernel's dynamic shared memory
 
+#ifdef FL_PROFILE     // development only: per-segment cycle counts of warp 0 of CTA 0
+static __device__ unsigned long long fl_prof[16];
+static __shared__ long long fl_prof_t;
+#define PROF_MARK(k)                                                                      \
+    do {                                                                                  \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                                        \
+            const long long now_ = clock64();                                             \
+            atomicAdd(&fl_prof[k], (unsigned long long)(now_ - fl_prof_t));               \
+            fl_prof_t = now_;                                                             \
+        }                                                                                 \
+    } while (0)
+#else
+#define PROF_MARK(k) do {} while (0)
+#endif
+
 // ------------------------------------------------------------------ costs
 
 __device__ __forceinline__ int64_t rhu(double x) {          // traceio.py:68-70
@@ -263,26 +278,33 @@ __device__ __forceinline__ int gor(int v, Shared &sh, int &par) {
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ uint64_t cl_step_min(uint64_t v, int &any, Shared &sh, int &par, unsigned &xk) {
+    PROF_MARK(12);                              // (profile builds: exchange entry)
     v = block_min_u64(v, sh, par);              // (its barrier also orders this CTA's pops before cflag)
+    PROF_MARK(13);                              // block min
     const int p = xk & 1;
     const unsigned ph = (xk >> 1) & 1;
     xk++;
     cg::cluster_group cl = cg::this_cluster();
     const unsigned n = cl.num_blocks(), me = cl.block_rank();
     const unsigned mb = smem_u32(&sh.xmbar[p]);
-    if (threadIdx.x == 0) {
-        const unsigned long long f = (unsigned long long)sh.cflag;
-        sh.cflag = 0;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(16u * n) : "memory");
-        const unsigned slot = smem_u32(&sh.xbuf[p][me][0]);
-        for (unsigned j = 0; j < n; j++) {
+    if (threadIdx.x < 32) {         // warp 0: lane j sends to CTA j
+        unsigned long long f = 0;
+        if (threadIdx.x == 0) {
+            f = (unsigned long long)sh.cflag;
+            sh.cflag = 0;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(16u * n) : "memory");
+        }
+        f = __shfl_sync(FULL, f, 0);
+        if (threadIdx.x < n) {
+            const unsigned slot = smem_u32(&sh.xbuf[p][me][0]);
             unsigned ra, rmb;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(slot), "r"(j));
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rmb) : "r"(mb), "r"(j));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(slot), "r"(threadIdx.x));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rmb) : "r"(mb), "r"(threadIdx.x));
             asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];"
                          ::"r"(ra), "l"(v), "l"(f), "r"(rmb) : "memory");
         }
     }
+    PROF_MARK(14);                              // sends
     unsigned done;
     do {
         asm volatile("{ .reg .pred q; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 q, [%1], %2; "
@@ -301,20 +323,6 @@ __device__ __forceinline__ uint64_t cl_step_min(uint64_t v, int &any, Shared &sh
 
 // ---------------------------------------------------------- rank state
 
-#ifdef FL_PROFILE     // development only: per-segment cycle counts of warp 0 of CTA 0
-static __device__ unsigned long long fl_prof[16];
-static __shared__ long long fl_prof_t;
-#define PROF_MARK(k)                                                                      \
-    do {                                                                                  \
-        if (blockIdx.x == 0 && threadIdx.x == 0) {                                        \
-            const long long now_ = clock64();                                             \
-            atomicAdd(&fl_prof[k], (unsigned long long)(now_ - fl_prof_t));               \
-            fl_prof_t = now_;                                                             \
-        }                                                                                 \
-    } while (0)
-#else
-#define PROF_MARK(k) do {} while (0)
-#endif
 
 // Node record built by capi.cu, two 16-byte words per node so that one
 // broadcast load per word serves the 32 ranks of a warp visiting the node (an L1
@@ -1478,7 +1486,7 @@ __global__ void __launch_bounds__(1024, 1)
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&fl_prof[15], 1ull);
         if (blockIdx.x == 0 && threadIdx.x == 0 && cfg + ncl >= p.n) {
             printf("FLPROF points %llu", fl_prof[15]);
-            for (int k = 0; k < 12; k++) printf(" s%d %llu", k, fl_prof[k]);
+            for (int k = 0; k < 15; k++) printf(" s%d %llu", k, fl_prof[k]);
             printf("\n");
         }
 #endif

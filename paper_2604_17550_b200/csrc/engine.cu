@@ -1580,7 +1580,11 @@ __global__ void cp_kernel(const __grid_constant__ DevGraph g, const __grid_const
 template <int T>
 static cudaError_t launch_t(int grid, int block, size_t smem, cudaStream_t st, int cluster, const DevGraph &g,
                             const DevPoints &p, const DevOut &o, const DevScratch &sc) {
-    if (cluster <= 1 || (T >> 5)) {     // narrow planes: single-CTA design points only
+    if constexpr ((T >> 5) != 0) {     // narrow planes: single-CTA design points only
+        sweep_kernel<T, false><<<grid, block, smem, st>>>(g, p, o, sc);
+        return cudaGetLastError();
+    } else {
+    if (cluster <= 1) {
         sweep_kernel<T, false><<<grid, block, smem, st>>>(g, p, o, sc);
         return cudaGetLastError();
     }
@@ -1597,6 +1601,7 @@ static cudaError_t launch_t(int grid, int block, size_t smem, cudaStream_t st, i
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, sweep_kernel<T, true>, g, p, o, sc);
+    }
 }
 
 static inline int plane_class(int block) { return block > 256 ? 0 : block > 64 ? 1 : 2; }

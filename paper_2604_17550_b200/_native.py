@@ -51,7 +51,8 @@ def _compile(out: Path, defines=(), verbose: bool = False) -> str:
     jobs.append((PKG / "csrc" / "capi.cu", tmp / "capi.o", []))
     procs = []
     for src, obj, extra in jobs:
-        cmd = [nvcc(), *NVCC_FLAGS, *dflags, *extra, *inc, "-c", str(src), "-o", str(obj)]
+        cmd = [nvcc(), *NVCC_FLAGS, *os.environ.get("FLINT_NVCC_EXTRA", "").split(), *dflags, *extra, *inc,
+               "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))

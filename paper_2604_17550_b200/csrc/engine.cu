@@ -172,10 +172,8 @@ struct Shared {
     int64_t redi[2][32];
     int64_t cend_all;               // every rank's comm stream ends here (valid iff cend_uniform)
     int cend_uniform;
-    int parity;
     int ncomp;
     int nmcomp;
-    int flag;
     // cluster variant: per-CTA partial results, written by every CTA of the cluster (DSMEM)
     uint64_t xkmin[2][16];
     int64_t xvmax[2][16];
@@ -404,9 +402,7 @@ struct Ctx {
     int RL;                         // ranks owned by this CTA
     int base;                       // first rank owned by this CTA (clusters of CTAs share a design point)
     int BR, DR;                     // strides of the touched / done bitmaps (RL in shared memory, else R)
-    int crank, CS;                  // this CTA's rank in its cluster, cluster size (1 without clusters)
     bool lead_cta;                  // the cluster's first CTA (its thread 0 does the serial work)
-    int touch;                      // first-dependency bitmap in shared memory (else epoch tags)
     uint64_t *done, *rdyc, *rdyh, *due;
     uint64_t *touched;              // [word][rank]: accumulator written in this design point
     int64_t *cp;                    // [max_nodes][R]
@@ -1145,8 +1141,6 @@ __global__ void __launch_bounds__(1024, 1)
         c.R = R;
         c.RL = RL;
         c.base = base_r;
-        c.crank = crank;
-        c.CS = CS;
         unsigned char *base = sc.base + (size_t)cid * sc.slot_bytes;
         const size_t words = (size_t)g.max_words * R;
         uint64_t *gbits = reinterpret_cast<uint64_t *>(base + sc.off_bits);
@@ -1179,7 +1173,6 @@ __global__ void __launch_bounds__(1024, 1)
         c.ncomp = CL ? ctr : &sh.ncomp;
         c.nmcomp = CL ? ctr + 1 : &sh.nmcomp;
         c.lead_cta = crank == 0;
-        c.touch = sc.touch_in_smem;
         const int M = g.n_msg;
         int64_t *mb = reinterpret_cast<int64_t *>(base + sc.off_msg);
         c.msg_sendt = mb;
@@ -1223,7 +1216,7 @@ __global__ void __launch_bounds__(1024, 1)
 
     int par = 0;
     unsigned xk = 0;                // cluster step exchanges done (cl_step_min)
-    if (tid == 0) { sh.parity = 0; sh.ncomp = 0; sh.nmcomp = 0; sh.flag = 0; sh.cflag = 0; }
+    if (tid == 0) { sh.ncomp = 0; sh.nmcomp = 0; sh.cflag = 0; }
     if (CL && tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sh.xmbar[0])) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sh.xmbar[1])) : "memory");

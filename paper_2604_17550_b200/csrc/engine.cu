@@ -168,6 +168,7 @@ struct Shared {
     unsigned long long xmbar[2];    // their mbarriers
     int cflag;                      // a rank of this CTA completed a collective / message since the last exchange
     int ncons;                      // cluster without messages: completion-list entries reserved so far
+    int fifo_empty;                 // rank 0's comm FIFO was empty before this step's reservations
     uint64_t red[2][32];
     int64_t redi[2][32];
     int64_t cend_all;               // every rank's comm stream ends here (valid iff cend_uniform)
@@ -1005,8 +1006,9 @@ static __device__ void reserve_msgs(const DevGraph &g, const DevOut &o, const Ct
 
 // Reserve the comm streams of every instance completed in this step, in the
 // reference's order (simulator.py:298-309), block- (or cluster-) wide; then the
-// step's messages (simulator.py:310-327).  Returns the largest critical-path
-// finish among them.
+// step's messages (simulator.py:310-327).  Returns the end of the first reserved
+// instance when every reserved instance spanned the world with uniform comm streams
+// (then every rank's FIFO changed the same way), else -1.
 // (inlined: as a real call the ABI spilled the caller's live registers around it)
 template <bool MSG, bool CL, int K>
 __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o, const Ctx &c, Shared &sh, int &par,
@@ -1017,7 +1019,9 @@ __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o,
     // counter could be reset (the instance times it writes are per-CTA copies).
     constexpr bool MONO = CL && !MSG;
     int32_t *const cl = c.complist + (MONO ? sh.ncons : 0);
-    int64_t cpm = 0;
+    int64_t cpm = 0;                // (critical path of the messages; members carry the collectives')
+    int64_t efirst = -1;            // end of the first reserved instance ...
+    bool allfull = true;            // ... if every one spanned the world with uniform comm streams
     if (nc > 1) {                   // one thread orders the list (shared by the cluster's CTAs)
         if ((!CL || c.lead_cta) && threadIdx.x == 0) {
             for (int a = 1; a < nc; a++) {
@@ -1042,6 +1046,7 @@ __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o,
         if (full_node >= 0 && uni) {
             s = cend > t ? cend : t;
         } else {
+            allfull = false;
             gsync<CL>();            // comm ends written by the previous reservation
             int64_t local = t;
             for (int64_t j = threadIdx.x; j < nm; j += blockDim.x) {
@@ -1053,8 +1058,7 @@ __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o,
             s = gmax_i64<CL>(local, sh, par);
         }
         const int64_t e = s + c.inst_dur[i];
-        const int64_t cpv = c.inst_cpmax[i] + c.inst_dur[i];
-        cpm = cpv > cpm ? cpv : cpm;
+        if (q == 0) efirst = e;
         if (threadIdx.x == 0) { c.inst_s[i] = s; c.inst_e[i] = e; }      // (each CTA its own copy)
         if (full_node >= 0) {
             for (int lm = threadIdx.x; lm < RL; lm += blockDim.x) {
@@ -1094,7 +1098,7 @@ __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o,
     // Without messages nothing written above is read before the caller's next barrier
     // (its step reduction, or reserve()'s own); the message phase fills other ranks' lists.
     if (MSG) gsync<CL>();
-    return cpm;
+    return allfull && !(MSG && nmc) ? efirst : -1;
 }
 
 // Barrier, then reserve whatever completed since the last reservation.
@@ -1415,12 +1419,23 @@ __global__ void __launch_bounds__(1024, 1)
             const int nc = CL ? (any ? *c.ncomp - (MSG ? 0 : sh.ncons) : 0) : sh.ncomp;
             const int nmc = MSG ? (CL ? (any ? *c.nmcomp : 0) : sh.nmcomp) : 0;
             if (nc | nmc) {
-                reserve_n<MSG, CL, K>(g, o, c, sh, par, tcur, false, cfg, f.epoch, nc, nmc,
-                                                     topo, p.cols[cfg]);
-                    if (active) refresh_ring(c, L, s);
-                nt = active ? next_time(g, c, L, s, tcur) : TINF;
-                key = nt == TINF ? KINF : ((uint64_t)(nt < TCAP ? nt : TCAP) << 14) | (uint64_t)L.r;
-                kmin = CL ? cl_step_min(key, any, sh, par, xk) : gmin_key<CL>(key, sh, par);
+                if (CL && tid == 0) sh.fifo_empty = s.head_e == TINF;   // (identical for every rank when uniform)
+                const int64_t ef = reserve_n<MSG, CL, K>(g, o, c, sh, par, tcur, false, cfg, f.epoch, nc, nmc,
+                                                         topo, p.cols[cfg]);
+                if (active) refresh_ring(c, L, s);
+                if (CL && ef >= 0) {       // (clusters only: on one CTA the A/B showed no gain)
+                    // every rank's next event only gained the same new FIFO head (if its FIFO was
+                    // empty), so the step minimum follows without another reduction; rank 0 is
+                    // the lowest rank holding it
+                    if (sh.fifo_empty) {
+                        const uint64_t k = (uint64_t)(ef < TCAP ? ef : TCAP) << 14;
+                        kmin = k < kmin ? k : kmin;
+                    }
+                } else {
+                    nt = active ? next_time(g, c, L, s, tcur) : TINF;
+                    key = nt == TINF ? KINF : ((uint64_t)(nt < TCAP ? nt : TCAP) << 14) | (uint64_t)L.r;
+                    kmin = CL ? cl_step_min(key, any, sh, par, xk) : gmin_key<CL>(key, sh, par);
+                }
             }
             if (kmin == KINF) break;
             const int64_t t = (int64_t)(kmin >> 14);

@@ -681,7 +681,8 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
         if (fx64 > cm) F64<K>(F_CPMAX, L.lr) = fx64;
     }
     int64_t freed = rec_u64(xa.z, xa.w);
-    if (xa.y >> 16) for (uint32_t q = (uint32_t)g.mfree_off[L.nb + x], qe = q + (xa.y >> 16); q < qe; q++) {
+    const uint32_t nmf = (xa.y >> 16) & 0xffu;
+    if (nmf) for (uint32_t q = (uint32_t)g.mfree_off[L.nb + x], qe = q + nmf; q < qe; q++) {
         const int tt = L.tb + g.free_tens[q];
         const int2 cr = g.tens_rng[tt];
         bool all = true;
@@ -696,6 +697,11 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
     const uint64_t fx = (uint64_t)fx64;     // this node's critical-path finish
     int seq = 0;
     const int32_t *sl = g.succ_ent;
+    // the first "last" edge's accumulator read goes out before the other edges are processed
+    const uint32_t lo = xa.y >> 24;
+    const uint32_t qlast = lo && f.fold ? xa.x + lo - 1 : 0xffffffffu;
+    uint64_t alast = 0;
+    if (qlast != 0xffffffffu) alast = (uint64_t)__ldcg(c.cp + ((int)((uint32_t)sl[qlast] & 0xffffu) * R + L.r));
     for (uint32_t q = xa.x, qe = xa.x + (xa.y & 0xffffu); q < qe; q++, seq++) {
         const uint32_t ent = (uint32_t)sl[q];
         const int d = (int)(ent & 0xffffu);
@@ -719,7 +725,7 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
         }
         if (cls == FL_EDGE_LAST) {
             PROF_MARK(10);                  // edges before a "last" one
-            const uint64_t a = (uint64_t)__ldcg(slot) & VAL48;    // the first/middle ones' max (at L2)
+            const uint64_t a = (q == qlast ? alast : (uint64_t)__ldcg(slot)) & VAL48;   // first/middle ones' max
             dispatch(g, c, L, s, f, d, db, (int64_t)(a > fx ? a : fx), seq, t);
             PROF_MARK(11);                  // "last" edge: accumulator read + dispatch
             continue;

@@ -286,14 +286,14 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
             const unsigned meta = (unsigned)d->node_kind[i] | ((unsigned)(d->node_flags[i] & 1) << 4) |
                                   ((unsigned)is_static[i] << 5) | ((unsigned)indeg_nh << 6) | ((unsigned)indeg << 16);
             const uint32_t nmf = (uint32_t)mfree.size() - m0;
-            if (nmf > 0xff) return fail(FL_ERR_CAPACITY, "a node frees more than 255 shared tensors");
+            if (nmf > 0xfff) return fail(FL_ERR_CAPACITY, "a node frees more than 4095 shared tensors");
             // offset + 1 of the node's first "last" dependency edge (its accumulator read is
             // issued before the other edges are processed), 0 when none or beyond 255
             uint32_t lo = 0;
             for (int q = d->succ_off[i]; q < d->succ_off[i + 1] && q - d->succ_off[i] < 255; q++)
                 if (((uint32_t)succ_ent[q] >> 16 & 7u) == (uint32_t)fl::FL_EDGE_LAST) { lo = q - d->succ_off[i] + 1; break; }
             mfree_off[i] = (int32_t)m0;
-            rec[2 * i] = make_uint4((unsigned)d->succ_off[i], (unsigned)(d->succ_off[i + 1] - d->succ_off[i]) | (nmf << 16) | (lo << 24),
+            rec[2 * i] = make_uint4((unsigned)d->succ_off[i], (unsigned)(d->succ_off[i + 1] - d->succ_off[i]) | (nmf << 12) | (lo << 24),
                                     (uint32_t)ufree, (uint32_t)(ufree >> 32));
             rec[2 * i + 1] = make_uint4(meta, (unsigned)(d->node_coll_ord[i] < 0 ? 0 : d->node_coll_ord[i]),
                                         (uint32_t)alloc, (uint32_t)(alloc >> 32));

@@ -326,7 +326,7 @@ __device__ __forceinline__ uint64_t cl_step_min(uint64_t v, int &any, Shared &sh
 // Node record built by capi.cu, two 16-byte words per node so that one
 // broadcast load per word serves the 32 ranks of a warp visiting the node (an L1
 // hit: the records of a graph set are a few tens of KB):
-//   a = {succ_off, succ_cnt | mfree_cnt << 16, ufree_lo, ufree_hi}
+//   a = {succ_off, succ_cnt | mfree_cnt << 12 | (first "last" edge + 1) << 24, ufree_lo, ufree_hi}
 //       dependents; tensors with more than one consumer it may free (from g.mfree_off);
 //       bytes of tensors it is the only (or statically last) consumer of
 //   b = {meta, coll_ord, alloc_lo, alloc_hi}        bytes allocated when the node starts
@@ -681,7 +681,7 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
         if (fx64 > cm) F64<K>(F_CPMAX, L.lr) = fx64;
     }
     int64_t freed = rec_u64(xa.z, xa.w);
-    const uint32_t nmf = (xa.y >> 16) & 0xffu;
+    const uint32_t nmf = (xa.y >> 12) & 0xfffu;
     if (nmf) for (uint32_t q = (uint32_t)g.mfree_off[L.nb + x], qe = q + nmf; q < qe; q++) {
         const int tt = L.tb + g.free_tens[q];
         const int2 cr = g.tens_rng[tt];
@@ -702,7 +702,7 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
     const uint32_t qlast = lo && f.fold ? xa.x + lo - 1 : 0xffffffffu;
     uint64_t alast = 0;
     if (qlast != 0xffffffffu) alast = (uint64_t)__ldcg(c.cp + ((int)((uint32_t)sl[qlast] & 0xffffu) * R + L.r));
-    for (uint32_t q = xa.x, qe = xa.x + (xa.y & 0xffffu); q < qe; q++, seq++) {
+    for (uint32_t q = xa.x, qe = xa.x + (xa.y & 0xfffu); q < qe; q++, seq++) {
         const uint32_t ent = (uint32_t)sl[q];
         const int d = (int)(ent & 0xffffu);
         const int cls = f.fold ? (int)(ent >> 16) : FL_EDGE_COUNTED;

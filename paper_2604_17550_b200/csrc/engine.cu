@@ -585,9 +585,12 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
             if (sk > t) break;
         }
         int64_t v;
+        // (the node's record and duration are read before the pop's own shared-memory traffic)
+        const uint2 xal = *reinterpret_cast<const uint2 *>(&g.node_rec[2 * (L.nb + ms_min(s.rc)) + 1].z);
+        const int64_t dx = dur_of(g, c, L.nb + ms_min(s.rc));
         const int x = ms_pop_cp<K, F_RC_CP, F_RC_SUM>(s.rc, c.rdyc, c.cp, R, L, v, g.max_words);
-        const int64_t e = t + dur_of(g, c, L.nb + x);
-        { const uint4 xb = rec_b(g, L.nb + x); F64<K>(F_ALLOC, L.lr) += rec_u64(xb.z, xb.w); }
+        const int64_t e = t + dx;
+        F64<K>(F_ALLOC, L.lr) += rec_u64(xal.x, xal.y);
         record(g, o, cfg, L.r, x, t, e);
         if ((K & 7) == 1 && e > t) {      // one compute stream: its busy intervals are disjoint
             F64<K>(F_COMP, L.lr) += e - t;

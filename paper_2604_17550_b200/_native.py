@@ -167,6 +167,13 @@ def _bind(L):
     return L
 
 
+def device_count() -> int:
+    """GPUs the engine can see (0 when none; the engine then refuses to run)."""
+    n = C.c_int32(0)
+    lib().fl_device_count(C.byref(n))
+    return int(n.value)
+
+
 def last_error() -> str:
     return lib().fl_last_error().decode(errors="replace")
 

@@ -39,7 +39,8 @@ def build_parser() -> _Parser:
     sp.add_argument("--fsdp-mode", choices=[m.value for m in FsdpMode], default=FsdpMode.DELAYED.value)
     sp.add_argument("--profile", help="measured-kernel profile JSON")
     sp.add_argument("--normalize-to", help="parallel token whose makespan is the baseline")
-    sp.add_argument("--jobs", type=int, default=1)
+    sp.add_argument("--jobs", type=int, default=1, help="the reference's worker-process count; here, the "
+                    "number of GPUs to spread the design points over (at most the GPUs present)")
     sp.add_argument("--device", type=int, default=0)
     sp.add_argument("--devices", help="extension: comma list of GPU ids to spread the design points over "
                     "(one process, one host thread per GPU)")
@@ -49,6 +50,18 @@ def build_parser() -> _Parser:
     return p
 
 
+def _devices(args):
+    """--devices wins; else --jobs N spreads the points over min(N, present) GPUs."""
+    if args.devices:
+        return [int(x) for x in args.devices.split(",") if x.strip()]
+    if args.jobs > 1:
+        from . import _native
+        n = min(args.jobs, _native.device_count())
+        if n > 1:
+            return list(range(n))
+    return None
+
+
 def cmd_sweep(args) -> int:
     from .sweep import normalize, sweep_rows, write_csv
     t0 = time.monotonic()
@@ -56,7 +69,7 @@ def cmd_sweep(args) -> int:
     rows = sweep_rows(args.preset, split(args.parallel), split(args.topo), split(args.algo),
                       args.comm_mode, args.fsdp_mode, args.profile, args.device,
                       split(args.passes) if args.passes else None,
-                      [int(x) for x in split(args.devices)] if args.devices else None)
+                      _devices(args))
     normalize(rows, args.normalize_to)
     write_csv(rows, args.out)
     print(f"wrote {len(rows)} rows to {args.out}")

@@ -1,15 +1,21 @@
 #!/usr/bin/env python
 """Benchmark of the hot path: batched design-point evaluation of a workload graph.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c3|c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c3|c2|c4]
+                    [--scaling strong|weak]
 
-One *step* = one engine launch evaluating every design point of the
-workload (BASELINE config 3 by default: llama-8b-like fsdp:1024, 4096 points,
-851,968 (rank, node) pairs per point) -- simulate + critical_path + the
-per-point reductions of cli._sweep_row for all of them.  Under torchrun each
-process drives one GPU; the job is weak-scaled: GPU k evaluates the C3 grid
-for compute-efficiency variant k (k = 0 is exactly C3), and the rows are
-all-gathered over NCCL at the end of every step.
+One *step* = one engine launch per graph family evaluating every design point
+of the workload (BASELINE config 3 by default: llama-8b-like fsdp:1024, 4096
+points, 851,968 (rank, node) pairs per point) -- simulate + critical_path +
+the per-point reductions of cli._sweep_row for all of them.
+
+`--gpus N` runs one process per GPU (re-launching itself under
+torch.distributed.run when WORLD_SIZE is unset).  Default strong scaling: each
+family's grid is split into N contiguous slices (sweep.shard, the reference's
+share-nothing points, cli.py:352-358) and one NCCL all_gather_into_tensor
+collects the rows inside every timed step; the gathered C3/C4 rows are checked
+against the committed golden rows.  `--scaling weak`: every GPU evaluates the
+whole grid (compute-efficiency variant k on GPU k).
 
 Prints one JSON line (rank 0): `value` = (rank, node, design point) triples
 per second over all GPUs with inputs resident in HBM, `e2e` = the same
@@ -101,25 +107,37 @@ class ClockSampler:
 
 
 def load_workload(name: str):
+    """The workload and, per part (graph family), its per-rank graphs."""
     from paper_2604_17550_b200 import sweep as S
     w = {"c3": S.c3_workload, "c2": S.c2_workload, "c4": S.c4_workload}[name]()
-    graphs = S.workload_graphs(w)
-    return w, graphs
+    return w, [S.part_graphs(w, part) for part in w.parts]
 
 
-def workload_desc(w, gs) -> dict:
-    st = gs.structs[0]
-    return {"workload": {"c3": "BASELINE config 3: llama-8b-like FSDP (delayed) graph at 1024 ranks, 4096 design "
-                               "points = {switch:1024+ring, mesh:32x32+mesh-hier} x 64 bw [10GB/s,1.8TB/s] x "
-                               "32 latency [100ns,20us]",
-                         "c2": "BASELINE config 2: GPT-2 small dp:64, 256 design points = {ring, tree} x 16 bw "
-                               "[10GB/s,1.8TB/s] x 8 latency [100ns,10us]",
-                         "c4": "BASELINE config 4 scale: llama-70b-like FSDP graph at 8192 ranks (clusters of 8 "
-                               "CTAs per design point), design points from {switch:8192+ring, mesh:64x128+"
-                               "mesh-hier} x 128 bw [10GB/s,1.8TB/s] x 64 latency [100ns,20us]"}[w.name],
-            "model": w.model, "parallel": w.parallel, "ranks": gs.n_ranks, "nodes_per_rank": st.n,
-            "edges_per_rank": int(st.pred_off[-1]), "points_per_gpu": len(w.points),
-            "units_per_point": gs.units()}
+WORKLOAD_TEXT = {
+    "c3": "BASELINE config 3: llama-8b-like FSDP (delayed) graph at 1024 ranks, 4096 design points = "
+          "{switch:1024+ring, mesh:32x32+mesh-hier} x 64 bw [10GB/s,1.8TB/s] x 32 latency [100ns,20us]",
+    "c2": "BASELINE config 2: GPT-2 small dp:64, 256 design points = {ring, tree} x 16 bw [10GB/s,1.8TB/s] x "
+          "8 latency [100ns,10us]",
+    "c4": "BASELINE config 4 (SURVEY.md 8d): llama-70b-like at 8192 ranks, 16384 design points = "
+          "{dp:8192 switch ring, dp:8192 switch tree, dp:8192 mesh:64x128 mesh-hier, fsdp:8192 mesh:64x128 "
+          "mesh-hier} x 64 bw [10GB/s,1.8TB/s] x 64 latency [100ns,20us]; clusters of 8 CTAs per design point",
+}
+
+
+def workload_desc(w, gss) -> dict:
+    parts = []
+    for part, gs in zip(w.parts, gss):
+        st = gs.structs[0]
+        parts.append({"parallel": part.parallel, "ranks": gs.n_ranks, "nodes_per_rank": st.n,
+                      "edges_per_rank": int(st.pred_off[-1]), "points": len(part.points),
+                      "units_per_point": gs.units()})
+    d = {"workload": WORKLOAD_TEXT[w.name], "model": w.model, "parallel": w.parallel,
+         "points": w.n_points(), "units_per_step": sum(p["points"] * p["units_per_point"] for p in parts)}
+    if len(parts) == 1:
+        d.update({k: v for k, v in parts[0].items() if k not in ("parallel", "points")})
+    else:
+        d["families"] = parts
+    return d
 
 
 def bytes_per_unit(gs) -> float:
@@ -138,7 +156,9 @@ def measured_peak_hbm():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def profiled_traffic(workload: str):
+def profiled(workload: str):
+    """ncu evidence for the workload's sweep kernel (scripts/record_profile.py): DRAM bytes and
+    executed warp instructions per launch of the full grid."""
     p = ROOT / "profiles" / f"traffic_{workload}.json"
     if p.exists():
         try:
@@ -150,29 +170,40 @@ def profiled_traffic(workload: str):
 
 # ------------------------------------------------------------ CPU oracle
 
+_FLAT: dict = {}
 
-def oracle_sample(gs_graphs, w, idxs, threads: int):
-    """Run the CPU oracle on design points `idxs` with `threads` threads; returns seconds."""
+
+def oracle_rows(graphs, pts, idxs, threads: int):
+    """The CPU oracle on design points `idxs` of `pts` with `threads` threads; (seconds, rows)."""
     from concurrent.futures import ThreadPoolExecutor
     from oracle import pyoracle as O
     from paper_2604_17550_b200.topology import Topology, TopologyKind
-    flat = getattr(oracle_sample, "_flat", None)
-    if flat is None or getattr(oracle_sample, "_key", None) != id(gs_graphs):
-        flat = O.flatten(gs_graphs)
-        oracle_sample._flat, oracle_sample._key = flat, id(gs_graphs)
-    pts = w.points
+    if id(graphs) not in _FLAT:
+        _FLAT[id(graphs)] = O.flatten(graphs)
+    flat = _FLAT[id(graphs)]
     algos = {0: "ring", 1: "tree", 2: "mesh-hier"}
-    R = len(gs_graphs)
+    R = len(graphs)
 
     def one(i):
         kind = TopologyKind.SWITCH if pts.topo_kind[i] == 0 else TopologyKind.MESH2D
         topo = Topology(kind, R, float(pts.bw[i]), int(pts.latency[i]), int(pts.rows[i]), int(pts.cols[i]))
-        return O.sweep_row(gs_graphs, topo, algos[int(pts.algo[i])], flat=flat)
+        return O.sweep_row(graphs, topo, algos[int(pts.algo[i])], flat=flat)
 
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=threads) as ex:
         rows = list(ex.map(one, idxs))
     return time.perf_counter() - t0, rows
+
+
+def sample_jobs(w, count: int):
+    """`count` (part, point) pairs spread evenly over the whole workload (every part visited)."""
+    flat = [(k, i) for k, part in enumerate(w.parts) for i in range(len(part.points))]
+    stride = max(1, len(flat) // max(1, count))
+    return [flat[(j * stride + stride // 2) % len(flat)] for j in range(count)]
+
+
+def _host_threads() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
 
 
 def run_reference(args):
@@ -181,29 +212,35 @@ def run_reference(args):
     if rank != 0:
         return 0
     from oracle import pyoracle as O
+    from paper_2604_17550_b200.store import compile_graphs
     O.build()
     w, graphs = load_workload(args.workload)
-    from paper_2604_17550_b200.store import compile_graphs
-    gs = compile_graphs(graphs)
-    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    n = len(w.points)
-    stride = max(1, n // (threads * (args.steps + args.warmup) + 1))
-    order = [(k * stride) % n for k in range(threads * (args.steps + args.warmup))]
-    times = []
+    gss = [compile_graphs(g) for g in graphs]
+    threads = _host_threads()
+    if args.workload == "c4":
+        threads = min(threads, 8)            # ~2.3 GB of oracle state per 8192-rank point
+    jobs = sample_jobs(w, threads * (args.steps + args.warmup))
+    times, units = [], []
     for s in range(args.warmup + args.steps):
-        dt, _ = oracle_sample(graphs, w, order[s * threads:(s + 1) * threads], threads)
+        mine = jobs[s * threads:(s + 1) * threads]
+        t0 = time.perf_counter()
+        for k in range(len(w.parts)):                     # one pool per family, all threads busy
+            idx = [i for kk, i in mine if kk == k]
+            if idx:
+                oracle_rows(graphs[k], w.parts[k].points, idx, threads)
+        dt = time.perf_counter() - t0
         if s >= args.warmup:
             times.append(dt)
-    units = threads * gs.units()
+            units.append(sum(gss[k].units() for k, _ in mine))
+    value = sum(units) / sum(times)
     step_s = sum(times) / len(times)
-    value = units / step_s
-    sample = (f"{threads} design points per step (one per host thread) of the {args.workload.upper()} grid, "
-              f"every {stride}th point; oracle/flint_oracle.c (C restatement of simulate+critical_path, "
+    sample = (f"{threads} design points per step (one per host thread), spread evenly over the "
+              f"{args.workload.upper()} grid; oracle/flint_oracle.c (C restatement of simulate+critical_path, "
               f"pinned to the reference) per point")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": workload_desc(w, gs),
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": workload_desc(w, gss),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
                              "cpu_model": _cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -224,6 +261,46 @@ def _cpu_model() -> str:
 # ------------------------------------------------------------ our arm
 
 
+def _spawn(args) -> int:
+    """`python bench.py --gpus N` without torchrun: re-launch this script as N ranks."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    log("spawning:", " ".join(cmd))
+    return subprocess.call(cmd)
+
+
+class Slice:
+    """One graph family's share of the step on this rank: its engine, its contiguous slice of
+    the family's design points (sweep.shard) and their device buffers."""
+
+    def __init__(self, torch, eng, pts, a: int, b: int, dev, rank: int, weak: bool):
+        import numpy as np
+        self.eng, self.a, self.b, self.n = eng, a, b, b - a
+        self.pts = pts.take(np.arange(a, b))
+        # every design point carries its device (traceio.py:82-88) and the kernel re-costs each COMP
+        # node from its flops; the default device reproduces the baked durations.  Weak scaling:
+        # GPU k uses efficiency 1 - 0.05 k (k = 0 is the workload itself).
+        self.pts.peak_flops = np.full(self.n, 1.0e12, np.float64)
+        self.pts.efficiency = np.full(self.n, 1.0 - 0.05 * rank if weak else 1.0, np.float64)
+        p = self.pts
+        self.cols = {"algo": p.algo, "topo_kind": p.topo_kind, "bw": p.bw, "latency": p.latency, "rows": p.rows,
+                     "cols": p.cols, "peak_flops": p.peak_flops, "efficiency": p.efficiency}
+        self.cols = {k: np.ascontiguousarray(v) for k, v in self.cols.items() if v is not None}
+        self.d_in = {k: torch.as_tensor(v).to(dev) for k, v in self.cols.items()}
+        self.d_status = torch.zeros(max(1, self.n), dtype=torch.int32, device=dev)
+        self.d_rows = torch.zeros((max(1, self.n), 6), dtype=torch.int64, device=dev)
+        self.ptrs = {k: t.data_ptr() for k, t in self.d_in.items()}
+        self.ptrs.update(out_status=self.d_status.data_ptr(), out_rows=self.d_rows.data_ptr())
+        self.units = self.n * eng.gs.units()
+
+    def launch(self, stream) -> int:
+        return self.eng.run_device(self.ptrs, stream.cuda_stream, self.n) if self.n else 0
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -232,13 +309,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (the engine has no CPU path)")
-    # FLINT_BENCH_SHARE_GPU=1 (development only): every rank on the visible GPUs modulo their
+    # FLINT_BENCH_SHARE_GPU=1 (development/tests only): every rank on the visible GPUs modulo their
     # count, gloo for the result gather -- exercises the multi-rank logic on a 1-GPU box
     share = os.environ.get("FLINT_BENCH_SHARE_GPU") == "1"
     if share:
         local %= torch.cuda.device_count()
+    elif world > torch.cuda.device_count():
+        raise SystemExit(f"{world} ranks but {torch.cuda.device_count()} visible GPUs")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cdev = torch.device("cpu") if share else dev       # where the collectives' tensors live
@@ -249,42 +330,62 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=dev)
 
     from paper_2604_17550_b200 import sweep as S
-    from paper_2604_17550_b200.engine import Engine
+    from paper_2604_17550_b200.engine import DesignPoints, Engine
+    from paper_2604_17550_b200.store import compile_graphs
     w, graphs = load_workload(args.workload)
     if args.points:
-        w.points = w.points.take(np.linspace(0, len(w.points) - 1, args.points).round().astype(np.int64))
-    eng = Engine(graphs, device=local)
-    gs = eng.gs
-    n = len(w.points)
-    units_step = n * gs.units()                        # per GPU, W_sched == W (no rank collapse)
-    pts = w.points
-    # weak scaling: GPU k re-costs compute for efficiency 1 - 0.05 k (k = 0 reproduces C3 exactly)
-    pts.peak_flops = np.full(n, 1.0e12, np.float64)
-    pts.efficiency = np.full(n, 1.0 - 0.05 * rank, np.float64)
-
-    cols = {"algo": (pts.algo, torch.uint8), "topo_kind": (pts.topo_kind, torch.uint8), "bw": (pts.bw, torch.float64),
-            "latency": (pts.latency, torch.int64), "rows": (pts.rows, torch.int32), "cols": (pts.cols, torch.int32),
-            "peak_flops": (pts.peak_flops, torch.float64), "efficiency": (pts.efficiency, torch.float64)}
-    d_in = {k: torch.as_tensor(np.ascontiguousarray(v)).to(dev) for k, (v, _) in cols.items()}
-    d_status = torch.zeros(n, dtype=torch.int32, device=dev)
-    d_rows = torch.zeros((n, 6), dtype=torch.int64, device=dev)
-    ptrs = {k: t.data_ptr() for k, t in d_in.items()}
-    ptrs.update(out_status=d_status.data_ptr(), out_rows=d_rows.data_ptr())
+        for part in w.parts:
+            k = max(1, round(args.points * len(part.points) / w.n_points()))
+            part.points = part.points.take(np.linspace(0, len(part.points) - 1, k).round().astype(np.int64))
+    weak = args.scaling == "weak"
+    gss = [compile_graphs(g) for g in graphs]
+    slices = []
+    for part, gs in zip(w.parts, gss):
+        n = len(part.points)
+        a, b = (0, n) if weak else S.shard(n, world, rank)
+        slices.append(Slice(torch, Engine(gs, device=local), part.points, a, b, dev, rank, weak))
+    # units this step evaluates over ALL ranks (W_sched == W: no rank-symmetry collapse)
+    units_job = sum(len(p.points) * gs.units() for p, gs in zip(w.parts, gss)) * (world if weak else 1)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)       # > L2 (126 MB)
-    per = -(-n * world // world)
-    gather_out = torch.empty((n * world, 7), dtype=torch.int64, device=cdev) if world > 1 else None
-    gather_in = torch.empty((n, 7), dtype=torch.int64, device=cdev) if world > 1 else None
+    per = max(sl.n for sl in slices)
+    if world > 1:
+        # strong: every rank's slices padded to the largest; weak: whole grids
+        n_loc = sum(-(-len(p.points) // world) if not weak else len(p.points) for p in w.parts)
+        gather_in = torch.full((n_loc, 7), -1, dtype=torch.int64, device=cdev)
+        gather_out = torch.empty((n_loc * world, 7), dtype=torch.int64, device=cdev)
 
     def step():
-        k = eng.run_device(ptrs, stream.cuda_stream, n)
-        return k
+        return sum(sl.launch(stream) for sl in slices)
 
     def gather():
         if world > 1:
-            gather_in[:, :6].copy_(d_rows)
-            gather_in[:, 6].copy_(d_status)
+            o = 0
+            for p, sl in zip(w.parts, slices):
+                if sl.n:
+                    gather_in[o:o + sl.n, :6].copy_(sl.d_rows[:sl.n])
+                    gather_in[o:o + sl.n, 6].copy_(sl.d_status[:sl.n])
+                o += len(p.points) if weak else -(-len(p.points) // world)
             dist.all_gather_into_tensor(gather_out, gather_in)
+
+    def assemble():
+        """Full-grid rows per part from the gathered blocks (strong scaling) or this rank's own."""
+        out = []
+        if world == 1 or weak:
+            for sl in slices:
+                out.append((sl.d_status[:sl.n].cpu().numpy(), sl.d_rows[:sl.n].cpu().numpy()))
+            return out
+        g = gather_out.cpu().numpy().reshape(world, -1, 7)
+        o = 0
+        for p in w.parts:
+            n, blk = len(p.points), -(-len(p.points) // world)
+            rows = np.zeros((n, 6), np.int64); st = np.zeros(n, np.int32)
+            for r in range(world):
+                a, b = S.shard(n, world, r)
+                rows[a:b] = g[r, o:o + b - a, :6]; st[a:b] = g[r, o:o + b - a, 6]
+            out.append((st, rows))
+            o += blk
+        return out
 
     for _ in range(args.warmup):
         step(); gather()
@@ -316,18 +417,35 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = world * units_step / (ms_per_step / 1e3)
-    status = d_status.cpu().numpy()
-    if (status != 0).any():
-        raise SystemExit(f"engine returned non-OK status for {(status != 0).sum()} points")
+    value = units_job / (ms_per_step / 1e3)
+    full = assemble()
+    bad = sum(int((st != 0).sum()) for st, _ in full)
+    if bad:
+        raise SystemExit(f"engine returned non-OK status for {bad} points")
+    check = rows_check(args, w, full) if rank == 0 and not weak else None
+    if rank == 0 and args.dump_rows:
+        np.savez(args.dump_rows, **{f"status{k}": st for k, (st, _) in enumerate(full)},
+                 **{f"rows{k}": rw for k, (_, rw) in enumerate(full)})
 
     # ---- e2e: public host-buffer API (fl_sweep_run), pinned host SoA, rows back to host ----
-    pin = {k: torch.as_tensor(np.ascontiguousarray(v)).pin_memory().numpy() for k, (v, _) in cols.items()}
-    from paper_2604_17550_b200.engine import DesignPoints
-    hp = DesignPoints(pin["algo"], pin["topo_kind"], pin["bw"], pin["latency"], pin["rows"], pin["cols"],
-                      pin["peak_flops"], pin["efficiency"])
+    hps = []
+    for sl in slices:
+        pin = {k: torch.as_tensor(v).pin_memory().numpy() for k, v in sl.cols.items()}
+        hps.append(DesignPoints(pin["algo"], pin["topo_kind"], pin["bw"], pin["latency"], pin["rows"],
+                                pin["cols"], pin.get("peak_flops"), pin.get("efficiency")))
+
+    def e2e_step():
+        outs = [sl.eng.run(hp) if sl.n else None for sl, hp in zip(slices, hps)]
+        if world > 1:
+            for p, sl, o in zip(w.parts, slices, outs):
+                st = o["status"] if o else np.zeros(0, np.int32)
+                rw = o["rows"] if o else np.zeros((0, 6), np.int64)
+                n_total = len(p.points) * (world if weak else 1)
+                S.gather_rows(st, rw, n_total, world, rank, device=cdev)
+        return outs
+
     for _ in range(max(1, args.warmup)):
-        eng.run(hp)
+        e2e_step()
     e2e_s = []
     torch.cuda.synchronize()
     if world > 1:
@@ -336,59 +454,106 @@ def run_ours(args):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        out = eng.run(hp)
-        if world > 1:
-            S.gather_rows(out["status"], out["rows"], n * world, world, rank, device=cdev)
+        outs = e2e_step()
         e2e_s.append(time.perf_counter() - t0)
-    e2e_step = sum(e2e_s) / len(e2e_s)
+    e2e_step_s = sum(e2e_s) / len(e2e_s)
     if world > 1:
-        t = torch.tensor([e2e_step], dtype=torch.float64, device=cdev)
+        t = torch.tensor([e2e_step_s], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_step = float(t.item())
-    h2d = sum(v.nbytes for v in pin.values())
-    d2h = out["status"].nbytes + out["rows"].nbytes
+        e2e_step_s = float(t.item())
+    h2d = sum(v.nbytes for sl in slices for v in sl.cols.values())
+    d2h = sum(o["status"].nbytes + o["rows"].nbytes for o in outs if o)
 
     kernel_ms = sum(k_ms) / len(k_ms)
-    bpu = bytes_per_unit(gs)
     peak, peak_src = measured_peak_hbm()
-    achieved = bpu * units_step / (kernel_ms / 1e3) / 1e9
-    traffic = profiled_traffic(args.workload) if not args.points else None   # (captured on the full grid)
+    alg_bytes = sum(bytes_per_unit(sl.eng.gs) * sl.units for sl in slices)
+    units_rank = sum(sl.units for sl in slices)
+    achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
+    prof = profiled(args.workload) if not args.points and world == 1 else None   # (captured on the full grid)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
-                "peak_source": peak_src, "kernel": "fl::sweep_kernel<1>",
-                "kernel_ms": kernel_ms, "algorithmic_bytes_per_unit": bpu,
-                "units_per_launch": units_step}
+                "traffic": prof.get("dram_bytes_per_launch") if prof else None,
+                "peak_source": peak_src, "kernel": "fl::sweep_kernel",
+                "kernel_ms": kernel_ms, "algorithmic_bytes_per_unit": alg_bytes / max(1, units_rank),
+                "units_per_launch": units_rank, "launches_per_step": launches // args.steps}
+    issue = None
+    if prof and prof.get("warp_inst_per_launch") and clocks.summary():
+        # issue-slot roofline: executed warp instructions (ncu) per second of kernel time against
+        # 148 SMs x 4 schedulers x 1 issue/clock at the measured SM clock
+        mhz = clocks.summary()["sm_mhz"]
+        ach = prof["warp_inst_per_launch"] / (kernel_ms / 1e3)
+        pk = 148 * 4 * mhz * 1e6
+        issue = {"bound": "issue", "achieved": ach, "peak": pk, "unit": "warp-inst/s", "frac": ach / pk,
+                 "warp_inst_per_launch": prof["warp_inst_per_launch"],
+                 "warp_inst_per_unit": prof["warp_inst_per_launch"] / units_rank,
+                 "source": prof.get("source")}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {**workload_desc(w, gs), "parallelism": f"dp{world} over design points",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {**workload_desc(w, gss),
+                       "parallelism": (f"dp{world} over design points: " +
+                                       ("every GPU the whole grid (efficiency variant k on GPU k)" if weak else
+                                        "each family's grid split into contiguous slices (sweep.shard), "
+                                        "one all-gather of the rows per step")),
                        "l2": "flushed before every timed step (256 MiB memset)",
                        "w_sched_equals_w": True},
             "roofline": roofline,
-            "e2e": {"value": world * units_step / e2e_step, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "e2e": {"value": units_job / e2e_step_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": launches, "clocks": clocks.summary()}
+    if issue:
+        line["roofline_issue"] = issue
+    if check:
+        line["rows_check"] = check
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import pyoracle as O
         O.build()
-        idxs = list(range(0, n, max(1, n // args.cpu_points)))[: args.cpu_points]
-        dt, rows = oracle_sample(graphs, w, idxs, 1)
-        got = d_rows.cpu().numpy()
-        if pts.efficiency[0] == 1.0:
+        jobs = sample_jobs(w, args.cpu_points)
+        dt, units, ok = 0.0, 0, 0
+        for k in range(len(w.parts)):
+            idx = [i for kk, i in jobs if kk == k]
+            if not idx:
+                continue
+            t, rows = oracle_rows(graphs[k], slices[k].pts, idx, 1)
+            dt += t
+            units += len(idx) * gss[k].units()
+            got = full[k][1]
             from paper_2604_17550_b200.engine import ROW_FIELDS
-            for i, r in zip(idxs, rows):
-                assert [int(x) for x in got[i]] == [r[k] for k in ROW_FIELDS], f"GPU/oracle mismatch at point {i}"
-        line["cpu_baseline"] = {"value": len(idxs) * gs.units() / dt, "unit": UNIT, "cores": 1, "kind": "port",
-                                "sample": f"{len(idxs)} of the {n} design points (every {n // len(idxs)}th), "
-                                          f"single thread, oracle/flint_oracle.c; rows checked equal to the GPU's",
-                                "seconds": dt, "cpu_model": _cpu_model()}
+            for i, r in zip(idx, rows):
+                assert [int(x) for x in got[i]] == [r[f] for f in ROW_FIELDS], f"GPU/oracle mismatch at {k}:{i}"
+                ok += 1
+        line["cpu_baseline"] = {"value": units / dt, "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": f"{len(jobs)} of the {w.n_points()} design points, spread evenly over "
+                                          f"the grid, single thread, oracle/flint_oracle.c; all {ok} rows checked "
+                                          f"equal to the GPU's", "seconds": dt, "cpu_model": _cpu_model()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def rows_check(args, w, full):
+    """Rows of the full grid (after the gather) against committed golden rows, when they exist."""
+    import numpy as np
+    if args.points:
+        return None
+    if args.workload == "c3":
+        fx = np.load(ROOT / "tests" / "golden" / "c3_grid_rows.npz")
+        bad = int((full[0][1] != fx["rows"]).any(1).sum())
+        if bad:
+            raise SystemExit(f"{bad} C3 rows differ from tests/golden/c3_grid_rows.npz")
+        return f"all {len(fx['rows'])} rows equal to tests/golden/c3_grid_rows.npz (oracle, full grid)"
+    if args.workload == "c4":
+        fx = json.loads((ROOT / "tests" / "golden" / "c4_golden.json").read_text())["grid"]
+        from paper_2604_17550_b200.engine import ROW_FIELDS
+        for r in fx:
+            got = [int(x) for x in full[r["part"]][1][r["point"]]]
+            if got != [r[f] for f in ROW_FIELDS]:
+                raise SystemExit(f"C4 row {r['part']}:{r['point']} differs from tests/golden/c4_golden.json")
+        return f"{len(fx)} rows equal to tests/golden/c4_golden.json (oracle at 8192 ranks)"
+    return None
 
 
 def main():
@@ -398,13 +563,18 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["c3", "c2", "c4"], default="c3")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="strong: the grid is split over the GPUs; weak: every GPU a whole grid")
     ap.add_argument("--points", type=int, default=0, help="evaluate an evenly spaced subset of the grid")
     ap.add_argument("--cpu-points", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dump-rows", default="", help="(tests) write the step's full-grid rows to this .npz")
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: W >= 3 warm-up steps are required by the bench contract; raising to 3")
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _spawn(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -45,7 +45,12 @@ enum { OR_OK = 0, OR_INVALID = 1, OR_DEADLOCK = 3, OR_UNSUPPORTED = 4, OR_INCONS
 typedef struct {
     int64_t n_ranks;
     const int64_t *rank_value;   /* [n_ranks], graphs list order              */
-    const int64_t *node_off;     /* [n_ranks+1] into the flat node arrays     */
+    const int64_t *node_off;     /* [n_ranks+1] flat node index of each rank  */
+    const int64_t *rank_base;    /* [n_ranks] first structure node of a rank  */
+    /* Per-node arrays below are indexed by STRUCTURE node (SV(G, flat)): ranks
+     * that share one node list (synth.py:331-335) share one copy, so a graph
+     * set costs O(structures), not O(R x N) -- and a full-world group list is
+     * stored once per structure node instead of R times (R x C x R at 8192). */
     const int64_t *node_id;
     const int32_t *node_kind;
     const int64_t *node_dur;     /* duration_ns, -1 for None                  */
@@ -57,9 +62,21 @@ typedef struct {
     const int64_t *coll_bytes;
     const int64_t *grp_off, *grp_rank;
     const int64_t *p2p_peer, *p2p_bytes, *p2p_tag;
-    const int64_t *tens_off;     /* [n_ranks+1] per-rank tensor table         */
+    const int64_t *tens_lo, *tens_hi;  /* [n_ranks] per-rank tensor table range */
     const int64_t *tens_id, *tens_bytes;
+    const int64_t *sv;           /* internal: flat node -> structure node (set by the entry points) */
 } or_graphs;
+
+#define SV(G, v) ((G)->sv[v])
+
+/* flat -> structure node map; the entry points run on a copy of G carrying it */
+static int64_t *build_sv(const or_graphs *G) {
+    int64_t nr = G->n_ranks, total = G->node_off[nr];
+    int64_t *sv = malloc((size_t)(total + 1) * sizeof(int64_t));
+    for (int64_t r = 0; r < nr; r++)
+        for (int64_t v = G->node_off[r]; v < G->node_off[r + 1]; v++) sv[v] = G->rank_base[r] + (v - G->node_off[r]);
+    return sv;
+}
 
 typedef struct {
     int32_t topo_kind;           /* 0 switch, 1 mesh2d */
@@ -144,11 +161,11 @@ int64_t or_duration_from_flops(int64_t flops, double peak, double eff) {
 
 /* simulator.py:109-114 */
 static int64_t coll_duration(const or_graphs *G, int64_t v, const or_config *cfg, int *st) {
-    int64_t n = G->grp_off[v + 1] - G->grp_off[v];
-    int64_t size = G->coll_kind[v] == C_AG ? G->coll_bytes[v] * n : G->coll_bytes[v];
+    int64_t n = G->grp_off[SV(G, v) + 1] - G->grp_off[SV(G, v)];
+    int64_t size = G->coll_kind[SV(G, v)] == C_AG ? G->coll_bytes[SV(G, v)] * n : G->coll_bytes[SV(G, v)];
     int mesh = cfg->topo_kind == 1;
     double beta = 1e9 / cfg->bw;
-    return or_analytical_time(G->coll_kind[v], size, n, cfg->algo, (double)cfg->latency, beta,
+    return or_analytical_time(G->coll_kind[SV(G, v)], size, n, cfg->algo, (double)cfg->latency, beta,
                               mesh ? cfg->rows : 0, mesh ? cfg->cols : 0, st);
 }
 
@@ -241,7 +258,7 @@ static int build_lookup(const or_graphs *G, lookup *L) {
     for (int64_t r = 0; r < nr; r++) {
         int64_t b = G->node_off[r], e = G->node_off[r + 1], c = e - b;
         int64_t *pp = malloc((size_t)(2 * c + 2) * sizeof(int64_t));
-        for (int64_t k = 0; k < c; k++) { pp[2 * k] = G->node_id[b + k]; pp[2 * k + 1] = b + k; }
+        for (int64_t k = 0; k < c; k++) { pp[2 * k] = G->node_id[SV(G, b + k)]; pp[2 * k + 1] = b + k; }
         qsort(pp, (size_t)c, 2 * sizeof(int64_t), cmp_i64);
         L->ids[r] = malloc((size_t)(c + 1) * sizeof(int64_t));
         L->flat[r] = malloc((size_t)(c + 1) * sizeof(int64_t));
@@ -273,7 +290,7 @@ static int match_instances(const or_graphs *G, const lookup *L, instances *I, in
     vec *colls = calloc((size_t)nr + 1, sizeof(vec));
     for (int64_t r = 0; r < nr; r++)
         for (int64_t v = G->node_off[r]; v < G->node_off[r + 1]; v++)
-            if (G->node_kind[v] == K_COLL) vpush(&colls[r], v);
+            if (G->node_kind[SV(G, v)] == K_COLL) vpush(&colls[r], v);
     int64_t *idx = calloc((size_t)nr + 1, sizeof(int64_t));
     vec off = {0}, mr = {0}, mn = {0}, lead = {0};
     vpush(&off, 0);
@@ -286,7 +303,7 @@ static int match_instances(const or_graphs *G, const lookup *L, instances *I, in
         }
         if (start < 0) break;
         int64_t lv = colls[start].a[idx[start]];
-        int64_t g0 = G->grp_off[lv], g1 = G->grp_off[lv + 1];
+        int64_t g0 = G->grp_off[SV(G, lv)], g1 = G->grp_off[SV(G, lv) + 1];
         /* members = [lead] + others in group order; pairs = zip(group, members) */
         vec members = {0};
         vpush(&members, lv);
@@ -300,11 +317,11 @@ static int match_instances(const or_graphs *G, const lookup *L, instances *I, in
                 set_err(err, errlen, m); rc = OR_INCONSISTENT; free(members.a); goto done;
             }
             int64_t ov = colls[r].a[idx[r]];
-            int same = G->coll_kind[ov] == G->coll_kind[lv] && G->coll_bytes[ov] == G->coll_bytes[lv] &&
-                       (G->grp_off[ov + 1] - G->grp_off[ov]) == (g1 - g0);
+            int same = G->coll_kind[SV(G, ov)] == G->coll_kind[SV(G, lv)] && G->coll_bytes[SV(G, ov)] == G->coll_bytes[SV(G, lv)] &&
+                       (G->grp_off[SV(G, ov) + 1] - G->grp_off[SV(G, ov)]) == (g1 - g0);
             if (same)
                 for (int64_t q = 0; q < g1 - g0; q++)
-                    if (G->grp_rank[G->grp_off[ov] + q] != G->grp_rank[g0 + q]) { same = 0; break; }
+                    if (G->grp_rank[G->grp_off[SV(G, ov)] + q] != G->grp_rank[g0 + q]) { same = 0; break; }
             if (!same) {
                 set_err(err, errlen, "collective disagrees across ranks");
                 rc = OR_INCONSISTENT; free(members.a); goto done;
@@ -346,19 +363,19 @@ static int pair_messages(const or_graphs *G, const lookup *L, message **out, int
     int64_t total = G->node_off[G->n_ranks];
     /* key rows: (src value, dst value, tag, is_recv, node_id, flat) */
     int64_t cnt = 0;
-    for (int64_t v = 0; v < total; v++) if (G->node_kind[v] == K_SEND || G->node_kind[v] == K_RECV) cnt++;
+    for (int64_t v = 0; v < total; v++) if (G->node_kind[SV(G, v)] == K_SEND || G->node_kind[SV(G, v)] == K_RECV) cnt++;
     int64_t *rows = malloc((size_t)(cnt * 6 + 6) * sizeof(int64_t));
     int64_t k = 0;
     for (int64_t r = 0; r < G->n_ranks; r++)
         for (int64_t v = G->node_off[r]; v < G->node_off[r + 1]; v++) {
-            int kd = G->node_kind[v];
+            int kd = G->node_kind[SV(G, v)];
             if (kd != K_SEND && kd != K_RECV) continue;
             int64_t *row = rows + 6 * k++;
-            row[0] = kd == K_SEND ? G->rank_value[r] : G->p2p_peer[v];
-            row[1] = kd == K_SEND ? G->p2p_peer[v] : G->rank_value[r];
-            row[2] = G->p2p_tag[v];
+            row[0] = kd == K_SEND ? G->rank_value[r] : G->p2p_peer[SV(G, v)];
+            row[1] = kd == K_SEND ? G->p2p_peer[SV(G, v)] : G->rank_value[r];
+            row[2] = G->p2p_tag[SV(G, v)];
             row[3] = kd == K_RECV;
-            row[4] = G->node_id[v];
+            row[4] = G->node_id[SV(G, v)];
             row[5] = v;
         }
     /* lexicographic sort of 6-wide rows: simple insertion-free approach via qsort on index */
@@ -384,7 +401,7 @@ static int pair_messages(const or_graphs *G, const lookup *L, message **out, int
         /* sends come first (is_recv=0), each sorted by node id */
         for (int64_t q = 0; q < ns; q++) {
             int64_t sv = rows[6 * (i + q) + 5], rv = rows[6 * (i + ns + q) + 5];
-            msgs[nm].send = sv; msgs[nm].recv = rv; msgs[nm].nbytes = G->p2p_bytes[sv];
+            msgs[nm].send = sv; msgs[nm].recv = rv; msgs[nm].nbytes = G->p2p_bytes[SV(G, sv)];
             msgs[nm].send_t = -1; msgs[nm].recv_t = -1;
             msg_of[sv] = nm; msg_of[rv] = nm;
             nm++;
@@ -461,7 +478,7 @@ static int cmp_memev(const void *x, const void *y) {
 /* simulator.py:370-393 */
 static int64_t peak_mem(const or_graphs *G, int64_t r, const int64_t *st, const int64_t *en, int64_t finish) {
     int64_t b = G->node_off[r], e = G->node_off[r + 1];
-    int64_t t0 = G->tens_off[r], t1 = G->tens_off[r + 1], nt = t1 - t0;
+    int64_t t0 = G->tens_lo[r], t1 = G->tens_hi[r], nt = t1 - t0;
     if (nt <= 0) return 0;
     /* tensor ids of this rank's table, sorted for lookup */
     int64_t *tid = malloc((size_t)(2 * nt + 2) * sizeof(int64_t));
@@ -473,11 +490,11 @@ static int64_t peak_mem(const or_graphs *G, int64_t r, const int64_t *st, const 
     int64_t *alloc = malloc((size_t)(nt + 1) * sizeof(int64_t)), *freet = malloc((size_t)(nt + 1) * sizeof(int64_t));
     char *hasp = calloc((size_t)nt + 1, 1), *hasc = calloc((size_t)nt + 1, 1);
     for (int64_t v = b; v < e; v++) {
-        for (int64_t q = G->out_off[v]; q < G->out_off[v + 1]; q++) {   /* producer[t] = last */
+        for (int64_t q = G->out_off[SV(G, v)]; q < G->out_off[SV(G, v) + 1]; q++) {   /* producer[t] = last */
             int64_t p = find_sorted(keys, nt, G->out_tid[q]);
             if (p >= 0) { alloc[pos[p]] = st[v]; hasp[pos[p]] = 1; }
         }
-        for (int64_t q = G->in_off[v]; q < G->in_off[v + 1]; q++) {
+        for (int64_t q = G->in_off[SV(G, v)]; q < G->in_off[SV(G, v) + 1]; q++) {
             int64_t p = find_sorted(keys, nt, G->in_tid[q]);
             if (p >= 0) {
                 int64_t k = pos[p];
@@ -517,7 +534,17 @@ static int64_t wake_time(const rank_state *R, int ncs) {
     return w;
 }
 
-int or_simulate(const or_graphs *G, const or_config *cfg, or_sim_out *out, char *err, int errlen) {
+static int simulate_impl(const or_graphs *G, const or_config *cfg, or_sim_out *out, char *err, int errlen);
+int or_simulate(const or_graphs *G0, const or_config *cfg, or_sim_out *out, char *err, int errlen) {
+    or_graphs g = *G0;
+    int64_t *sv = build_sv(G0);
+    g.sv = sv;
+    int rc = simulate_impl(&g, cfg, out, err, errlen);
+    free(sv);
+    return rc;
+}
+
+static int simulate_impl(const or_graphs *G, const or_config *cfg, or_sim_out *out, char *err, int errlen) {
     int64_t nr = G->n_ranks, total = G->node_off[nr];
     int ncs = cfg->compute_streams, nms = cfg->comm_streams;
     if (ncs < 1 || nms < 1) { set_err(err, errlen, "stream counts must be >= 1"); return OR_INVALID; }
@@ -533,9 +560,9 @@ int or_simulate(const or_graphs *G, const or_config *cfg, or_sim_out *out, char 
     int64_t *tmp = NULL; int64_t tmpcap = 0;
     vec edges = {0};   /* (dep flat, node flat) in iteration order */
     for (int64_t v = 0; v < total; v++) {
-        int64_t n = G->dep_off[v + 1] - G->dep_off[v];
+        int64_t n = G->dep_off[SV(G, v) + 1] - G->dep_off[SV(G, v)];
         if (n > tmpcap) { tmpcap = n; tmp = realloc(tmp, (size_t)tmpcap * sizeof(int64_t)); }
-        memcpy(tmp, G->dep_ids + G->dep_off[v], (size_t)n * sizeof(int64_t));
+        memcpy(tmp, G->dep_ids + G->dep_off[SV(G, v)], (size_t)n * sizeof(int64_t));
         qsort(tmp, (size_t)n, sizeof(int64_t), cmp_i64);
         int64_t u = 0;
         for (int64_t k = 0; k < n; k++) if (k == 0 || tmp[k] != tmp[k - 1]) tmp[u++] = tmp[k];
@@ -598,14 +625,14 @@ int or_simulate(const or_graphs *G, const or_config *cfg, or_sim_out *out, char 
     int64_t done = 0;
     int64_t *links = malloc((size_t)(4 + 2 * (cfg->rows + cfg->cols) + 2) * sizeof(int64_t));
 
-#define FINISH(v, s_, e_) do { st[v] = (s_); en[v] = (e_); int64_t k_[4] = {(e_), G->rank_value[rank_of[v]], G->node_id[v], (v)}; hpush(&ev, k_); } while (0)
+#define FINISH(v, s_, e_) do { st[v] = (s_); en[v] = (e_); int64_t k_[4] = {(e_), G->rank_value[rank_of[v]], G->node_id[SV(G, v)], (v)}; hpush(&ev, k_); } while (0)
 #define REWAKE(r) do { int64_t w_ = wake_time(&RS[r], ncs); RS[r].wake_version++; if (w_ != INT64_MAX) { int64_t k_[3] = {w_, (r), RS[r].wake_version}; hpush(&wake, k_); } } while (0)
 
     /* dispatch (simulator.py:247-268) */
 #define DISPATCH(v, now_) do { \
-        int64_t r_ = rank_of[v]; int kd_ = G->node_kind[v]; \
-        if (kd_ == K_HOST) { int64_t k_[2] = {G->node_id[v], (v)}; hpush(&RS[r_].host_ready, k_); REWAKE(r_); } \
-        else if (kd_ == K_COMP) { int64_t k_[2] = {G->node_id[v], (v)}; hpush(&RS[r_].comp_ready, k_); REWAKE(r_); } \
+        int64_t r_ = rank_of[v]; int kd_ = G->node_kind[SV(G, v)]; \
+        if (kd_ == K_HOST) { int64_t k_[2] = {G->node_id[SV(G, v)], (v)}; hpush(&RS[r_].host_ready, k_); REWAKE(r_); } \
+        else if (kd_ == K_COMP) { int64_t k_[2] = {G->node_id[SV(G, v)], (v)}; hpush(&RS[r_].comp_ready, k_); REWAKE(r_); } \
         else if (kd_ == K_COLL) { int64_t i_ = inst_of[v]; inst_wait[i_]--; if ((now_) > inst_ready[i_]) inst_ready[i_] = (now_); \
             if (inst_wait[i_] == 0) vpush(&pend_c, i_); } \
         else { int64_t m_ = msg_of[v]; \
@@ -627,7 +654,7 @@ int or_simulate(const or_graphs *G, const or_config *cfg, or_sim_out *out, char 
             rank_state *R = &RS[r];
             while (R->host_ready.n && R->host_slot <= now) {
                 hpop(&R->host_ready, tmpk);
-                int64_t v = tmpk[1], d = G->node_dur[v] < 0 ? 0 : G->node_dur[v];
+                int64_t v = tmpk[1], d = G->node_dur[SV(G, v)] < 0 ? 0 : G->node_dur[SV(G, v)];
                 R->host_slot = now + d;
                 FINISH(v, now, now + d);
             }
@@ -636,7 +663,7 @@ int or_simulate(const or_graphs *G, const or_config *cfg, or_sim_out *out, char 
                 for (int q = 1; q < ncs; q++) if (R->comp_slots[q] < R->comp_slots[k]) k = q;
                 if (R->comp_slots[k] > now) break;
                 hpop(&R->comp_ready, tmpk);
-                int64_t v = tmpk[1], d = G->node_dur[v] < 0 ? 0 : G->node_dur[v];
+                int64_t v = tmpk[1], d = G->node_dur[SV(G, v)] < 0 ? 0 : G->node_dur[SV(G, v)];
                 R->comp_slots[k] = now + d;
                 FINISH(v, now, now + d);
             }
@@ -648,7 +675,7 @@ int or_simulate(const or_graphs *G, const or_config *cfg, or_sim_out *out, char 
                 while (b >= 0) {
                     int64_t y = pend_c.a[b];
                     int gt = inst_ready[y] > inst_ready[x] ||
-                             (inst_ready[y] == inst_ready[x] && G->node_id[I.lead[y]] > G->node_id[I.lead[x]]);
+                             (inst_ready[y] == inst_ready[x] && G->node_id[SV(G, I.lead[y])] > G->node_id[SV(G, I.lead[x])]);
                     if (!gt) break;
                     pend_c.a[b + 1] = y; b--;
                 }
@@ -675,11 +702,11 @@ int or_simulate(const or_graphs *G, const or_config *cfg, or_sim_out *out, char 
                 int64_t x = pend_m.a[a], b = a - 1;
                 message *mx = &msgs[x];
                 int64_t kx0 = mx->send_t > mx->recv_t ? mx->send_t : mx->recv_t;
-                int64_t kx1 = G->rank_value[rank_of[mx->send]], kx2 = G->node_id[mx->send];
+                int64_t kx1 = G->rank_value[rank_of[mx->send]], kx2 = G->node_id[SV(G, mx->send)];
                 while (b >= 0) {
                     message *my = &msgs[pend_m.a[b]];
                     int64_t ky0 = my->send_t > my->recv_t ? my->send_t : my->recv_t;
-                    int64_t ky1 = G->rank_value[rank_of[my->send]], ky2 = G->node_id[my->send];
+                    int64_t ky1 = G->rank_value[rank_of[my->send]], ky2 = G->node_id[SV(G, my->send)];
                     int gt = ky0 > kx0 || (ky0 == kx0 && (ky1 > kx1 || (ky1 == kx1 && ky2 > kx2)));
                     if (!gt) break;
                     pend_m.a[b + 1] = pend_m.a[b]; b--;
@@ -727,7 +754,7 @@ loop_end:
         for (int64_t r = 0; r < nr; r++) {
             int64_t nc = 0, fin = 0;
             for (int64_t v = G->node_off[r]; v < G->node_off[r + 1]; v++) {
-                if (G->node_kind[v] == K_COMP) { cbuf[nc].s = st[v]; cbuf[nc].e = en[v]; nc++; }
+                if (G->node_kind[SV(G, v)] == K_COMP) { cbuf[nc].s = st[v]; cbuf[nc].e = en[v]; nc++; }
                 if (en[v] > fin) fin = en[v];
             }
             nc = merge_iv(cbuf, nc);
@@ -768,8 +795,20 @@ cleanup:
 /* critical_path, optionally with every node's finish and start, its collective
  * instance (-1: none) and, for a RECV, its SEND (-1: none) -- the inputs of the
  * node-trace rule in pyoracle.critical_path_trace.  Flat node order. */
-int or_critical_path_ex(const or_graphs *G, const or_config *cfg, int64_t *result, int64_t *node_fin,
+static int critical_path_impl(const or_graphs *G, const or_config *cfg, int64_t *result, int64_t *node_fin,
+                              int64_t *node_start, int64_t *node_inst, int64_t *node_send, char *err, int errlen);
+int or_critical_path_ex(const or_graphs *G0, const or_config *cfg, int64_t *result, int64_t *node_fin,
                         int64_t *node_start, int64_t *node_inst, int64_t *node_send, char *err, int errlen) {
+    or_graphs g = *G0;
+    int64_t *sv = build_sv(G0);
+    g.sv = sv;
+    int rc = critical_path_impl(&g, cfg, result, node_fin, node_start, node_inst, node_send, err, errlen);
+    free(sv);
+    return rc;
+}
+
+static int critical_path_impl(const or_graphs *G, const or_config *cfg, int64_t *result, int64_t *node_fin,
+                              int64_t *node_start, int64_t *node_inst, int64_t *node_send, char *err, int errlen) {
     int64_t nr = G->n_ranks, total = G->node_off[nr];
     lookup L;
     if (build_lookup(G, &L)) { free_lookup(&L); set_err(err, errlen, "duplicate rank in graphs"); return OR_INVALID; }
@@ -793,7 +832,7 @@ int or_critical_path_ex(const or_graphs *G, const or_config *cfg, int64_t *resul
     vert_of = malloc((size_t)(total + 1) * sizeof(int64_t));
     for (int64_t v = 0; v < total; v++) vert_of[v] = inst_of[v] >= 0 ? total + inst_of[v] : v;
     vdur = calloc((size_t)nv + 1, sizeof(int64_t));
-    for (int64_t v = 0; v < total; v++) vdur[v] = G->node_dur[v] < 0 ? 0 : G->node_dur[v];
+    for (int64_t v = 0; v < total; v++) vdur[v] = G->node_dur[SV(G, v)] < 0 ? 0 : G->node_dur[SV(G, v)];
     for (int64_t i = 0; i < I.n_inst; i++) {
         int s2;
         vdur[total + i] = coll_duration(G, I.lead[i], cfg, &s2);
@@ -808,11 +847,11 @@ int or_critical_path_ex(const or_graphs *G, const or_config *cfg, int64_t *resul
         vec *pv = calloc((size_t)nv + 1, sizeof(vec));
         for (int64_t v = 0; v < total; v++) {
             int64_t w = vert_of[v];
-            for (int64_t q = G->dep_off[v]; q < G->dep_off[v + 1]; q++) {
+            for (int64_t q = G->dep_off[SV(G, v)]; q < G->dep_off[SV(G, v) + 1]; q++) {
                 int64_t d = node_index(&L, rank_of[v], G->dep_ids[q]);
                 vpush(&pv[w], d >= 0 ? d : -(++dangling_tag));   /* dangling dep: never finishes */
             }
-            if (G->node_kind[v] == K_RECV && msg_of[v] >= 0) vpush(&pv[w], msgs[msg_of[v]].send);
+            if (G->node_kind[SV(G, v)] == K_RECV && msg_of[v] >= 0) vpush(&pv[w], msgs[msg_of[v]].send);
         }
         indeg = calloc((size_t)nv + 1, sizeof(int64_t));
         vec edges = {0};
@@ -844,7 +883,7 @@ int or_critical_path_ex(const or_graphs *G, const or_config *cfg, int64_t *resul
     while (qh < qt) {
         int64_t w = queue[qh++];
         int64_t start = vstart[w];
-        if (w < total && G->node_kind[w] == K_RECV && msg_of[w] >= 0) {   /* :450-452 */
+        if (w < total && G->node_kind[SV(G, w)] == K_RECV && msg_of[w] >= 0) {   /* :450-452 */
             message *M = &msgs[msg_of[w]];
             int64_t sv = G->rank_value[rank_of[M->send]], dv = G->rank_value[rank_of[M->recv]];
             int64_t wire = vfin[vert_of[M->send]] + transfer_ns(cfg, sv, dv, M->nbytes);
@@ -882,7 +921,7 @@ int or_critical_path_ex(const or_graphs *G, const or_config *cfg, int64_t *resul
                 node_fin[v] = vfin[vert_of[v]];
                 node_start[v] = vstart[vert_of[v]];
                 node_inst[v] = inst_of[v];
-                node_send[v] = (G->node_kind[v] == K_RECV && msg_of[v] >= 0) ? msgs[msg_of[v]].send : -1;
+                node_send[v] = (G->node_kind[SV(G, v)] == K_RECV && msg_of[v] >= 0) ? msgs[msg_of[v]].send : -1;
             }
     }
     free(vstart); free(queue); free(live);

@@ -43,12 +43,12 @@ P32 = C.POINTER(C.c_int32)
 
 
 class OrGraphs(C.Structure):
-    _fields_ = [("n_ranks", C.c_int64), ("rank_value", P), ("node_off", P), ("node_id", P),
+    _fields_ = [("n_ranks", C.c_int64), ("rank_value", P), ("node_off", P), ("rank_base", P), ("node_id", P),
                 ("node_kind", P32), ("node_dur", P), ("dep_off", P), ("dep_ids", P),
                 ("in_off", P), ("in_tid", P), ("out_off", P), ("out_tid", P),
                 ("coll_kind", P32), ("coll_bytes", P), ("grp_off", P), ("grp_rank", P),
                 ("p2p_peer", P), ("p2p_bytes", P), ("p2p_tag", P),
-                ("tens_off", P), ("tens_id", P), ("tens_bytes", P)]
+                ("tens_lo", P), ("tens_hi", P), ("tens_id", P), ("tens_bytes", P), ("sv", P)]
 
 
 class OrConfig(C.Structure):
@@ -122,35 +122,51 @@ def _flatten_nodes(nodes) -> dict:
 
 
 def flatten(graphs) -> dict:
-    """Concatenate per-rank arrays; structures shared by identity are flattened once."""
-    cache: dict = {}
-    parts, tparts = [], []
+    """Per-structure node tables plus a per-rank index into them.
+
+    Ranks whose graphs share one node list (by identity, as synth emits,
+    synth.py:331-335) share one copy of the node arrays, group lists included,
+    and likewise for tensor tables.  The C side maps a flat (rank, position)
+    node to its structure node (``SV`` in flint_oracle.c), so memory is
+    O(R + structures) instead of O(R x N) -- and O(R x C x R) for full-world
+    group lists, which at 8192 ranks would be ~120 GiB."""
+    scache: dict = {}
+    tcache: dict = {}
+    sparts, tparts = [], []
+    rank_base, node_count, tens_lo, tens_hi = [], [], [], []
+    sbase = tbase = 0
     for g in graphs:
         key = id(g.nodes)
-        if key not in cache:
-            cache[key] = _flatten_nodes(g.nodes)
-        parts.append(cache[key])
+        if key not in scache:
+            part = _flatten_nodes(g.nodes)
+            scache[key] = (sbase, len(part["node_id"]))
+            sparts.append(part)
+            sbase += len(part["node_id"])
+        b, c = scache[key]
+        rank_base.append(b); node_count.append(c)
         tk = id(g.tensors)
-        if tk not in cache:
+        if tk not in tcache:
             items = list(g.tensors.items())
-            cache[tk] = (np.asarray([k for k, _ in items], np.int64),
-                         np.asarray([t.bytes for _, t in items], np.int64))
-        tparts.append(cache[tk])
-    out = {"n_ranks": len(graphs), "rank_value": np.asarray([g.rank for g in graphs], np.int64)}
-    counts = np.asarray([len(p["node_id"]) for p in parts], np.int64)
-    out["node_off"] = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+            tcache[tk] = (tbase, tbase + len(items))
+            tparts.append((np.asarray([k for k, _ in items], np.int64),
+                           np.asarray([t.bytes for _, t in items], np.int64)))
+            tbase += len(items)
+        lo, hi = tcache[tk]
+        tens_lo.append(lo); tens_hi.append(hi)
+    i64 = lambda a: np.asarray(a, np.int64)
+    out = {"n_ranks": len(graphs), "rank_value": i64([g.rank for g in graphs]),
+           "node_off": np.concatenate([[0], np.cumsum(i64(node_count))]).astype(np.int64),
+           "rank_base": i64(rank_base), "tens_lo": i64(tens_lo), "tens_hi": i64(tens_hi)}
     for name in ("node_id", "node_kind", "node_dur", "coll_kind", "coll_bytes", "p2p_peer", "p2p_bytes", "p2p_tag"):
-        out[name] = np.concatenate([p[name] for p in parts]) if parts else np.zeros(0, np.int64)
+        out[name] = np.concatenate([p[name] for p in sparts]) if sparts else np.zeros(0, np.int64)
     for off, val in (("dep_off", "dep_ids"), ("in_off", "in_tid"), ("out_off", "out_tid"), ("grp_off", "grp_rank")):
         vals, offs, base = [], [np.zeros(1, np.int64)], 0
-        for p in parts:
+        for p in sparts:
             vals.append(p[val])
             offs.append(p[off][1:] + base)
             base += len(p[val])
         out[val] = np.concatenate(vals) if vals else np.zeros(0, np.int64)
         out[off] = np.concatenate(offs).astype(np.int64)
-    tcounts = np.asarray([len(t[0]) for t in tparts], np.int64)
-    out["tens_off"] = np.concatenate([[0], np.cumsum(tcounts)]).astype(np.int64)
     out["tens_id"] = np.concatenate([t[0] for t in tparts]) if tparts else np.zeros(0, np.int64)
     out["tens_bytes"] = np.concatenate([t[1] for t in tparts]) if tparts else np.zeros(0, np.int64)
     for k, v in out.items():
@@ -159,10 +175,18 @@ def flatten(graphs) -> dict:
     return out
 
 
+def structure_index(flat: dict) -> np.ndarray:
+    """flat node -> structure node (the C side's SV map)."""
+    node_off = flat["node_off"]
+    counts = np.diff(node_off)
+    rank_of = np.repeat(np.arange(len(counts)), counts)
+    return flat["rank_base"][rank_of] + (np.arange(int(node_off[-1])) - node_off[rank_of])
+
+
 def _struct(flat: dict) -> OrGraphs:
     g = OrGraphs()
     g.n_ranks = flat["n_ranks"]
-    for name, typ in OrGraphs._fields_[1:]:
+    for name, typ in OrGraphs._fields_[1:-1]:
         arr = flat[name]
         if len(arr) == 0:
             arr = np.zeros(1, arr.dtype)
@@ -260,7 +284,9 @@ def critical_path_trace(graphs, topo, algo="ring", flat=None):
         raise OracleError(rc, err.value.decode())
     if total == 0:
         return int(res.value), []
-    node_off, node_id, rank_value = flat["node_off"], flat["node_id"], flat["rank_value"]
+    node_off, rank_value = flat["node_off"], flat["rank_value"]
+    sv = structure_index(flat)
+    node_id = flat["node_id"][sv]
     rank_of = np.repeat(np.arange(len(rank_value)), np.diff(node_off))
     index = {(int(rank_of[v]), int(node_id[v])): v for v in range(total)}
     members = {}
@@ -276,7 +302,7 @@ def critical_path_trace(graphs, topo, algo="ring", flat=None):
         out = set()
         for m in (members[int(inst[v])] if inst[v] >= 0 else [v]):
             r = int(rank_of[m])
-            for q in range(int(dep_off[m]), int(dep_off[m + 1])):
+            for q in range(int(dep_off[sv[m]]), int(dep_off[sv[m] + 1])):
                 out.add(index[(r, int(dep_ids[q]))])
         return out
 

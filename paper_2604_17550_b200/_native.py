@@ -130,8 +130,16 @@ class Outputs(C.Structure):
 _lib = None
 
 
+def _header_abi_version() -> int:
+    for line in (ROOT / "include" / "flint_b200.h").read_text().splitlines():
+        if line.startswith("#define FL_ABI_VERSION"):
+            return int(line.split()[2])
+    raise EngineError("include/flint_b200.h has no FL_ABI_VERSION")
+
+
 def lib():
-    """Load the engine (building it first if this is a source checkout)."""
+    """Load the engine, (re)building it first when the in-tree library is missing or older than
+    its sources, and refuse a library whose ABI version differs from include/flint_b200.h."""
     global _lib
     if _lib is not None:
         return _lib
@@ -139,12 +147,19 @@ def lib():
     if override:
         _lib = _bind(C.CDLL(override))
         return _lib
-    if not LIB.exists():
+    stale = LIB.exists() and all(p.exists() for p in SOURCES + HEADERS) and \
+        LIB.stat().st_mtime < max(p.stat().st_mtime for p in SOURCES + HEADERS)
+    if not LIB.exists() or stale:
         try:
             build()
         except (OSError, EngineError) as e:
-            raise EngineError(f"CUDA engine library {LIB} is missing and could not be built: {e}") from e
-    _lib = _bind(C.CDLL(str(LIB)))
+            raise EngineError(f"CUDA engine library {LIB} is {'stale' if stale else 'missing'} and could not "
+                              f"be built: {e}") from e
+    L = _bind(C.CDLL(str(LIB)))
+    want = _header_abi_version()
+    if L.fl_version() != want:
+        raise EngineError(f"{LIB} has ABI version {L.fl_version()}, include/flint_b200.h {want}: rebuild it")
+    _lib = L
     return _lib
 
 

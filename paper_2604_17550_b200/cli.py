@@ -14,7 +14,7 @@ import argparse
 import sys
 import time
 
-from .errors import TrainsimError, UnsupportedAlgoTopologyError, UnsupportedComboError
+from .errors import EngineError, TrainsimError, UnsupportedAlgoTopologyError, UnsupportedComboError
 from .synth import PRESETS, FsdpMode
 
 USAGE_ERROR = 1
@@ -56,9 +56,10 @@ def _devices(args):
         return [int(x) for x in args.devices.split(",") if x.strip()]
     if args.jobs > 1:
         from . import _native
-        n = min(args.jobs, _native.device_count())
-        if n > 1:
-            return list(range(n))
+        present = _native.device_count()
+        ids = [(args.device + k) % present for k in range(min(args.jobs, present))] if present else []
+        if len(ids) > 1:
+            return ids       # starting at --device, wrapping over the GPUs present
     return None
 
 
@@ -85,6 +86,9 @@ def main(argv=None) -> int:
         print(f"error: {e}", file=sys.stderr)
         return USAGE_ERROR
     except TrainsimError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return VALIDATION_ERROR
+    except EngineError as e:      # engine limits (ranks, nodes, streams, ...) or no usable GPU
         print(f"error: {e}", file=sys.stderr)
         return VALIDATION_ERROR
 

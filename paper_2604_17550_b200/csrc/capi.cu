@@ -147,6 +147,22 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     UP(msg_recv_node, d->n_msg);
     UP(msg_bytes, d->n_msg);
     UP(msg_send_id, d->n_msg);
+    if (d->n_msg > 0 || dg.p2p_stride > 1) {
+        // every SEND/RECV must be paired (simulator.py:177-200); an unmatched channel would make the
+        // kernel index message -1, so refuse it here (the Python layer raises DeadlockError first)
+        std::vector<int> s_p2p(S, 0);
+        for (int s = 0; s < S; s++)
+            for (int i = d->s_node_off[s]; i < d->s_node_off[s + 1]; i++)
+                s_p2p[s] += d->node_kind[i] == FL_SEND || d->node_kind[i] == FL_RECV;
+        for (int r = 0; r < R; r++) {
+            const int c = s_p2p[d->rank_struct[r]];
+            if (c > dg.p2p_stride) return fail(FL_ERR_INVALID, "p2p_stride below a rank's SEND/RECV count");
+            for (int q = 0; q < c; q++) {
+                const int m = d->rank_p2p_msg[(size_t)r * dg.p2p_stride + q];
+                if (m < 0 || m >= d->n_msg) return fail(FL_ERR_DEADLOCK, "a SEND/RECV has no matching peer (unmatched channel)");
+            }
+        }
+    }
     {
         int rc = upload(g, d->rank_p2p_msg, (size_t)R * dg.p2p_stride, &dg.rank_p2p_msg);
         if (rc) return rc;

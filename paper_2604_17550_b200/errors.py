@@ -81,6 +81,36 @@ _STATUS_EXC = {
 }
 
 
+REFERENCE_NAMES = ("TrainsimError", "FormatError", "UnresolvedReferenceError", "MissingShapeError",
+                   "UnknownOperatorError", "CyclicGraphError", "InvalidGraphError", "UnsupportedComboError",
+                   "UnsupportedAlgoTopologyError", "InconsistentGroupsError", "DeadlockError", "RankMismatchError")
+
+
+def _adopt_reference_classes() -> bool:
+    """A caller switching from the reference catches ``trainsim.errors`` classes
+    (errors.py:4-55).  When that package is importable, this module re-exports
+    the reference's own classes, so every exception raised here *is* the
+    reference's type.  ``FLINT_OWN_ERRORS=1`` keeps the local tree."""
+    import os
+    if os.environ.get("FLINT_OWN_ERRORS") == "1":
+        return False
+    try:
+        from trainsim import errors as ref
+    except Exception:       # not installed: keep the identical local tree above
+        return False
+    if not all(hasattr(ref, n) for n in REFERENCE_NAMES):
+        return False
+    g = globals()
+    for n in REFERENCE_NAMES:
+        g[n] = getattr(ref, n)
+    _STATUS_EXC.update({FL_ERR_DEADLOCK: ref.DeadlockError, FL_ERR_UNSUPPORTED_ALGO: ref.UnsupportedAlgoTopologyError,
+                        FL_ERR_INCONSISTENT: ref.InconsistentGroupsError})
+    return True
+
+
+USING_REFERENCE_CLASSES = _adopt_reference_classes()
+
+
 def raise_for_status(code: int, what: str = "") -> None:
     if code == FL_OK:
         return

@@ -54,13 +54,39 @@ def latency_grid(lo_ns: float, hi_ns: float, n: int) -> np.ndarray:
 
 
 @dataclass
-class Workload:
-    """A named BASELINE configuration: one graph family x a design-point grid."""
-    name: str
-    model: str
+class WorkloadPart:
+    """One graph family of a workload and the design points evaluated on it."""
     parallel: str
     points: DesignPoints
     labels: list               # (topology kind, algo) per point, for reporting
+
+
+@dataclass
+class Workload:
+    """A named BASELINE configuration: graph families x design-point grids.
+
+    A step of the bench evaluates every part (one engine launch per graph
+    family); single-family workloads expose ``parallel``/``points`` directly."""
+    name: str
+    model: str
+    parts: list
+
+    @property
+    def parallel(self) -> str:
+        return self.parts[0].parallel if len(self.parts) == 1 else ",".join(p.parallel for p in self.parts)
+
+    @property
+    def points(self) -> DesignPoints:
+        assert len(self.parts) == 1, "multi-family workload: use .parts"
+        return self.parts[0].points
+
+    @points.setter
+    def points(self, pts: DesignPoints) -> None:
+        assert len(self.parts) == 1, "multi-family workload: use .parts"
+        self.parts[0].points = pts
+
+    def n_points(self) -> int:
+        return sum(len(p.points) for p in self.parts)
 
 
 def _grid(pairs, bws, lats, rows_cols) -> DesignPoints:
@@ -77,41 +103,53 @@ def _grid(pairs, bws, lats, rows_cols) -> DesignPoints:
                         np.asarray(lat, np.int64), np.asarray(rows, np.int32), np.asarray(cols, np.int32))
 
 
+def _part(parallel, pairs, bws, lats, rows_cols) -> WorkloadPart:
+    return WorkloadPart(parallel, _grid(pairs, bws, lats, rows_cols),
+                        [p for p in pairs for _ in range(len(bws) * len(lats))])
+
+
 def c3_workload() -> Workload:
     """BASELINE config 3: llama-8b-like fsdp:1024, 4096 points =
     {switch:1024 + ring, mesh:32x32 + mesh-hier} x 64 bandwidths in
     [10 GB/s, 1.8 TB/s] x 32 latencies in [100 ns, 20 us] (log-spaced)."""
     pairs = [("switch", "ring"), ("mesh", "mesh-hier")]
-    pts = _grid(pairs, log_grid(10e9, 1.8e12, 64), latency_grid(100, 20000, 32), (32, 32))
-    return Workload("c3", "llama-8b-like", "fsdp:1024", pts, [p for p in pairs for _ in range(64 * 32)])
+    return Workload("c3", "llama-8b-like", [_part("fsdp:1024", pairs, log_grid(10e9, 1.8e12, 64),
+                                                  latency_grid(100, 20000, 32), (32, 32))])
 
 
 def c2_workload() -> Workload:
     """BASELINE config 2: GPT-2 small dp:64, 256 points = {ring, tree} x 16
     bandwidths in [10 GB/s, 1.8 TB/s] x 8 latencies in [100 ns, 10 us]."""
     pairs = [("switch", "ring"), ("switch", "tree")]
-    pts = _grid(pairs, log_grid(10e9, 1.8e12, 16), latency_grid(100, 10000, 8), (0, 0))
-    return Workload("c2", "gpt2-small", "dp:64", pts, [p for p in pairs for _ in range(16 * 8)])
+    return Workload("c2", "gpt2-small", [_part("dp:64", pairs, log_grid(10e9, 1.8e12, 16),
+                                               latency_grid(100, 10000, 8), (0, 0))])
 
 
 def c4_workload() -> Workload:
-    """BASELINE config 4 at its rank count: 8192 ranks, 16384 points =
-    {switch:8192 + ring, mesh:64x128 + mesh-hier} x 128 bandwidths in
-    [10 GB/s, 1.8 TB/s] x 64 latencies in [100 ns, 20 us].  The reference's
-    synthesizer has no pipeline/3-D strategy (synth.py:29-32 in this package,
-    trainsim synth.py), so the graph is its largest family at that scale:
-    llama-70b-like fsdp:8192 (2080 nodes per rank).  A design point spans a
-    cluster of 8 CTAs."""
-    pairs = [("switch", "ring"), ("mesh", "mesh-hier")]
-    pts = _grid(pairs, log_grid(10e9, 1.8e12, 128), latency_grid(100, 20000, 64), (64, 128))
-    return Workload("c4", "llama-70b-like", "fsdp:8192", pts, [p for p in pairs for _ in range(128 * 64)])
+    """BASELINE config 4 as SURVEY.md 8(d) defines it: llama-70b-like at 8192
+    ranks, 16384 points = {dp:8192 + switch ring, dp:8192 + switch tree,
+    dp:8192 + mesh:64x128 mesh-hier, fsdp:8192 + mesh:64x128 mesh-hier} x 64
+    bandwidths in [10 GB/s, 1.8 TB/s] x 64 latencies in [100 ns, 20 us].
+    Two graph families (dp: 1760 nodes per rank, fsdp: 2080), one engine
+    launch each; a design point spans a cluster of 8 CTAs.  The pipeline /
+    3-D part of the BASELINE wording is not expressible in the reference
+    (synth.py:172-181)."""
+    bws, lats = log_grid(10e9, 1.8e12, 64), latency_grid(100, 20000, 64)
+    return Workload("c4", "llama-70b-like", [
+        _part("dp:8192", [("switch", "ring"), ("switch", "tree"), ("mesh", "mesh-hier")], bws, lats, (64, 128)),
+        _part("fsdp:8192", [("mesh", "mesh-hier")], bws, lats, (64, 128))])
+
+
+def part_graphs(w: Workload, part: WorkloadPart):
+    from .synth import GPT2_SMALL
+    m = GPT2_SMALL if w.model == "gpt2-small" else PRESETS[w.model]
+    p = parse_parallel(part.parallel)
+    return synth_transformer(m, p, p.degree)
 
 
 def workload_graphs(w: Workload):
-    from .synth import GPT2_SMALL
-    m = GPT2_SMALL if w.model == "gpt2-small" else PRESETS[w.model]
-    p = parse_parallel(w.parallel)
-    return synth_transformer(m, p, p.degree)
+    assert len(w.parts) == 1, "multi-family workload: use part_graphs"
+    return part_graphs(w, w.parts[0])
 
 
 # ------------------------------------------------------------- sharding

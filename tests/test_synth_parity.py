@@ -18,7 +18,7 @@ def _ref():
 
 def canon(gs):
     out = []
-    for g in gs[:2]:
+    for g in gs[:2] + gs[-1:]:
         nodes = [(n.node_id, n.kind.value, n.op_name, list(n.inputs), list(n.outputs), list(n.data_deps),
                   [tuple(c) for c in n.ctrl_deps], n.duration_ns,
                   (n.coll.kind.value, list(n.coll.group), n.coll.comm_bytes) if n.coll else None) for n in g.nodes]
@@ -27,7 +27,7 @@ def canon(gs):
     return out
 
 
-@pytest.mark.parametrize("preset", ["tiny", "llama-8b-like"])
+@pytest.mark.parametrize("preset", ["tiny", "llama-8b-like", "llama-70b-like"])
 @pytest.mark.parametrize("strat", ["dp", "fsdp", "tp"])
 @pytest.mark.parametrize("mode", ["delayed", "none"])
 @pytest.mark.parametrize("deg", [2, 4, 8])
@@ -39,6 +39,17 @@ def test_synth_matches_reference(preset, strat, mode, deg):
                                                mod.ParallelConfig(mod.Strategy(strat), deg, mod.FsdpMode(mode)), deg))
         except Exception as e:
             return type(e).__name__
+    assert build(ms) == build(rs)
+
+
+@pytest.mark.parametrize("strat", ["dp", "fsdp"])
+def test_synth_matches_reference_c4_scale(strat):
+    """The BASELINE config-4 graphs themselves: llama-70b-like at 8192 ranks."""
+    rs = _ref()
+    def build(mod):
+        gs = mod.synth_transformer(mod.PRESETS["llama-70b-like"], mod.ParallelConfig(mod.Strategy(strat), 8192), 8192)
+        assert len(gs) == 8192 and all(g.nodes is gs[0].nodes for g in gs)   # one shared node list
+        return canon(gs)
     assert build(ms) == build(rs)
 
 

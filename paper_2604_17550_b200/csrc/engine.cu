@@ -406,7 +406,8 @@ struct Ctx {
     bool lead_cta;                  // the cluster's first CTA (its thread 0 does the serial work)
     uint64_t *done, *rdyc, *rdyh, *due;
     uint64_t *touched;              // [word][rank]: accumulator written in this design point
-    int64_t *cp;                    // [max_nodes][R]
+    int64_t *cp;                    // [max_nodes][R]: counted accumulators, parked set members
+    int64_t *acc;                   // [n_acc][R]: accumulators of statically ordered nodes, by slot
     int32_t *ring_inst, *ring_node; // [coll_stride][R] per-rank comm FIFO
     int64_t *dur;                   // [total_nodes] this design point's durations
     int64_t *inst_dur, *inst_s, *inst_e, *inst_cpmax;
@@ -704,22 +705,25 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
     const uint32_t lo = xa.y >> 24;
     const uint32_t qlast = lo && f.fold ? xa.x + lo - 1 : 0xffffffffu;
     uint64_t alast = 0;
-    if (qlast != 0xffffffffu) alast = (uint64_t)__ldcg(c.cp + ((int)((uint32_t)sl[qlast] & 0xffffu) * R + L.r));
+    if (qlast != 0xffffffffu) alast = (uint64_t)__ldcg(c.acc + ((int)((uint32_t)sl[qlast] >> 19) * R + L.r));
     for (uint32_t q = xa.x, qe = xa.x + (xa.y & 0xfffu); q < qe; q++, seq++) {
         const uint32_t ent = (uint32_t)sl[q];
         const int d = (int)(ent & 0xffffu);
-        const int cls = f.fold ? (int)(ent >> 16) : FL_EDGE_COUNTED;
-        int64_t *slot = c.cp + (d * R + L.r);
+        const int cls = f.fold ? (int)((ent >> 16) & 7u) : FL_EDGE_COUNTED;
         // Statically ordered predecessors (capi.cu): no counting, and only the last one
-        // reads the accumulator.  A node that waits on a missing one is never dispatched.
+        // reads the accumulator -- a word of the small slot table [n_acc][R] that nodes with
+        // disjoint accumulator lifetimes share (capi.cu "Accumulator slots"), so it stays in
+        // L2.  A node that waits on a missing one is never dispatched.
         if (cls == FL_EDGE_FIRST) {
-            *slot = (int64_t)(f.epoch | fx);
+            c.acc[(int)(ent >> 19) * R + L.r] = (int64_t)(f.epoch | fx);
             continue;
         }
         if (cls == FL_EDGE_MID) {
-            atomicMax(reinterpret_cast<unsigned long long *>(slot), (unsigned long long)(f.epoch | fx));
+            atomicMax(reinterpret_cast<unsigned long long *>(c.acc + ((int)(ent >> 19) * R + L.r)),
+                      (unsigned long long)(f.epoch | fx));
             continue;
         }
+        int64_t *slot = c.cp + (d * R + L.r);
         const uint4 db = rec_b(g, L.nb + d);
         if (rec_never(db)) continue;
         if (cls == FL_EDGE_SINGLE) {
@@ -728,7 +732,7 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
         }
         if (cls == FL_EDGE_LAST) {
             PROF_MARK(10);                  // edges before a "last" one
-            const uint64_t a = (q == qlast ? alast : (uint64_t)__ldcg(slot)) & VAL48;   // first/middle ones' max
+            const uint64_t a = (q == qlast ? alast : (uint64_t)__ldcg(c.acc + ((int)(ent >> 19) * R + L.r))) & VAL48;
             dispatch(g, c, L, s, f, d, db, (int64_t)(a > fx ? a : fx), seq, t);
             PROF_MARK(11);                  // "last" edge: accumulator read + dispatch
             continue;
@@ -1165,6 +1169,7 @@ __global__ void __launch_bounds__(1024, 1)
         c.touched = sc.touch_in_smem ? reinterpret_cast<uint64_t *>(smem + sc.sm_off_touch) : gbits + 4 * words;
         c.BR = sc.touch_in_smem ? bd : R;
         c.cp = reinterpret_cast<int64_t *>(base + sc.off_cp);
+        c.acc = reinterpret_cast<int64_t *>(base + sc.off_acc);
         c.ring_inst = reinterpret_cast<int32_t *>(base + sc.off_ring);
         c.ring_node = c.ring_inst + (size_t)g.coll_stride * R;
         c.dur = sc.dur_in_smem ? reinterpret_cast<int64_t *>(smem + sc.sm_off_dur)

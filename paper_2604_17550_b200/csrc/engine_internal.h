@@ -35,6 +35,8 @@ struct DevGraph {
     unsigned dur_sm_off;         // per-point durations in shared memory at this offset (0: HBM, per CTA)
     const int32_t *s_init_ns_off, *init_ns;   // initial dispatch list without static hosts
     const int32_t *succ_ent;     // succ_idx | edge class << 16 (FL_EDGE_*, valid when static hosts are folded)
+                                 // | accumulator slot << 19 (FIRST / MID / LAST edges, capi.cu "slots")
+    int n_acc;                   // accumulator slots per rank (colouring of the ordered multi-dependency nodes)
     // messages
     const int64_t *rank_value;
     int n_msg, p2p_stride;
@@ -62,6 +64,7 @@ struct DevOut {
 struct DevScratch {
     unsigned char *base;
     size_t slot_bytes, off_bits, off_cp, off_ring, off_dur, off_inst;
+    size_t off_acc;              // [n_acc][R] int64: accumulators of statically ordered nodes, by slot
     // dynamic shared-memory layout (bytes from the start of the CTA's smem)
     size_t off_msg;              // message state, link state, per-rank in-flight lists
     size_t off_ctr;              // cluster-wide completion counters

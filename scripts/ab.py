@@ -31,9 +31,11 @@ def child(name, workload, points, reps):
     ranks = 0
     if ":" in workload:                 # e.g. c3:512 -- the C3 grid on fsdp:512 (scaling probes)
         workload, ranks = workload.split(":")[0], int(workload.split(":")[1])
-    w = {"c3": S.c3_workload, "c2": S.c2_workload, "c4": S.c4_workload}[workload]()
+    part = {"c4dp": 0, "c4fsdp": 1}.get(workload, 0)     # one family of the C4 grid
+    w = {"c3": S.c3_workload, "c2": S.c2_workload, "c4dp": S.c4_workload, "c4fsdp": S.c4_workload}[workload]()
+    w.parts = [w.parts[part]]
     if ranks:
-        w.parallel = f"fsdp:{ranks}"
+        w.parts[0].parallel = f"fsdp:{ranks}"
         side = int(round(ranks ** 0.5))
         while ranks % side:
             side -= 1

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define FL_ABI_VERSION 1
+#define FL_ABI_VERSION 3
 
 enum fl_status {
     FL_OK = 0,
@@ -53,9 +53,9 @@ enum fl_algo { FL_RING = 0, FL_TREE = 1, FL_MESH_HIER = 2 };
 enum fl_topo { FL_SWITCH = 0, FL_MESH2D = 1 };
 
 /* Engine limits of this build. */
-#define FL_MAX_NODES_PER_RANK 4096   /* 64 bitmap words x 64 bits        */
+#define FL_MAX_NODES_PER_RANK 65535  /* 16-bit local node index (set heads, dependency entries) */
 #define FL_MAX_RANKS 16384           /* one thread per rank; > 1024 ranks run on a CTA cluster (<= 16) */
-#define FL_MAX_P2P_PER_RANK 4096     /* SEND+RECV nodes per rank graph */
+#define FL_MAX_P2P_PER_RANK 65535    /* SEND+RECV nodes per rank graph */
 
 /*
  * A compiled graph set.  Ranks are dense 0..R-1 in ascending rank-value
@@ -142,6 +142,17 @@ typedef struct {
     int64_t *ev_start, *ev_end;       /* optional [n*R*max_nodes] (record_events) */
     int64_t *link_busy;               /* optional [n*link_cap]; -1 = link never used (SimReport.link_busy_ns) */
     int32_t link_cap;                 /* links per point in link_busy: switch 2*R (eg/in per rank), mesh 4*rows*cols */
+    /* optional critical-path node trace per point ("duration_ns and node path"; the
+     * reference returns only the length, simulator.py:400-460), walked back on the device from the
+     * contention-free finish times the simulation computes.  trace[n*trace_cap]: entries from the
+     * sink back to the source, (rank index << 32) | local node index; trace_len[n]: the full path
+     * length (entries beyond trace_cap are not stored; 0 for a point that did not complete).
+     * Rule (engine.critical_path_trace): sink = largest finish, lowest (rank, node_id) on ties; a
+     * node's predecessor = its lowest (rank, node_id) dependency (a collective: over all members'
+     * dependencies) whose finish equals the node's start, else a RECV's SEND. */
+    int64_t *trace;
+    int32_t *trace_len;
+    int32_t trace_cap;
 } fl_outputs;
 
 typedef struct fl_graph fl_graph;
@@ -184,6 +195,14 @@ int fl_critical_path_values(fl_graph *g, const fl_points *host_points, int32_t n
                             const int32_t *vkind, const int32_t *va, const int32_t *vb, const int32_t *vsend,
                             const int32_t *vmsg, const int32_t *pred_off, const int32_t *pred_idx,
                             int64_t *out_cp, int32_t *out_status, int64_t *out_vals);
+
+/* Deterministic topological order of every structure of the graph set and each node's
+ * topological level, computed on the graph's device (replaces graph.py:282-306 topo_order:
+ * Kahn's algorithm, lowest node_id first).  out_order[s_node_off[s] + k] = local index of
+ * the k-th node of structure s (-1 past the placed nodes when the structure has a cycle ->
+ * CyclicGraphError); out_level[global node] = longest path from a zero-indegree node, in
+ * edges.  Host buffers of total nodes each; synchronous. */
+int fl_topo_order(fl_graph *g, int32_t *out_order, int32_t *out_level);
 
 /* Cost stage alone (K1 parity hook): alpha-beta time of n collectives and
  * flops->ns of m compute nodes, evaluated by the device code path. Host buffers. */

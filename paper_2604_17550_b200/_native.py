@@ -124,7 +124,8 @@ class Points(C.Structure):
 
 class Outputs(C.Structure):
     _fields_ = [("status", P32), ("rows", P64), ("rank_stats", P64),
-                ("ev_start", P64), ("ev_end", P64), ("link_busy", P64), ("link_cap", C.c_int32)]
+                ("ev_start", P64), ("ev_end", P64), ("link_busy", P64), ("link_cap", C.c_int32),
+                ("trace", P64), ("trace_len", P32), ("trace_cap", C.c_int32)]
 
 
 _lib = None
@@ -177,6 +178,7 @@ def _bind(L):
                                    P32, P64, P32]
     L.fl_critical_path_values.argtypes = [C.c_void_p, C.POINTER(Points), C.c_int32, P32, P32, P32, P32, P32, P32,
                                           P32, P32, P64, P32, P64]
+    L.fl_topo_order.argtypes = [C.c_void_p, P32, P32]
     L.fl_cost_only.argtypes = [C.c_int32, PU8, P64, P64, PU8, PF64, PF64, P32, P32, P64, P32,
                                C.c_int32, P64, PF64, PF64, P64]
     return L
@@ -195,4 +197,4 @@ def last_error() -> str:
 
 EXPORTED = ["fl_version", "fl_last_error", "fl_device_count", "fl_graph_create", "fl_graph_destroy",
             "fl_graph_max_nodes", "fl_sweep_run", "fl_sweep_run_device", "fl_critical_path",
-            "fl_critical_path_values", "fl_cost_only"]
+            "fl_critical_path_values", "fl_cost_only", "fl_topo_order"]

@@ -45,9 +45,13 @@ struct fl_graph {
     unsigned char *scratch = nullptr;
     size_t scratch_bytes = 0;
     fl::DevScratch sc{};
-    // staging for fl_sweep_run (host-buffer entry point), grown on demand
+    // staging for fl_sweep_run (host-buffer entry point), grown on demand: a device block and
+    // its pinned host mirror, so inputs go up in one copy and rows come back in one
     unsigned char *stage = nullptr;
     size_t stage_bytes = 0;
+    unsigned char *hstage = nullptr;
+    size_t hstage_bytes = 0;
+    cudaStream_t stream = nullptr;  // fl_sweep_run's own non-blocking stream (not the legacy one)
     int grid_cap = 0;
     int block = 32;
     int cluster = 1;
@@ -453,15 +457,18 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     sc.off_dur = off;  off = align_up(off + dur_bytes * CS, 256);      // one copy per CTA of a cluster
     sc.off_inst = off; off = align_up(off + inst_bytes, 256);
     sc.off_inst_se = off; off = align_up(off + 16 * (size_t)(d->n_inst > 0 ? d->n_inst : 1) * CS, 256);
-    // links: switch eg/in per rank; mesh 4 per position (bounded by the largest rank id)
+    // links: switch eg/in per rank; mesh 4 per position.  The table is the last piece of a
+    // slot, sized at create from the largest rank id and grown per launch (fl_sweep_run knows
+    // its points' mesh shapes) -- see grow_links.
     int64_t maxv = 0;
     for (int r = 0; r < R; r++) maxv = d->rank_value[r] > maxv ? d->rank_value[r] : maxv;
     sc.link_cap = d->n_msg > 0 ? (int)std::max<int64_t>(2 * (int64_t)R, 8 * (maxv + 1)) : 0;
     sc.off_msg = off;
-    off = align_up(off + (size_t)d->n_msg * 8 * 8 + (size_t)sc.link_cap * 16 + (size_t)d->n_msg * 8 +
-                       (size_t)R * 4 + 2 * (size_t)dg.p2p_stride * R * 4 + 64, 256);
+    off = align_up(off + (size_t)d->n_msg * 8 * 8 + (size_t)d->n_msg * 8 + (size_t)R * 4 +
+                       2 * (size_t)dg.p2p_stride * R * 4 + 64, 256);
     sc.off_ctr = off;  off = align_up(off + 64, 256);
-    sc.slot_bytes = off;
+    sc.off_links = off;
+    sc.slot_bytes = align_up(off + (size_t)sc.link_cap * 16, 256);
 
     // shared memory: header | comm_end, stats, ring tails | [instances] | [durations] | [done bitmap]
     size_t sm = fl::sweep_shared_header_bytes();
@@ -491,6 +498,14 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     if (occ < 1) return fail(FL_ERR_CAPACITY, "engine kernel cannot be resident with this shared-memory footprint");
     g->grid_cap = CS > 1 ? occ : sms * occ;           // concurrent design points (clusters or CTAs)
     return FL_OK;
+}
+
+// A launch whose mesh points need more links than the slot holds grows the table (the
+// reference accepts any mesh at least as large as the ranks, topology.py:68-102).
+void grow_links(fl_graph *g, int need) {
+    if (g->dg.n_msg <= 0 || need <= g->sc.link_cap) return;
+    g->sc.link_cap = need;
+    g->sc.slot_bytes = align_up(g->sc.off_links + (size_t)need * 16, 256);
 }
 
 int ensure_scratch(fl_graph *g, int grid) {
@@ -531,6 +546,9 @@ int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stre
     dout.ev_end = out->ev_end;
     dout.link_busy = out->link_busy;
     dout.link_cap = out->link_cap;
+    dout.trace = out->trace_len ? out->trace : nullptr;
+    dout.trace_len = out->trace_len;
+    dout.trace_cap = out->trace ? out->trace_cap : 0;
     CK(fl::launch_sweep(cs == 3 ? 4 : cs, grid * g->cluster, g->block, g->smem, stream, g->cluster, g->dg, dp, dout,
                         g->sc));
     return FL_OK;
@@ -587,6 +605,8 @@ int fl_graph_destroy(fl_graph *g) {
     for (void *p : g->allocs) cudaFree(p);
     if (g->scratch) cudaFree(g->scratch);
     if (g->stage) cudaFree(g->stage);
+    if (g->hstage) cudaFreeHost(g->hstage);
+    if (g->stream) cudaStreamDestroy(g->stream);
     delete g;
     return FL_OK;
 }
@@ -607,21 +627,39 @@ int fl_sweep_run(fl_graph *g, const fl_points *hp, fl_outputs *ho) {
     CK(cudaSetDevice(g->device));
     const size_t n = (size_t)hp->n_points;
     if (n == 0) return FL_OK;
+    if (!g->stream) CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    if (g->dg.n_msg > 0 && hp->topo_kind && hp->rows && hp->cols) {
+        int64_t need = 0;
+        for (size_t i = 0; i < n; i++)
+            if (hp->topo_kind[i] == FL_MESH2D && hp->rows[i] > 0 && hp->cols[i] > 0)
+                need = std::max<int64_t>(need, 4 * (int64_t)hp->rows[i] * hp->cols[i]);
+        if (need > (int64_t)1 << 28) return fail(FL_ERR_CAPACITY, "mesh too large for the link table");
+        grow_links(g, (int)need);
+    }
+    cudaStream_t st = g->stream;
     const size_t R = (size_t)g->dg.R, MN = (size_t)g->dg.max_nodes;
-    // one staging block: inputs then outputs, 256-byte aligned sub-buffers
+    // One staging block, mirrored in pinned host memory: the packed inputs (one H2D copy),
+    // then the per-point outputs (status, rows, trace lengths: one D2H copy), then the
+    // optional bulk outputs, which are copied straight into the caller's buffers.
     struct Part { const void *src; size_t bytes; size_t off; };
     Part in[8] = {{hp->algo, n, 0}, {hp->topo_kind, n, 0}, {hp->bw, 8 * n, 0}, {hp->latency, 8 * n, 0},
                   {hp->rows, 4 * n, 0}, {hp->cols, 4 * n, 0},
                   {hp->peak_flops, hp->peak_flops ? 8 * n : 0, 0}, {hp->efficiency, hp->efficiency ? 8 * n : 0, 0}};
     size_t off = 0;
-    for (auto &p : in) { p.off = off; off = align_up(off + p.bytes, 256); }
-    const size_t o_status = off; off = align_up(off + 4 * n, 256);
+    for (auto &p : in) { p.off = off; off = align_up(off + p.bytes, 16); }
+    const size_t in_bytes = off;
+    off = align_up(off, 256);
+    const size_t o_status = off; off = align_up(off + 4 * n, 16);
+    const size_t o_tl = off; off = align_up(off + (ho->trace_len ? 4 * n : 0), 16);
     const size_t o_rows = off; off = align_up(off + 48 * n, 256);
+    const size_t small_end = off;                  // [o_status, small_end): copied back in one piece
     const size_t o_rs = off; off = align_up(off + (ho->rank_stats ? 40 * n * R : 0), 256);
     const size_t o_es = off; off = align_up(off + (ho->ev_start ? 8 * n * R * MN : 0), 256);
     const size_t o_ee = off; off = align_up(off + (ho->ev_start ? 8 * n * R * MN : 0), 256);
     const size_t LC = ho->link_busy ? (size_t)(ho->link_cap > 0 ? ho->link_cap : 0) : 0;
     const size_t o_lb = off; off = align_up(off + 8 * n * LC, 256);
+    const size_t TC = ho->trace_len ? (size_t)(ho->trace && ho->trace_cap > 0 ? ho->trace_cap : 0) : 0;
+    const size_t o_tr = off; off = align_up(off + 8 * n * TC, 256);
     if (off > g->stage_bytes) {
         if (g->stage) cudaFree(g->stage);
         g->stage = nullptr;
@@ -629,9 +667,17 @@ int fl_sweep_run(fl_graph *g, const fl_points *hp, fl_outputs *ho) {
         CK(cudaMalloc(&g->stage, off));
         g->stage_bytes = off;
     }
-    unsigned char *S = g->stage;
+    if (small_end > g->hstage_bytes) {
+        if (g->hstage) cudaFreeHost(g->hstage);
+        g->hstage = nullptr;
+        g->hstage_bytes = 0;
+        CK(cudaHostAlloc(&g->hstage, small_end, cudaHostAllocDefault));
+        g->hstage_bytes = small_end;
+    }
+    unsigned char *S = g->stage, *H = g->hstage;
     for (auto &p : in)
-        if (p.bytes) CK(cudaMemcpyAsync(S + p.off, p.src, p.bytes, cudaMemcpyHostToDevice, 0));
+        if (p.bytes) memcpy(H + p.off, p.src, p.bytes);
+    CK(cudaMemcpyAsync(S, H, in_bytes, cudaMemcpyHostToDevice, st));
     fl_points dp = *hp;
     dp.algo = S + in[0].off;
     dp.topo_kind = S + in[1].off;
@@ -649,18 +695,24 @@ int fl_sweep_run(fl_graph *g, const fl_points *hp, fl_outputs *ho) {
     dout.ev_end = ho->ev_start ? reinterpret_cast<int64_t *>(S + o_ee) : nullptr;
     dout.link_busy = LC ? reinterpret_cast<int64_t *>(S + o_lb) : nullptr;
     dout.link_cap = (int32_t)LC;
-    int rc = launch(g, &dp, &dout, 0);
+    dout.trace = TC ? reinterpret_cast<int64_t *>(S + o_tr) : nullptr;
+    dout.trace_len = ho->trace_len ? reinterpret_cast<int32_t *>(S + o_tl) : nullptr;
+    dout.trace_cap = (int32_t)TC;
+    int rc = launch(g, &dp, &dout, st);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(ho->status, dout.status, 4 * n, cudaMemcpyDeviceToHost, 0));
-    CK(cudaMemcpyAsync(ho->rows, dout.rows, 48 * n, cudaMemcpyDeviceToHost, 0));
-    if (ho->rank_stats) CK(cudaMemcpyAsync(ho->rank_stats, dout.rank_stats, 40 * n * R, cudaMemcpyDeviceToHost, 0));
-    if (LC) CK(cudaMemcpyAsync(ho->link_busy, dout.link_busy, 8 * n * LC, cudaMemcpyDeviceToHost, 0));
+    CK(cudaMemcpyAsync(H + o_status, S + o_status, small_end - o_status, cudaMemcpyDeviceToHost, st));
+    if (ho->rank_stats) CK(cudaMemcpyAsync(ho->rank_stats, dout.rank_stats, 40 * n * R, cudaMemcpyDeviceToHost, st));
+    if (LC) CK(cudaMemcpyAsync(ho->link_busy, dout.link_busy, 8 * n * LC, cudaMemcpyDeviceToHost, st));
+    if (TC) CK(cudaMemcpyAsync(ho->trace, dout.trace, 8 * n * TC, cudaMemcpyDeviceToHost, st));
     if (ho->ev_start) {
-        CK(cudaMemcpyAsync(ho->ev_start, dout.ev_start, 8 * n * R * MN, cudaMemcpyDeviceToHost, 0));
-        CK(cudaMemcpyAsync(ho->ev_end, dout.ev_end, 8 * n * R * MN, cudaMemcpyDeviceToHost, 0));
+        CK(cudaMemcpyAsync(ho->ev_start, dout.ev_start, 8 * n * R * MN, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ho->ev_end, dout.ev_end, 8 * n * R * MN, cudaMemcpyDeviceToHost, st));
     }
-    cudaError_t e = cudaStreamSynchronize(0);
+    cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return fail(FL_ERR_CUDA, std::string("engine kernel: ") + cudaGetErrorString(e));
+    memcpy(ho->status, H + o_status, 4 * n);
+    memcpy(ho->rows, H + o_rows, 48 * n);
+    if (ho->trace_len) memcpy(ho->trace_len, H + o_tl, 4 * n);
     return FL_OK;
 }
 
@@ -754,13 +806,30 @@ int fl_cost_only(int32_t n, const uint8_t *kind, const int64_t *size_bytes, cons
             free_all(tmp);
             return fail(FL_ERR_CUDA, cudaGetErrorString(e));
         }
-        if (N) {
-            cudaMemcpy(out_ns, dout, N * 8, cudaMemcpyDeviceToHost);
-            cudaMemcpy(out_status, dst, N * 4, cudaMemcpyDeviceToHost);
+        if (N && e == cudaSuccess) e = cudaMemcpy(out_ns, dout, N * 8, cudaMemcpyDeviceToHost);
+        if (N && e == cudaSuccess) e = cudaMemcpy(out_status, dst, N * 4, cudaMemcpyDeviceToHost);
+        if (M && e == cudaSuccess) e = cudaMemcpy(out_comp_ns, dcomp, M * 8, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) {
+            free_all(tmp);
+            return fail(FL_ERR_CUDA, cudaGetErrorString(e));
         }
-        if (M) cudaMemcpy(out_comp_ns, dcomp, M * 8, cudaMemcpyDeviceToHost);
     }
     free_all(tmp);
+    return FL_OK;
+}
+
+int fl_topo_order(fl_graph *g, int32_t *out_order, int32_t *out_level) {
+    if (!g || !out_order || !out_level) return fail(FL_ERR_INVALID, "null argument");
+    CK(cudaSetDevice(g->device));
+    const size_t n = (size_t)(g->dg.total_nodes > 0 ? g->dg.total_nodes : 1);
+    int32_t *dw = nullptr;
+    CK(cudaMalloc(&dw, 3 * n * sizeof(int32_t)));
+    cudaError_t e = fl::launch_topo(g->dg, dw, dw + n, dw + 2 * n);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(out_order, dw + n, (size_t)g->dg.total_nodes * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(out_level, dw + 2 * n, (size_t)g->dg.total_nodes * 4, cudaMemcpyDeviceToHost);
+    cudaFree(dw);
+    if (e != cudaSuccess) return fail(FL_ERR_CUDA, cudaGetErrorString(e));
     return FL_OK;
 }
 

@@ -165,6 +165,8 @@ constexpr uint64_t KINF = ~0ull;
 
 struct Shared {
     alignas(16) uint64_t xbuf[2][16][2];   // cluster step exchange: {min key, completions} per CTA (st.async)
+    int tr_r, tr_x;                 // critical-path trace walk: the current (rank, local node)
+    int seq_ovf;                    // a rank popped more than 8191 events at one time (ordering key capacity)
     unsigned long long xmbar[2];    // their mbarriers
     int cflag;                      // a rank of this CTA completed a collective / message since the last exchange
     int ncons;                      // cluster without messages: completion-list entries reserved so far
@@ -200,6 +202,21 @@ __device__ __forceinline__ uint64_t block_min_u64(uint64_t v, Shared &sh, int &p
     __syncthreads();
     v = lane < nw ? b[lane] : b[0];
     return warp_min_key(v);
+}
+
+// block-wide min of arbitrary 64-bit keys (no lockstep shortcut)
+__device__ __forceinline__ uint64_t block_min_any(uint64_t v, Shared &sh, int &par) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) { uint64_t w = __shfl_xor_sync(FULL, v, o); v = w < v ? w : v; }
+    uint64_t *b = sh.red[par];
+    par ^= 1;
+    if (lane == 0) b[warp] = v;
+    __syncthreads();
+    v = lane < nw ? b[lane] : KINF;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) { uint64_t w = __shfl_xor_sync(FULL, v, o); v = w < v ? w : v; }
+    return v;
 }
 
 __device__ __forceinline__ int64_t block_max_i64(int64_t v, Shared &sh, int &par) {
@@ -309,15 +326,14 @@ __device__ __forceinline__ uint64_t cl_step_min(uint64_t v, int &any, Shared &sh
         asm volatile("{ .reg .pred q; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 q, [%1], %2; "
                      "selp.u32 %0, 1, 0, q; }" : "=r"(done) : "r"(mb), "r"(ph) : "memory");
     } while (!done);
-    uint64_t m = KINF;
-    int a = 0;
-    for (unsigned j = 0; j < n; j++) {
-        const uint64_t x = sh.xbuf[p][j][0];
-        m = x < m ? x : m;
-        a |= (int)sh.xbuf[p][j][1];
-    }
-    any = a;
-    return m;
+    // lane j reads CTA j's slot; the warp reduces them (two REDUX for the 64-bit min)
+    const unsigned lane = threadIdx.x & 31u;
+    const uint64_t x = lane < n ? sh.xbuf[p][lane][0] : KINF;
+    const unsigned f = lane < n ? (unsigned)sh.xbuf[p][lane][1] : 0u;
+    const unsigned hi = (unsigned)(x >> 32), mh = __reduce_min_sync(FULL, hi);
+    const unsigned ml = __reduce_min_sync(FULL, hi == mh ? (unsigned)x : 0xffffffffu);
+    any = (int)__reduce_or_sync(FULL, f);
+    return ((uint64_t)mh << 32) | ml;
 }
 
 // ---------------------------------------------------------- rank state
@@ -486,6 +502,7 @@ struct Step {                       // block-uniform per-step context
     int init;
     int fold;                       // static hosts folded (see "t = 0 host pops")
     int touch;                      // first-dependency bitmap in shared memory (else epoch tags)
+    int trace;                      // record every node's critical-path finish for the trace walk
 };
 
 __device__ __forceinline__ void bm_set(uint64_t *b, int R, int r, int idx) {
@@ -678,7 +695,7 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
     const uint4 xa = rec_a(g, L.nb + x);
     if (g.needs_done) done_ref<K>(c, L, R, x >> 6) |= 1ull << (x & 63);
     F32<K>(Q_DONE, L.lr)++;
-    s.pop_seq++;
+    if (++s.pop_seq > 8191) reinterpret_cast<Shared *>(fl_smem)->seq_ovf = 1;   // 13-bit field of the keys
     F64<K>(F_FIN, L.lr) = t;
     {
         const int64_t cm = F64<K>(F_CPMAX, L.lr);
@@ -699,6 +716,9 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
     if (freed) F64<K>(F_FREE, L.lr) += freed;
     PROF_MARK(9);                           // pop: records, statistics
     const uint64_t fx = (uint64_t)fx64;     // this node's critical-path finish
+    // trace: the node's own word is dead once it is popped (its accumulator and its parking
+    // as a set member are behind it), so it keeps the finish for the walk-back
+    if (f.trace) c.cp[x * R + L.r] = (int64_t)(f.epoch | fx);
     int seq = 0;
     const int32_t *sl = g.succ_ent;
     // the first "last" edge's accumulator read goes out before the other edges are processed
@@ -1124,13 +1144,91 @@ __device__ __forceinline__ int64_t reserve(const DevGraph &g, const DevOut &o, c
     return (nc | nmc) ? reserve_n<MSG, CL, K>(g, o, c, sh, par, t, init, cfg, epoch, nc, nmc, topo, cols) : 0;
 }
 
+// Critical-path node trace of one completed design point, walked back on the device
+// (fl_outputs.trace; the rule of engine.critical_path_trace, restated in
+// oracle/pyoracle.py).  Every node's contention-free finish is in its word of c.cp
+// (pop_event, f.trace); a node's start is finish - duration for HOST / COMP, the
+// instance's critical-path start for a collective member (the union-of-deps join,
+// simulator.py:419-428) and the finish itself for SEND / RECV (no duration; a RECV's
+// start already includes its SEND plus the wire, simulator.py:450-452).  Runs on one
+// CTA (a cluster's lead CTA reads the other CTAs' ranks from the shared slot): warp 0
+// resolves ordinary nodes, the whole CTA a collective's union of member dependencies.
+static __device__ void trace_walk(const DevGraph &g, const DevOut &o, const Ctx &c, Shared &sh, int &par, int cfg,
+                                  int r0, int64_t best) {
+    const int R = g.R, tid = threadIdx.x, lane = tid & 31, bd = blockDim.x;
+    auto fin = [&](int r, int x) -> int64_t { return __ldcg(c.cp + ((size_t)x * R + r)) & (int64_t)VAL48; };
+    if (tid < 32) {             // the sink: rank r0's lowest node finishing at the critical path
+        const int st = g.rank_struct[r0], nb = g.s_node_off[st], n = g.s_node_off[st + 1] - nb;
+        int found = -1;
+        for (int x0 = 0; x0 < n && found < 0; x0 += 32) {
+            const unsigned b = __ballot_sync(FULL, x0 + lane < n && fin(r0, x0 + lane) == best);
+            if (b) found = x0 + __ffs(b) - 1;
+        }
+        if (tid == 0) { sh.tr_r = r0; sh.tr_x = found; }
+    }
+    __syncthreads();
+    const int64_t cap = o.trace ? o.trace_cap : 0, guard = (int64_t)g.total_nodes * R + g.n_inst + 1;
+    int64_t *out = o.trace + (size_t)cfg * cap;
+    int64_t len = 0;
+    for (;;) {
+        const int r = sh.tr_r, x = sh.tr_x;
+        if (x < 0 || len >= guard) break;
+        if (tid == 0 && len < cap) out[len] = ((int64_t)r << 32) | x;
+        len++;
+        const int nb = g.s_node_off[g.rank_struct[r]];
+        const uint4 rb = rec_b(g, nb + x);
+        const int kind = rec_kind(rb);
+        __syncthreads();                            // every thread has read sh.tr_*
+        if (kind == FL_COLL) {
+            const int i = g.rank_coll_inst[r * g.coll_stride + (int)rb.y];
+            const int64_t s0 = c.inst_cpmax[i];
+            uint64_t k = KINF;
+            for (int64_t j = g.inst_mem_off[i] + tid; j < g.inst_mem_off[i + 1]; j += bd) {
+                const int rm = g.inst_mem_rank[j];
+                const int gm = g.s_node_off[g.rank_struct[rm]] + g.inst_mem_node[j];
+                for (int u = g.pred_off[gm]; u < g.pred_off[gm + 1]; u++) {
+                    const int pn = g.pred_idx[u];
+                    if (fin(rm, pn) == s0) {
+                        const uint64_t kk = ((uint64_t)rm << 32) | (uint32_t)pn;
+                        k = kk < k ? kk : k;
+                    }
+                }
+            }
+            k = block_min_any(k, sh, par);
+            if (tid == 0) { sh.tr_r = k == KINF ? 0 : (int)(k >> 32); sh.tr_x = k == KINF ? -1 : (int)(uint32_t)k; }
+        } else if (tid < 32) {
+            const int64_t fx = fin(r, x);
+            const int64_t s0 = kind <= FL_COMP ? fx - dur_of(g, c, nb + x) : fx;
+            int kx = 0x7fffffff;
+            for (int u = g.pred_off[nb + x] + lane; u < g.pred_off[nb + x + 1]; u += 32) {
+                const int pn = g.pred_idx[u];
+                if (fin(r, pn) == s0) kx = pn < kx ? pn : kx;
+            }
+            kx = __reduce_min_sync(FULL, kx);
+            if (lane == 0) {
+                int nr = r, nx = kx == 0x7fffffff ? -1 : kx;
+                if (nx < 0 && kind == FL_RECV) {    // the start was set by the SEND plus the wire
+                    const int m = g.rank_p2p_msg[r * g.p2p_stride + (int)rb.y];
+                    nr = g.msg_send_rank[m];
+                    nx = g.msg_send_node[m];
+                }
+                sh.tr_r = nr;
+                sh.tr_x = nx;
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) o.trace_len[cfg] = (int32_t)len;
+}
+
 // Zero this CTA's ranks' columns of a [rows][R] array (clusters split a point's ranks).
 template <bool CL, typename T>
 __device__ __forceinline__ void zero_cols(T *a, size_t rows, int R, int base, int RL) {
     if constexpr (!CL) {
         for (size_t i = threadIdx.x; i < rows * R; i += blockDim.x) a[i] = 0;
-    } else {
-        for (size_t i = threadIdx.x; i < rows * RL; i += blockDim.x) a[(i / RL) * R + base + (i % RL)] = 0;
+    } else {               // (a cluster CTA's columns: RL == blockDim.x except in the last CTA)
+        if ((int)threadIdx.x < RL)
+            for (size_t w = 0; w < rows; w++) a[w * R + base + threadIdx.x] = 0;
     }
 }
 
@@ -1201,10 +1299,10 @@ __global__ void __launch_bounds__(1024, 1)
         c.msg_e = mb + 5 * M;
         c.msg_xfer = mb + 6 * M;
         c.msg_ckey = reinterpret_cast<unsigned long long *>(mb + 7 * M);
-        c.link_free = mb + 8 * M;
+        c.link_free = reinterpret_cast<int64_t *>(base + sc.off_links);
         c.link_busy = c.link_free + sc.link_cap;
         c.link_cap = sc.link_cap;
-        c.msg_wait = reinterpret_cast<int32_t *>(c.link_busy + sc.link_cap);
+        c.msg_wait = reinterpret_cast<int32_t *>(mb + 8 * M);
         c.mcomplist = c.msg_wait + M;
         c.mcount = c.mcomplist + M;
         c.mlist = c.mcount + R;
@@ -1307,7 +1405,7 @@ __global__ void __launch_bounds__(1024, 1)
             else zero_cols<CL>(c.done, (size_t)g.max_words, R, base_r, RL);
         }
         if (sc.touch_in_smem) for (size_t i = tid; i < (size_t)g.max_words * bd; i += bd) c.touched[i] = 0;
-        if (tid == 0) { sh.cend_all = 0; sh.cend_uniform = 1; sh.ncons = 0; }
+        if (tid == 0) { sh.cend_all = 0; sh.cend_uniform = 1; sh.ncons = 0; sh.seq_ovf = 0; }
         if (CL && is_leader) *c.ncomp = 0;          // (MONO clusters: the list restarts per point)
 #pragma unroll
         for (int k = 0; k < F_N64; k++) F64<K>(k, tid) = 0;
@@ -1321,6 +1419,7 @@ __global__ void __launch_bounds__(1024, 1)
         dev_zdur = zdur;
         if (bad) {
             if (is_leader) o.status[cfg] = bad == 2 ? FL_ERR_CAPACITY : FL_ERR_UNSUPPORTED_ALGO;
+            if (is_leader && o.trace_len) o.trace_len[cfg] = 0;
             dirty = false;
             gsync<CL>();
             continue;
@@ -1336,6 +1435,7 @@ __global__ void __launch_bounds__(1024, 1)
         f.init = 1;
         f.fold = g.fold_ok && !zero && !zdur;
         f.touch = sc.touch_in_smem;
+        f.trace = o.trace_len != nullptr;
 
         // ---- per-rank state ----
         Rank<KK> s;
@@ -1396,13 +1496,16 @@ __global__ void __launch_bounds__(1024, 1)
                     const int4 tr = g.trig[q];
                     if (tr.x != prev) {
                         if (prev >= 0) start_phase(g, o, c, L, s, f, 0, cfg);
-                        s.pop_seq++;
+                        if (++s.pop_seq > 8191) sh.seq_ovf = 1;
                         prev = tr.x;
                     }
                     dispatch(g, c, L, s, f, tr.y, rec_b(g, L.nb + tr.y), 0, tr.z, 0);
                 }
                 if (prev >= 0) start_phase(g, o, c, L, s, f, 0, cfg);
                 F32<K>(Q_DONE, tid) += g.s_nstatic[st];
+                if (f.trace)        // folded static hosts start and finish at 0 (never popped here)
+                    for (int q = g.static_off[st]; q < g.static_off[st + 1]; q++)
+                        c.cp[g.static_list[q] * R + L.r] = (int64_t)f.epoch;
                 if (o.ev_start)
                     for (int q = g.static_off[st]; q < g.static_off[st + 1]; q++)
                         record(g, o, cfg, L.r, g.static_list[q], 0, 0);
@@ -1514,6 +1617,7 @@ __global__ void __launch_bounds__(1024, 1)
 #endif
 
         // ---- row: reductions over ranks (cli.py:336-341) ----
+        overflow |= gor<CL>(sh.seq_ovf, sh, par) != 0;
         int dead = active && F32<K>(Q_DONE, tid) != F32<K>(Q_MYN, tid);
         dead = gor<CL>(dead | overflow, sh, par);
         dirty = dead != 0;
@@ -1531,12 +1635,24 @@ __global__ void __launch_bounds__(1024, 1)
                 rs[0] = vals[0]; rs[1] = vals[2]; rs[2] = vals[3]; rs[3] = vals[4]; rs[4] = vals[5];
             }
         }
+        int64_t cpbest = 0;
 #pragma unroll
         for (int k = 0; k < 6; k++) {
             const int64_t v = gmax_i64<CL>(vals[k], sh, par);
+            if (k == 1) cpbest = v;
             if (is_leader) o.rows[(size_t)cfg * 6 + k] = v;
         }
         if (is_leader) o.status[cfg] = overflow ? FL_ERR_CAPACITY : dead ? FL_ERR_DEADLOCK : FL_OK;
+        if (o.trace_len) {
+            // the sink's rank: the lowest one whose largest critical-path finish is the point's
+            uint64_t rk = (active && F64<K>(F_CPMAX, tid) == cpbest) ? (uint64_t)L.r : KINF;
+            rk = gmin_key<CL>(rk, sh, par);
+            gsync<CL>();                                // (cluster: every CTA's finishes visible)
+            if (!CL || crank == 0) {
+                if (dead || rk == KINF) { if (tid == 0) o.trace_len[cfg] = 0; }
+                else trace_walk(g, o, c, sh, par, cfg, (int)rk, cpbest);
+            }
+        }
         if (o.link_busy && crank == 0)   // SimReport.link_busy_ns (simulator.py:321, :367)
             for (int l = tid; l < o.link_cap; l += bd)
                 o.link_busy[(size_t)cfg * o.link_cap + l] = (g.n_msg && l < c.link_cap) ? c.link_busy[l] : -1;
@@ -1736,6 +1852,67 @@ cudaError_t launch_cp(const DevGraph &g, const DevPoints &p, int nv, const int32
                       int32_t *status) {
     cp_kernel<<<(p.n + 127) / 128, 128>>>(g, p, nv, order, vkind, va, vb, vsend, vmsg, poff, pidx, vals, starts, out,
                                           status);
+    return cudaGetLastError();
+}
+
+// Deterministic topological order of each structure (graph.py:282-306: Kahn's
+// algorithm, lowest node_id first -- local index order is node_id order) and every
+// node's level (longest path from a source, in edges).  One warp per structure: the
+// ready set is a bitmap whose lowest set bit is found with ballots; a node's
+// successors are released in parallel.  order[s_node_off[s] + k] is the k-th node
+// (local index), -1 past the placed ones when the structure has a cycle.
+__global__ void topo_kernel(const __grid_constant__ DevGraph g, int32_t *indeg, int32_t *order, int32_t *level) {
+    extern __shared__ uint64_t ready[];
+    const int s = blockIdx.x, lane = threadIdx.x;
+    const int nb = g.s_node_off[s], n = g.s_node_off[s + 1] - nb, W = (n + 63) / 64;
+    for (int v = lane; v < n; v += 32) {
+        indeg[nb + v] = g.pred_off[nb + v + 1] - g.pred_off[nb + v];
+        level[nb + v] = 0;
+        order[nb + v] = -1;
+    }
+    for (int w = lane; w < W; w += 32) {
+        uint64_t word = 0;
+        for (int b = 0; b < 64 && 64 * w + b < n; b++)
+            if (g.pred_off[nb + 64 * w + b + 1] == g.pred_off[nb + 64 * w + b]) word |= 1ull << b;
+        ready[w] = word;
+    }
+    __syncwarp();
+    for (int k = 0; k < n; k++) {
+        int v = -1;
+        for (int w0 = 0; w0 < W && v < 0; w0 += 32) {
+            const uint64_t word = w0 + lane < W ? ready[w0 + lane] : 0ull;
+            const unsigned bal = __ballot_sync(FULL, word != 0ull);
+            if (bal) {
+                const int src = __ffs(bal) - 1;
+                const uint64_t wv = __shfl_sync(FULL, word, src);
+                v = 64 * (w0 + src) + __ffsll((long long)wv) - 1;
+            }
+        }
+        if (v < 0) break;                           // cycle: nothing ready
+        __syncwarp();
+        if (lane == 0) {
+            atomicAnd(reinterpret_cast<unsigned long long *>(&ready[v >> 6]), ~(1ull << (v & 63)));
+            order[nb + k] = v;
+        }
+        __syncwarp();
+        const int lv = level[nb + v] + 1;
+        for (int q = g.succ_off[nb + v] + lane; q < g.succ_off[nb + v + 1]; q += 32) {
+            const int w = g.succ_idx[q];
+            atomicMax(&level[nb + w], lv);
+            if (atomicSub(&indeg[nb + w], 1) == 1) atomicOr(reinterpret_cast<unsigned long long *>(&ready[w >> 6]),
+                                                            1ull << (w & 63));
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_topo(const DevGraph &g, int32_t *indeg_ws, int32_t *order, int32_t *level) {
+    const size_t smem = (size_t)g.max_words * 8;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(topo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    topo_kernel<<<g.S, 32, smem>>>(g, indeg_ws, order, level);
     return cudaGetLastError();
 }
 

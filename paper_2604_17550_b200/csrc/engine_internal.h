@@ -58,6 +58,9 @@ struct DevOut {
     int32_t *status;
     int64_t *rows, *rank_stats, *ev_start, *ev_end, *link_busy;
     int link_cap;
+    int64_t *trace;              // critical-path node trace (flint_b200.h fl_outputs.trace)
+    int32_t *trace_len;
+    int trace_cap;
 };
 
 // Per-CTA scratch: slot_bytes each, laid out at the given byte offsets.
@@ -66,7 +69,8 @@ struct DevScratch {
     size_t slot_bytes, off_bits, off_cp, off_ring, off_dur, off_inst;
     size_t off_acc;              // [n_acc][R] int64: accumulators of statically ordered nodes, by slot
     // dynamic shared-memory layout (bytes from the start of the CTA's smem)
-    size_t off_msg;              // message state, link state, per-rank in-flight lists
+    size_t off_msg;              // message state, per-rank in-flight lists
+    size_t off_links;            // link state [2][link_cap] (last in the slot: grows per launch)
     size_t off_ctr;              // cluster-wide completion counters
     size_t off_inst_se;          // clusters: per-CTA copies of the instances' reservation start / end
     int link_cap;
@@ -85,6 +89,7 @@ cudaError_t launch_cp(const DevGraph &g, const DevPoints &p, int nv, const int32
                       const int32_t *va, const int32_t *vb, const int32_t *vsend, const int32_t *vmsg,
                       const int32_t *poff, const int32_t *pidx, int64_t *vals, int64_t *starts, int64_t *out,
                       int32_t *status);
+cudaError_t launch_topo(const DevGraph &g, int32_t *indeg_ws, int32_t *order, int32_t *level);
 cudaError_t launch_cost_only(int n, const uint8_t *kind, const int64_t *size, const int64_t *gn,
                              const uint8_t *algo, const double *alpha, const double *beta,
                              const int32_t *rows, const int32_t *cols, int64_t *out, int32_t *status,

@@ -198,8 +198,12 @@ class Engine:
         return cap
 
     def run(self, pts: DesignPoints, rank_stats: bool = False, events: bool = False,
-            links: bool = False) -> dict:
-        """Evaluate design points from host buffers (copies included)."""
+            links: bool = False, trace_cap: int = 0) -> dict:
+        """Evaluate design points from host buffers (copies included).
+
+        ``trace_cap > 0`` also returns each point's critical-path node trace, walked back on
+        the device (fl_outputs.trace): ``trace_len[n]`` and ``trace[n, trace_cap]`` with
+        entries (rank index << 32 | local node index) from the sink back to the source."""
         n = len(pts)
         R = self.gs.n_ranks
         out = {"status": np.zeros(n, np.int32), "rows": np.zeros((n, 6), np.int64)}
@@ -216,12 +220,40 @@ class Engine:
                            _ptr(pts.rows, _native.P32), _ptr(pts.cols, _native.P32),
                            _ptr(pts.peak_flops, _native.PF64), _ptr(pts.efficiency, _native.PF64),
                            pts.compute_streams)
+        if trace_cap > 0:
+            out["trace"] = np.zeros((n, trace_cap), np.int64)
+            out["trace_len"] = np.zeros(n, np.int32)
         o = _native.Outputs(_ptr(out["status"], _native.P32), _ptr(out["rows"], _native.P64),
                             _ptr(out.get("rank_stats"), _native.P64), _ptr(out.get("ev_start"), _native.P64),
-                            _ptr(out.get("ev_end"), _native.P64), _ptr(out.get("link_busy"), _native.P64), cap)
+                            _ptr(out.get("ev_end"), _native.P64), _ptr(out.get("link_busy"), _native.P64), cap,
+                            _ptr(out.get("trace"), _native.P64), _ptr(out.get("trace_len"), _native.P32),
+                            int(trace_cap))
         rc = _native.lib().fl_sweep_run(self._h, C.byref(p), C.byref(o))
         if rc:
             raise EngineError(f"fl_sweep_run: {_native.last_error()} (status {rc})")
+        return out
+
+    def topo_levels(self):
+        """Every structure's deterministic topological order and node levels, computed on the
+        device (fl_topo_order; graph.py:282-306).  Returns one ``(order, level)`` pair per
+        structure: node ids in Kahn / lowest-id-first order, and {node_id: level} (longest
+        path from a zero-indegree node, in edges).  CyclicGraphError for a cyclic structure."""
+        from .errors import CyclicGraphError
+        total = sum(st.n for st in self.gs.structs)
+        order = np.zeros(max(1, total), np.int32)
+        level = np.zeros(max(1, total), np.int32)
+        rc = _native.lib().fl_topo_order(self._h, order.ctypes.data_as(_native.P32),
+                                         level.ctypes.data_as(_native.P32))
+        if rc:
+            raise EngineError(f"fl_topo_order: {_native.last_error()} (status {rc})")
+        out, b = [], 0
+        for st in self.gs.structs:
+            o, lv = order[b:b + st.n], level[b:b + st.n]
+            b += st.n
+            if (o < 0).any():
+                raise CyclicGraphError("graph has a dependency cycle; no topological order")
+            ids = st.node_id
+            out.append(([int(ids[k]) for k in o], {int(ids[k]): int(lv[k]) for k in range(st.n)}))
         return out
 
     def critical_path_only(self, pts: DesignPoints, mg: dict) -> int:
@@ -379,13 +411,49 @@ def critical_path_trace(graphs, topo, algo=CollectiveAlgo.RING, device: int = 0)
       set by a RECV's SEND plus the wire time (simulator.py:430-435, :450-452) and the
       path continues at the SEND; a node whose start no predecessor sets is the source.
 
-    Every finish and start comes from the GPU (fl_critical_path_values); the host only
-    walks back through them.
+    The walk runs on the device inside the sweep kernel (fl_outputs.trace, from the
+    finishes the simulation computes); ``trace_paths`` converts any batch of them.  Only a
+    graph whose *simulation* deadlocks (a SEND waits for its RECV, simulator.py:259-268,
+    while the contention-free bound has no such wait) falls back to the standalone
+    critical-path kernel (fl_critical_path_values) and a host walk.
     """
-    from .store import merged_cp_graph
     gs = compile_graphs(graphs)
     if gs.pair_error:
         _raise_pair_error(gs, topo, algo)
+    eng = Engine(gs, device)
+    try:
+        out = eng.run(_single_point(topo, algo), trace_cap=trace_capacity(gs))
+    finally:
+        eng.close()
+    st = int(out["status"][0])
+    if st == FL_OK:
+        return int(out["rows"][0, 1]), trace_paths(gs, out)[0]
+    if st != 3:
+        raise_for_status(st)
+    return _critical_path_trace_fallback(gs, topo, algo, device)
+
+
+def trace_capacity(gs: GraphSet) -> int:
+    """Entries that always hold a critical-path trace: every (rank, node) once."""
+    return int(gs.units()) + 1
+
+
+def trace_paths(gs: GraphSet, out: dict) -> list:
+    """Device traces (Engine.run(..., trace_cap=)) -> per point [(rank, node_id), ...] source first."""
+    paths = []
+    for k in range(len(out["trace_len"])):
+        n = int(out["trace_len"][k])
+        if n > out["trace"].shape[1]:
+            raise EngineError(f"critical-path trace of {n} nodes exceeds trace_cap {out['trace'].shape[1]}")
+        ent = out["trace"][k, :n][::-1]
+        ranks, nodes = (ent >> 32).astype(np.int64), (ent & 0xffffffff).astype(np.int64)
+        paths.append([(int(gs.rank_values[r]), int(gs.structs[gs.rank_struct[r]].node_id[x]))
+                      for r, x in zip(ranks, nodes)])
+    return paths
+
+
+def _critical_path_trace_fallback(gs, topo, algo, device):
+    from .store import merged_cp_graph
     mg = merged_cp_graph(gs)
     eng = Engine(gs, device)
     try:
@@ -468,6 +536,18 @@ def simulate_batch(graphs, points: DesignPoints, device: int = 0, engine: Option
     for k, name in enumerate(ROW_FIELDS):
         res[name] = out["rows"][:, k]
     return res
+
+
+def topo_orders(graphs, device: int = 0) -> dict:
+    """``trainsim.graph.topo_order`` (graph.py:282-306) for every rank of a graph set,
+    computed on the GPU: {rank: [node_id, ...]}.  Ranks sharing a structure share its order."""
+    eng = Engine(graphs, device)
+    try:
+        per = eng.topo_levels()
+        return {int(eng.gs.rank_values[r]): list(per[int(eng.gs.rank_struct[r])][0])
+                for r in range(eng.gs.n_ranks)}
+    finally:
+        eng.close()
 
 
 def cost_only(kind, size_bytes, group_n, algo, alpha, beta, rows, cols, flops=None, peak=None, eff=None):

@@ -392,7 +392,7 @@ def desc_arrays(gs: GraphSet) -> dict:
     )
 
 
-def check_supported(gs: GraphSet, max_ranks: int = 16384, max_nodes: int = 4096) -> None:
+def check_supported(gs: GraphSet, max_ranks: int = 16384, max_nodes: int = 65535) -> None:
     if gs.n_ranks > max_ranks:
         raise EngineError(f"{gs.n_ranks} ranks exceed this engine build's {max_ranks} per design point")
     if gs.max_nodes > max_nodes:

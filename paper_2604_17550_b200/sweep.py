@@ -55,10 +55,15 @@ def latency_grid(lo_ns: float, hi_ns: float, n: int) -> np.ndarray:
 
 @dataclass
 class WorkloadPart:
-    """One graph family of a workload and the design points evaluated on it."""
+    """One graph family of a workload and the design points evaluated on it.
+
+    ``expand`` = (algo, topology spec): the family is the EXPANDED form of the
+    graphs (collectives lowered to SEND/RECV plans, collectives.py:456-537),
+    which depends on the algorithm and, for MESH_HIER, the mesh shape."""
     parallel: str
     points: DesignPoints
     labels: list               # (topology kind, algo) per point, for reporting
+    expand: Optional[tuple] = None
 
 
 @dataclass
@@ -140,11 +145,41 @@ def c4_workload() -> Workload:
         _part("fsdp:8192", [("mesh", "mesh-hier")], bws, lats, (64, 128))])
 
 
+def c2x_workload() -> Workload:
+    """BASELINE config 2 in EXPANDED comm mode: GPT-2 small
+    dp:64 with every all-reduce lowered to its ring or tree SEND/RECV plan and
+    replayed on switch:64 links, 256 points = {ring, tree} x 16 bw x 8 latency.
+    The expanded graph depends on the algorithm: two families."""
+    bws, lats = log_grid(10e9, 1.8e12, 16), latency_grid(100, 10000, 8)
+    w = Workload("c2x", "gpt2-small", [
+        _part("dp:64", [("switch", "ring")], bws, lats, (0, 0)),
+        _part("dp:64", [("switch", "tree")], bws, lats, (0, 0))])
+    w.parts[0].expand, w.parts[1].expand = ("ring", "switch:64:50GB:1us"), ("tree", "switch:64:50GB:1us")
+    return w
+
+
+def meshx_workload() -> Workload:
+    """The reference's mesh study (acceptance criterion 6, test_acceptance.py:260-276)
+    at 8x8: tiny dp:64 on mesh:8x8, collectives expanded to ring and to mesh-hier
+    SEND/RECV plans with per-link FIFOs, 256 points = {ring, mesh-hier} x 16 bw x 8
+    latency."""
+    bws, lats = log_grid(10e9, 1.8e12, 16), latency_grid(100, 10000, 8)
+    w = Workload("meshx", "tiny", [
+        _part("dp:64", [("mesh", "ring")], bws, lats, (8, 8)),
+        _part("dp:64", [("mesh", "mesh-hier")], bws, lats, (8, 8))])
+    w.parts[0].expand, w.parts[1].expand = ("ring", "mesh:8x8:50GB:1us"), ("mesh-hier", "mesh:8x8:50GB:1us")
+    return w
+
+
 def part_graphs(w: Workload, part: WorkloadPart):
     from .synth import GPT2_SMALL
     m = GPT2_SMALL if w.model == "gpt2-small" else PRESETS[w.model]
     p = parse_parallel(part.parallel)
-    return synth_transformer(m, p, p.degree)
+    graphs = synth_transformer(m, p, p.degree)
+    if part.expand:
+        algo, spec = part.expand
+        graphs = expand_collectives(graphs, CollectiveAlgo(algo), parse_topology(spec))
+    return graphs
 
 
 def workload_graphs(w: Workload):

@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     assert set(names) == set(_native.EXPORTED)
     for name in names:
         assert hasattr(lib, name), name
-    assert lib.fl_version() == 1
+    assert lib.fl_version() == _native._header_abi_version()
 
 
 def test_library_is_sm100a_only():

@@ -366,3 +366,33 @@ def test_sweep_rows_split_over_devices_is_identical():
     one = sweep_rows(*args)
     two = sweep_rows(*args, devices=[0, 0, 0])
     assert one == two and len(one) == 2 * len(topos)
+
+
+def test_c3_grid_with_device_traces():
+    """BASELINE config 3 in full with the critical-path node trace of every point walked back
+    on the device (fl_outputs.trace): rows unchanged (golden full-grid rows), every path ends
+    at the row's critical path, and four points' paths equal the oracle restatement's
+    (pyoracle.critical_path_trace, the rule of engine.critical_path_trace)."""
+    from pathlib import Path
+    from paper_2604_17550_b200 import sweep as S
+    from paper_2604_17550_b200.topology import Topology, TopologyKind
+    w = S.c3_workload()
+    gs = S.workload_graphs(w)
+    eng = E.Engine(gs)
+    try:
+        out = eng.run(w.points, trace_cap=4 * eng.gs.max_nodes)
+    finally:
+        eng.close()
+    fx = np.load(Path(__file__).parent / "golden" / "c3_grid_rows.npz")
+    assert (out["status"] == 0).all() and (out["rows"] == fx["rows"]).all()
+    paths = E.trace_paths(eng.gs, out)
+    assert all(len(p) > 1 for p in paths)
+    flat = O.flatten(gs)
+    algos = {0: "ring", 1: "tree", 2: "mesh-hier"}
+    pts = w.points
+    for i in (0, 1000, 2049, 4095):
+        kind = TopologyKind.SWITCH if pts.topo_kind[i] == 0 else TopologyKind.MESH2D
+        topo = Topology(kind, 1024, float(pts.bw[i]), int(pts.latency[i]), int(pts.rows[i]), int(pts.cols[i]))
+        length, path = O.critical_path_trace(gs, topo, algos[int(pts.algo[i])], flat=flat)
+        assert length == int(out["rows"][i, 1])
+        assert paths[i] == path, i

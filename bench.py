@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark of the hot path: batched design-point evaluation of a workload graph.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c3|c2|c4]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c3|c2|c4|c2x|meshx]
                     [--scaling strong|weak]
 
 One *step* = one engine launch per graph family evaluating every design point
@@ -109,7 +109,8 @@ class ClockSampler:
 def load_workload(name: str):
     """The workload and, per part (graph family), its per-rank graphs."""
     from paper_2604_17550_b200 import sweep as S
-    w = {"c3": S.c3_workload, "c2": S.c2_workload, "c4": S.c4_workload}[name]()
+    w = {"c3": S.c3_workload, "c2": S.c2_workload, "c4": S.c4_workload, "c2x": S.c2x_workload,
+         "meshx": S.meshx_workload}[name]()
     return w, [S.part_graphs(w, part) for part in w.parts]
 
 
@@ -121,6 +122,12 @@ WORKLOAD_TEXT = {
     "c4": "BASELINE config 4 (SURVEY.md 8d): llama-70b-like at 8192 ranks, 16384 design points = "
           "{dp:8192 switch ring, dp:8192 switch tree, dp:8192 mesh:64x128 mesh-hier, fsdp:8192 mesh:64x128 "
           "mesh-hier} x 64 bw [10GB/s,1.8TB/s] x 64 latency [100ns,20us]; clusters of 8 CTAs per design point",
+    "c2x": "BASELINE config 2 in EXPANDED comm mode (SURVEY.md 8f row 1): GPT-2 small dp:64, every all-reduce "
+           "lowered to its ring / tree SEND+RECV plan on switch:64 links, 256 design points = {ring, tree} x 16 bw "
+           "[10GB/s,1.8TB/s] x 8 latency [100ns,10us]",
+    "meshx": "The reference's mesh study (test_acceptance.py:260-276) at 8x8: tiny dp:64 on mesh:8x8, collectives "
+             "expanded to ring / mesh-hier SEND+RECV plans with per-link FIFOs, 256 design points = {ring, "
+             "mesh-hier} x 16 bw [10GB/s,1.8TB/s] x 8 latency [100ns,10us]",
 }
 
 
@@ -562,7 +569,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c3", "c2", "c4"], default="c3")
+    ap.add_argument("--workload", choices=["c3", "c2", "c4", "c2x", "meshx"], default="c3")
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
                     help="strong: the grid is split over the GPUs; weak: every GPU a whole grid")
     ap.add_argument("--points", type=int, default=0, help="evaluate an evenly spaced subset of the grid")

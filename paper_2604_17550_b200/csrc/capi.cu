@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <array>
 #include <string>
 #include <vector>
@@ -53,6 +54,7 @@ struct fl_graph {
     size_t hstage_bytes = 0;
     cudaStream_t stream = nullptr;  // fl_sweep_run's own non-blocking stream (not the legacy one)
     int grid_cap = 0;
+    int links_sm_cap = 0;           // link-table capacity reserved in shared memory
     int block = 32;
     int cluster = 1;
     size_t smem = 0;
@@ -171,6 +173,24 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     {
         int rc = upload(g, d->rank_p2p_msg, (size_t)R * dg.p2p_stride, &dg.rank_p2p_msg);
         if (rc) return rc;
+        // the message phase's static tie order (simulator.py:311: source rank, then SEND node_id)
+        std::vector<int32_t> by((size_t)(d->n_msg > 0 ? d->n_msg : 1)), ord(by.size(), 0);
+        for (int m = 0; m < d->n_msg; m++) by[m] = m;
+        std::sort(by.begin(), by.begin() + d->n_msg, [&](int a, int b) {
+            const int64_t ra = d->rank_value[d->msg_send_rank[a]], rb = d->rank_value[d->msg_send_rank[b]];
+            if (ra != rb) return ra < rb;
+            if (d->msg_send_id[a] != d->msg_send_id[b]) return d->msg_send_id[a] < d->msg_send_id[b];
+            return a < b;
+        });
+        for (int k = 0; k < d->n_msg; k++) ord[by[k]] = k;
+        rc = upload(g, ord.data(), ord.size(), &dg.msg_ord);
+        if (rc) return rc;
+        dg.msg_self = 0;
+        dg.msg_min_bytes = INT64_MAX;
+        for (int m = 0; m < d->n_msg; m++) {
+            dg.msg_self |= d->msg_send_rank[m] == d->msg_recv_rank[m];
+            dg.msg_min_bytes = std::min<int64_t>(dg.msg_min_bytes, d->msg_bytes[m]);
+        }
     }
     {
         int rc = upload(g, d->rank_coll_inst, (size_t)R * dg.coll_stride, &dg.rank_coll_inst);
@@ -463,18 +483,18 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     int64_t maxv = 0;
     for (int r = 0; r < R; r++) maxv = d->rank_value[r] > maxv ? d->rank_value[r] : maxv;
     sc.link_cap = d->n_msg > 0 ? (int)std::max<int64_t>(2 * (int64_t)R, 8 * (maxv + 1)) : 0;
-    sc.off_msg = off;
-    off = align_up(off + (size_t)d->n_msg * 8 * 8 + (size_t)d->n_msg * 8 + (size_t)R * 4 +
-                       2 * (size_t)dg.p2p_stride * R * 4 + 64, 256);
+    sc.off_msg = off;                 // [n_msg] 64-byte message records | completion list | in-flight lists
+    off = align_up(off + (size_t)d->n_msg * 64 + (size_t)d->n_msg * 4 + 2 * (size_t)dg.p2p_stride * R * 4 + 64, 256);
     sc.off_ctr = off;  off = align_up(off + 64, 256);
     sc.off_links = off;
-    sc.slot_bytes = align_up(off + (size_t)sc.link_cap * 16, 256);
+    sc.slot_bytes = align_up(off + (size_t)sc.link_cap * 24, 256);
 
     // shared memory: header | comm_end, stats, ring tails | [instances] | [durations] | [done bitmap]
     size_t sm = fl::sweep_shared_header_bytes();
     sc.sm_off_dyn = (unsigned)sm;
     const size_t B = (size_t)g->block;              // shared per-rank arrays have blockDim stride
-    sm = align_up(sm + (size_t)fl::sweep_plane_lanes(g->block, CS) * fl::sweep_shared_bytes_per_rank(), 16);   // per-rank fields (engine.cu F_*, Q_*)
+    sm = align_up(sm + (size_t)fl::sweep_plane_lanes(g->block, CS) * fl::sweep_shared_bytes_per_rank(d->n_msg > 0),
+                  16);   // per-rank fields (engine.cu F_*, Q_*, M_*)
     const size_t budget = (size_t)optin - 1024;   // the kernel's static shared memory (Ctx) comes off the top
     const size_t sbits = (size_t)dg.max_words * B * 8;   // a bitmap over this CTA's ranks
     sc.inst_in_smem = CS == 1 && sm + inst_bytes <= budget;   // clusters share instance state in HBM
@@ -490,9 +510,39 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     sc.touch_in_smem = sm + sbits <= budget;
 #endif
     if (sc.touch_in_smem) { sc.sm_off_touch = (unsigned)sm; sm = align_up(sm + sbits, 16); }
+    // the accumulator slot table [n_acc][R] (single-CTA points: its words are per-rank columns
+    // that only the rank's own thread touches, so plain shared-memory accesses replace the L2
+    // reads on the critical chain of every "last" edge)
+    const size_t acc_bytes = (size_t)dg.n_acc * R * 8;
+#ifdef FL_NO_ACC_SMEM
+    sc.acc_in_smem = false;
+#else
+    sc.acc_in_smem = CS == 1 && acc_bytes <= 64 * 1024 && sm + acc_bytes <= budget;   // (small tables only: occupancy)
+#endif
+    if (sc.acc_in_smem) { sc.sm_off_acc = (unsigned)sm; sm = align_up(sm + acc_bytes, 16); }
+    // the link table [3][link_cap] of the message phase, which only the (lead) CTA runs; a
+    // launch whose meshes need a larger table than reserved here uses the slot's copy in HBM
+    g->links_sm_cap = 0;
+    if (d->n_msg > 0 && sm + (size_t)sc.link_cap * 24 <= budget) {
+        sc.sm_off_links = (unsigned)sm;
+        sm = align_up(sm + (size_t)sc.link_cap * 24, 16);
+        g->links_sm_cap = sc.link_cap;
+    }
     if (sm > budget) return fail(FL_ERR_CAPACITY, "per-rank state exceeds shared memory");
     g->smem = sm;
-    CK(fl::sweep_set_smem(sm));
+    {
+        // the kernels' dynamic shared-memory limit is per function and device, shared by every
+        // handle: only ever raise it (a handle created later with a smaller footprint must not
+        // invalidate the launches of one created earlier)
+        static std::mutex mu;
+        static size_t smem_max[64] = {};
+        std::lock_guard<std::mutex> lock(mu);
+        if (device < 0 || device >= 64) return fail(FL_ERR_INVALID, "device ordinal out of range");
+        if (sm > smem_max[device]) {
+            CK(fl::sweep_set_smem(sm));
+            smem_max[device] = sm;
+        }
+    }
     int occ = 0;
     CK(fl::sweep_occupancy(g->block, g->smem, CS, &occ));
     if (occ < 1) return fail(FL_ERR_CAPACITY, "engine kernel cannot be resident with this shared-memory footprint");
@@ -505,7 +555,7 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
 void grow_links(fl_graph *g, int need) {
     if (g->dg.n_msg <= 0 || need <= g->sc.link_cap) return;
     g->sc.link_cap = need;
-    g->sc.slot_bytes = align_up(g->sc.off_links + (size_t)need * 16, 256);
+    g->sc.slot_bytes = align_up(g->sc.off_links + (size_t)need * 24, 256);
 }
 
 int ensure_scratch(fl_graph *g, int grid) {
@@ -538,6 +588,8 @@ int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stre
     dp.peak_flops = pts->peak_flops;
     dp.efficiency = pts->efficiency;
     dp.compute_streams = cs;
+    fl::DevScratch sc = g->sc;
+    sc.links_in_smem = g->links_sm_cap > 0 && sc.link_cap <= g->links_sm_cap;
     fl::DevOut dout;
     dout.status = out->status;
     dout.rows = out->rows;
@@ -550,7 +602,7 @@ int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stre
     dout.trace_len = out->trace_len;
     dout.trace_cap = out->trace ? out->trace_cap : 0;
     CK(fl::launch_sweep(cs == 3 ? 4 : cs, grid * g->cluster, g->block, g->smem, stream, g->cluster, g->dg, dp, dout,
-                        g->sc));
+                        sc));
     return FL_OK;
 }
 

@@ -177,6 +177,8 @@ struct Shared {
     int cend_uniform;
     int ncomp;
     int nmcomp;
+    double mbeta;                   // this design point's 1e9 / bw and latency (message wire times)
+    int64_t mlat;
     // cluster variant: per-CTA partial results, written by every CTA of the cluster (DSMEM)
     uint64_t xkmin[2][16];
     int64_t xvmax[2][16];
@@ -410,6 +412,30 @@ __device__ __forceinline__ int32_t &F32(int k, int lr) {
     constexpr int SR = plane_lanes<K>();
     return reinterpret_cast<int32_t *>(fl_smem + SM_HDR + (size_t)F_N64 * 8 * SR)[k * SR + lr];
 }
+// Variants with messages (K & 8) add per-rank summaries of the rank's in-flight messages,
+// so that a step reads no message state from HBM unless one of them starts or ends:
+// the earliest end, the earliest start, the earliest start of one whose outputs are not
+// yet allocated (TINF when none), and the list length (the list itself is unordered, in HBM).
+enum { MF_E = 0, MF_S, MF_NA, MF_N64 };
+template <int K>
+__device__ __forceinline__ int64_t &FM64(int k, int lr) {
+    constexpr int SR = plane_lanes<K>();
+    return reinterpret_cast<int64_t *>(fl_smem + SM_HDR + (size_t)(F_N64 * 8 + Q_ALL * 4) * SR)[k * SR + lr];
+}
+template <int K>
+__device__ __forceinline__ int32_t &QMN(int lr) {
+    constexpr int SR = plane_lanes<K>();
+    return reinterpret_cast<int32_t *>(fl_smem + SM_HDR + (size_t)(F_N64 * 8 + Q_ALL * 4 + MF_N64 * 8) * SR)[lr];
+}
+
+// Dynamic state of one point-to-point message (expanded comm mode), one 64-byte record:
+// both endpoints' dispatch times and critical-path starts (simulator.py:259-268), the wire
+// reservation [s, e) (simulator.py:310-327), the completion key and the endpoints to come.
+struct alignas(64) MsgState {
+    int64_t sendt, recvt, cps_s, cps_r, s, e;
+    unsigned long long ckey;
+    int32_t wait, pad;              // (ckey and wait are reset together: one 16-byte store)
+};
 
 // Per-CTA (block-uniform) state pointers.  Bitmaps are word-major,
 // rank-minor ([word][rank]) so a warp's 32 ranks touch one 256-byte segment;
@@ -431,15 +457,14 @@ struct Ctx {
     int32_t *inst_wait, *complist;
     int *ncomp;                     // shared
     // point-to-point messages (expanded comm mode), simulator.py:177-200, :310-327
-    int64_t *msg_sendt, *msg_recvt, *msg_cps_s, *msg_cps_r, *msg_s, *msg_e, *msg_xfer;
-    unsigned long long *msg_ckey;
-    int32_t *msg_wait, *mcomplist;
+    MsgState *msg;                  // [n_msg]
+    int32_t *mcomplist;
     int *nmcomp;                    // shared: messages completed in this step
     int64_t *link_free, *link_busy; // [link_cap]
+    unsigned long long *link_owner; // [link_cap] message-phase claims (KINF when free)
     int link_cap;
-    int32_t *mlist;                 // [p2p_stride][R] per-rank in-flight messages (id | MSG_ALLOC), by end time
+    int32_t *mlist;                 // [p2p_stride][R] per-rank in-flight messages (id | MSG_ALLOC), unordered
     int32_t *mlist_node;            // [p2p_stride][R] this rank's endpoint node of that message
-    int32_t *mcount;                // shared [R]
 };
 
 // This design point's duration of node n: an LDS when the durations are in shared memory
@@ -472,15 +497,19 @@ template <int K> __device__ __forceinline__ uint64_t &touch_ref(const Ctx &c, co
 }
 
 // A node set with its minimum cached in a register and the rest in a global
-// bitmap ([word][rank]).  head < 0: empty; else bits 0-15 = the minimum, bit 16 =
-// the bitmap may be non-empty (invariant: the minimum < every bitmap member).  The
-// due / ready sets rarely hold more than one node, so most inserts and pops are
-// register operations; a pop after an overflow scans the words above the minimum.
+// bitmap ([word][rank]).  head < 0: empty; else bits 0-15 = the minimum, bits 17-30 =
+// the number of bitmap members (saturating at MS_SAT: then "some, maybe none"), so
+// the bitmap is scanned only when it holds a member (invariant: the minimum < every
+// bitmap member).  The due / ready sets rarely hold more than one node, so most
+// inserts and pops are register operations; a pop with bitmap members scans the words
+// above the minimum.
 struct MinSet {
     int head;
 };
-constexpr int MS_MORE = 1 << 16;
+constexpr int MS_SAT = 0x3fff;
 __device__ __forceinline__ int ms_min(const MinSet &m) { return m.head & 0xffff; }
+__device__ __forceinline__ int ms_cnt(const MinSet &m) { return m.head >> 17; }     // (head >= 0)
+__device__ __forceinline__ int ms_inc(int cnt) { return (cnt + (cnt < MS_SAT)) << 17; }
 
 template <int K>
 struct Rank {
@@ -503,6 +532,7 @@ struct Step {                       // block-uniform per-step context
     int fold;                       // static hosts folded (see "t = 0 host pops")
     int touch;                      // first-dependency bitmap in shared memory (else epoch tags)
     int trace;                      // record every node's critical-path finish for the trace walk
+    int acc_sm;                     // the accumulator slot table is in shared memory
 };
 
 __device__ __forceinline__ void bm_set(uint64_t *b, int R, int r, int idx) {
@@ -534,12 +564,12 @@ __device__ __forceinline__ void ms_insert_cp(MinSet &m, uint64_t *b, int64_t *cp
         const int h = ms_min(m);
         cp[h * R + L.r] = F64<K>(F, L.lr);
         bm_set(b, R, L.r, h);
-        m.head = idx | MS_MORE;
+        m.head = idx | ms_inc(ms_cnt(m));
         F64<K>(F, L.lr) = v;
     } else {
         cp[idx * R + L.r] = v;
         bm_set(b, R, L.r, idx);
-        m.head |= MS_MORE;
+        m.head = ms_min(m) | ms_inc(ms_cnt(m));
     }
 }
 
@@ -548,10 +578,11 @@ __device__ __forceinline__ int ms_pop_cp(MinSet &m, uint64_t *b, const int64_t *
                                          int64_t &v, int nwords) {
     const int x = ms_min(m);
     v = F64<K>(F, L.lr);
-    if (m.head & MS_MORE) {
+    const int n = ms_cnt(m);
+    if (n) {
         const int h = bm_pop(b, R, L.r, x, nwords);
         if (h >= 0) {
-            m.head = h | MS_MORE;
+            m.head = h | ((n - (n < MS_SAT)) << 17);
             F64<K>(F, L.lr) = cp[h * R + L.r] & (int64_t)VAL48;
         } else {
             m.head = -1;
@@ -649,14 +680,15 @@ __device__ __forceinline__ void dispatch(const DevGraph &g, const Ctx &c, const 
     const int kind = rec_kind(rb);
     if ((K & 8) && kind >= FL_SEND) {   // simulator.py:259-268: the message is granted once both ends are ready
         const int m = g.rank_p2p_msg[L.r * g.p2p_stride + (int)rb.y];
-        if (kind == FL_SEND) { c.msg_sendt[m] = t; c.msg_cps_s[m] = cps; }
-        else { c.msg_recvt[m] = t; c.msg_cps_r[m] = cps; }
+        MsgState &ms = c.msg[m];
+        if (kind == FL_SEND) { ms.sendt = t; ms.cps_s = cps; }
+        else { ms.recvt = t; ms.cps_r = cps; }
         if (f.step) {
             const unsigned long long key = ((unsigned long long)f.step << 39) | ((unsigned long long)L.r << 25) |
                                            ((unsigned long long)s.pop_seq << 12) | (unsigned long long)seq;
-            atomicMax(&c.msg_ckey[m], key);
+            atomicMax(&ms.ckey, key);
         }
-        if (atomicSub(&c.msg_wait[m], 1) == 1) {
+        if (atomicSub(&ms.wait, 1) == 1) {
             c.mcomplist[atomicAdd(c.nmcomp, 1)] = m;
             if (K & 16) reinterpret_cast<Shared *>(fl_smem)->cflag = 1;
         }
@@ -684,6 +716,13 @@ __device__ __forceinline__ void dispatch(const DevGraph &g, const Ctx &c, const 
     const int64_t fin = cps + dur_of(g, c, L.nb + d);
     if (kind == FL_COMP) ms_insert_cp<K, F_RC_CP, F_RC_SUM>(s.rc, c.rdyc, c.cp, R, L, d, fin);
     else ms_insert_cp<K, F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, d, fin);
+}
+
+// A statically ordered node's accumulator word (capi.cu "Accumulator slots"): in shared
+// memory when the slot table fits there, else an L2 read that bypasses L1 (the words are
+// written with RED operations).
+__device__ __forceinline__ uint64_t acc_read(const Ctx &c, const Step &f, int idx) {
+    return f.acc_sm ? (uint64_t)c.acc[idx] : (uint64_t)__ldcg(c.acc + idx);
 }
 
 // Pop one completion event (simulator.py:335-340) and free tensors whose last
@@ -725,7 +764,7 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
     const uint32_t lo = xa.y >> 24;
     const uint32_t qlast = lo && f.fold ? xa.x + lo - 1 : 0xffffffffu;
     uint64_t alast = 0;
-    if (qlast != 0xffffffffu) alast = (uint64_t)__ldcg(c.acc + ((int)((uint32_t)sl[qlast] >> 19) * R + L.r));
+    if (qlast != 0xffffffffu) alast = acc_read(c, f, (int)((uint32_t)sl[qlast] >> 19) * R + L.r);
     for (uint32_t q = xa.x, qe = xa.x + (xa.y & 0xfffu); q < qe; q++, seq++) {
         const uint32_t ent = (uint32_t)sl[q];
         const int d = (int)(ent & 0xffffu);
@@ -739,8 +778,9 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
             continue;
         }
         if (cls == FL_EDGE_MID) {
-            atomicMax(reinterpret_cast<unsigned long long *>(c.acc + ((int)(ent >> 19) * R + L.r)),
-                      (unsigned long long)(f.epoch | fx));
+            int64_t *const w = c.acc + ((int)(ent >> 19) * R + L.r);
+            if (f.acc_sm) { if ((int64_t)(f.epoch | fx) > *w) *w = (int64_t)(f.epoch | fx); }   // (own column)
+            else atomicMax(reinterpret_cast<unsigned long long *>(w), (unsigned long long)(f.epoch | fx));
             continue;
         }
         int64_t *slot = c.cp + (d * R + L.r);
@@ -752,7 +792,7 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
         }
         if (cls == FL_EDGE_LAST) {
             PROF_MARK(10);                  // edges before a "last" one
-            const uint64_t a = (q == qlast ? alast : (uint64_t)__ldcg(c.acc + ((int)(ent >> 19) * R + L.r))) & VAL48;
+            const uint64_t a = (q == qlast ? alast : acc_read(c, f, (int)(ent >> 19) * R + L.r)) & VAL48;
             dispatch(g, c, L, s, f, d, db, (int64_t)(a > fx ? a : fx), seq, t);
             PROF_MARK(11);                  // "last" edge: accumulator read + dispatch
             continue;
@@ -833,8 +873,8 @@ __device__ __forceinline__ int64_t next_time(const DevGraph &g, const Ctx &c, co
 #pragma unroll
     for (int q = 0; q < (K & 7); q++) if (s.occ_n[q] >= 0 && s.occ_e[q] < nt) nt = s.occ_e[q];
     if (s.head_e < nt) nt = s.head_e;
-    if ((K & 8) && c.mcount[L.r] > 0) {          // in-flight messages, sorted by end time
-        const int64_t e = c.msg_e[c.mlist[L.r] & ~MSG_ALLOC];
+    if (K & 8) {                                  // the earliest end of an in-flight message
+        const int64_t e = FM64<K>(MF_E, L.lr);
         nt = e < nt ? e : nt;
     }
     return nt;
@@ -866,22 +906,32 @@ __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, cons
         F32<K>(Q_RING_HEAD, L.lr)++;
         load_head(c, L, s, R);
     }
-    if (K & 8) {
-        int n = c.mcount[L.r], k = 0;
-        for (; k < n; k++) {
+    if ((K & 8) && FM64<K>(MF_E, L.lr) == t) {   // messages of this rank ending now: their endpoints complete
+        int n = QMN<K>(L.lr);
+        int64_t me = TINF, msn = TINF, mna = TINF;
+        for (int k = 0; k < n;) {
             const int ent = c.mlist[k * R + L.r];
-            if (c.msg_e[ent & ~MSG_ALLOC] != t) break;
-            const int node = c.mlist_node[k * R + L.r];
-            if (!(ent & MSG_ALLOC)) { const uint4 hb = rec_b(g, L.nb + node); F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
-            ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, node, c.cp[node * R + L.r] & (int64_t)VAL48);
-        }
-        if (k) {
-            for (int q = k; q < n; q++) {
-                c.mlist[(q - k) * R + L.r] = c.mlist[q * R + L.r];
-                c.mlist_node[(q - k) * R + L.r] = c.mlist_node[q * R + L.r];
+            const MsgState &ms = c.msg[ent & ~MSG_ALLOC];
+            const int64_t e = ms.e, st = ms.s;
+            if (e == t) {
+                const int node = c.mlist_node[k * R + L.r];
+                if (!(ent & MSG_ALLOC)) { const uint4 hb = rec_b(g, L.nb + node); F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
+                ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, node, c.cp[node * R + L.r] & (int64_t)VAL48);
+                if (k != --n) {         // (unordered list: the last entry takes its place)
+                    c.mlist[k * R + L.r] = c.mlist[n * R + L.r];
+                    c.mlist_node[k * R + L.r] = c.mlist_node[n * R + L.r];
+                }
+                continue;
             }
-            c.mcount[L.r] = n - k;
+            me = e < me ? e : me;
+            msn = st < msn ? st : msn;
+            if (!(ent & MSG_ALLOC)) mna = st < mna ? st : mna;
+            k++;
         }
+        QMN<K>(L.lr) = n;
+        FM64<K>(MF_E, L.lr) = me;
+        FM64<K>(MF_S, L.lr) = msn;
+        FM64<K>(MF_NA, L.lr) = mna;
     }
 }
 
@@ -899,17 +949,23 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
     }
     bool msg_on = false;            // a message of this rank is on the wire during [tcur, tnew)
     if (K & 8) {
-        const int n = c.mcount[L.r];
-        for (int k = 0; k < n; k++) {
-            const int ent = c.mlist[k * R + L.r];
-            if (c.msg_s[ent & ~MSG_ALLOC] <= tcur) {
-                msg_on = true;
-                if (!(ent & MSG_ALLOC)) {
+        msg_on = FM64<K>(MF_S, L.lr) <= tcur;     // (TINF when no message is in flight)
+        if (FM64<K>(MF_NA, L.lr) <= tcur) {      // a message started: allocate its endpoint's outputs
+            const int n = QMN<K>(L.lr);
+            int64_t mna = TINF;
+            for (int k = 0; k < n; k++) {
+                const int ent = c.mlist[k * R + L.r];
+                if (ent & MSG_ALLOC) continue;
+                const int64_t st = c.msg[ent].s;
+                if (st <= tcur) {
                     const uint4 hb = rec_b(g, L.nb + c.mlist_node[k * R + L.r]);
                     F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w);
                     c.mlist[k * R + L.r] = ent | MSG_ALLOC;
+                } else {
+                    mna = st < mna ? st : mna;
                 }
             }
+            FM64<K>(MF_NA, L.lr) = mna;
         }
     }
     {
@@ -950,17 +1006,6 @@ __device__ __forceinline__ bool comp_before(const DevGraph &g, const Ctx &c, int
     return (c.inst_ckey[a] & 0xfff) < (c.inst_ckey[b] & 0xfff);
 }
 
-__device__ __forceinline__ bool msg_before(const DevGraph &g, const Ctx &c, int a, int b, bool init) {
-    // simulator.py:311: (max(send_t, recv_t), src rank, src node id) within one pop
-    if (!init) {
-        const unsigned long long ka = c.msg_ckey[a] >> 12, kb = c.msg_ckey[b] >> 12;
-        if (ka != kb) return ka < kb;
-    }
-    const int64_t ra = g.rank_value[g.msg_send_rank[a]], rb = g.rank_value[g.msg_send_rank[b]];
-    if (ra != rb) return ra < rb;
-    return g.msg_send_id[a] < g.msg_send_id[b];
-}
-
 // Visit the directed links of a src->dst message in route order
 // (topology.py:68-86); ids: switch eg/in of rank index i -> 2i / 2i+1,
 // mesh a -> neighbour: 4a + {+col, -col, +row, -row}.
@@ -988,52 +1033,98 @@ __device__ __forceinline__ int64_t transfer_ns(const DevGraph &g, int topo, int 
     return rhu(__dadd_rn((double)(hops * lat), __dmul_rn((double)bytes, beta)));
 }
 
-// Message phase (simulator.py:310-327), one thread: FIFO per link, a message holds
-// every link on its route for the whole transfer.
+// Message phase (simulator.py:310-327): FIFO per link, a message holds every link on its
+// route for the whole transfer, messages are granted in (completing pop, source rank id,
+// SEND node id) order.  Only messages that share a link interact, so the phase runs on the
+// whole CTA in rounds: each pending message claims its links with an atomicMin of its
+// order key, a message that holds every one of its links is the earliest pending user of
+// each and is granted (reads and advances their free times), then the claims are released.
+// A message is granted only after every earlier message sharing one of its links, so the
+// result is the reference's sequential loop; messages on disjoint links (a ring step: every
+// rank sends to its neighbour) are granted in one round.
+//   key: completing pop (rank << 13 | pop sequence, the reservation's step is common) << 32
+//        | the message's static (source rank id, SEND id) order (capi.cu msg_ord)
+constexpr int32_t MQ_DONE = 1 << 30;     // mcomplist entry granted in the current round
+__device__ __forceinline__ unsigned long long msg_key(const DevGraph &g, const Ctx &c, int m, bool init) {
+    const unsigned long long pop = init ? 0ull : (c.msg[m].ckey >> 12) & ((1ull << 27) - 1);
+    return (pop << 32) | (uint32_t)g.msg_ord[m];
+}
+
+// Rank rr's in-flight summary field (or list length): this CTA's shared memory, or in a
+// cluster the owning CTA's, through distributed shared memory (1024 ranks per CTA).
+template <int K, bool CL>
+__device__ __forceinline__ int64_t *msg_field(int k, int rr) {
+    if constexpr (!CL) return &FM64<K>(k, rr);
+    else return cg::this_cluster().map_shared_rank(&FM64<K>(k, rr & 1023), rr >> 10);
+}
+template <int K, bool CL>
+__device__ __forceinline__ int32_t *msg_count(int rr) {
+    if constexpr (!CL) return &QMN<K>(rr);
+    else return cg::this_cluster().map_shared_rank(&QMN<K>(rr & 1023), rr >> 10);
+}
+
+template <int K, bool CL>
 static __device__ void reserve_msgs(const DevGraph &g, const DevOut &o, const Ctx &c, int nm, bool init, int topo,
-                             int cols, int cfg, uint64_t epoch, int64_t &cpm) {
-    const int R = g.R;                      // (a kernel parameter: no shared-memory load)
-    for (int a = 1; a < nm; a++) {
-        const int x = c.mcomplist[a];
-        int b = a - 1;
-        while (b >= 0 && msg_before(g, c, x, c.mcomplist[b], init)) { c.mcomplist[b + 1] = c.mcomplist[b]; b--; }
-        c.mcomplist[b + 1] = x;
-    }
-    for (int q = 0; q < nm; q++) {
-        const int m = c.mcomplist[q];
-        const int si = g.msg_send_rank[m], di = g.msg_recv_rank[m];
-        int64_t st = c.msg_sendt[m] > c.msg_recvt[m] ? c.msg_sendt[m] : c.msg_recvt[m];
-        for_route(g, topo, cols, si, di, [&](int l) { st = c.link_free[l] > st ? c.link_free[l] : st; });
-        const int64_t xf = c.msg_xfer[m], e = st + xf;
-        for_route(g, topo, cols, si, di, [&](int l) {
-            c.link_free[l] = e;
-            const int64_t b0 = c.link_busy[l];
-            c.link_busy[l] = (b0 < 0 ? 0 : b0) + (e - st);
-        });
-        c.msg_s[m] = st;
-        c.msg_e[m] = e;
-        // critical path: a RECV also waits for its SEND plus the wire (simulator.py:430-435, :450-452)
-        const int64_t cs = c.msg_cps_s[m];
-        const int64_t cr = c.msg_cps_r[m] > cs + xf ? c.msg_cps_r[m] : cs + xf;
-        cpm = cr > cpm ? cr : cpm;
-        cpm = cs > cpm ? cs : cpm;
-        const int sn = g.msg_send_node[m], dn = g.msg_recv_node[m];
-        c.cp[sn * R + si] = (int64_t)(epoch | (uint64_t)cs);
-        c.cp[dn * R + di] = (int64_t)(epoch | (uint64_t)cr);
-        record(g, o, cfg, si, sn, st, e);
-        record(g, o, cfg, di, dn, st, e);
-        for (int side = 0; side < 2; side++) {     // both endpoints' in-flight lists, ordered by end
-            const int rr = side ? di : si, node = side ? dn : sn;
-            int k = c.mcount[rr];
-            while (k > 0 && c.msg_e[c.mlist[(k - 1) * R + rr] & ~MSG_ALLOC] > e) {
-                c.mlist[k * R + rr] = c.mlist[(k - 1) * R + rr];
-                c.mlist_node[k * R + rr] = c.mlist_node[(k - 1) * R + rr];
-                k--;
-            }
-            c.mlist[k * R + rr] = m;
-            c.mlist_node[k * R + rr] = node;
-            c.mcount[rr]++;
+                                    int cols, int cfg, uint64_t epoch, int64_t lat, double beta) {
+    const int R = g.R, tid = threadIdx.x, bd = blockDim.x;
+    unsigned long long *own = c.link_owner;           // KINF between phases
+    for (;;) {
+        int left = 0;
+        for (int q = tid; q < nm; q += bd) {           // claim
+            const int m = c.mcomplist[q];
+            if (m < 0) continue;
+            left = 1;
+            const unsigned long long k = msg_key(g, c, m, init);
+            for_route(g, topo, cols, g.msg_send_rank[m], g.msg_recv_rank[m], [&](int l) { atomicMin(&own[l], k); });
         }
+        if (!__syncthreads_or(left)) break;
+        for (int q = tid; q < nm; q += bd) {           // grant the messages holding all their links
+            const int m = c.mcomplist[q];
+            if (m < 0) continue;
+            const int si = g.msg_send_rank[m], di = g.msg_recv_rank[m];
+            const unsigned long long k = msg_key(g, c, m, init);
+            bool mine = true;
+            for_route(g, topo, cols, si, di, [&](int l) { mine &= *(volatile unsigned long long *)&own[l] == k; });
+            if (!mine) continue;
+            MsgState &ms = c.msg[m];
+            int64_t st = ms.sendt > ms.recvt ? ms.sendt : ms.recvt;
+            for_route(g, topo, cols, si, di, [&](int l) { st = c.link_free[l] > st ? c.link_free[l] : st; });
+            const int64_t xf = transfer_ns(g, topo, cols, si, di, g.msg_bytes[m], lat, beta), e = st + xf;
+            for_route(g, topo, cols, si, di, [&](int l) {
+                c.link_free[l] = e;
+                const int64_t b0 = c.link_busy[l];
+                c.link_busy[l] = (b0 < 0 ? 0 : b0) + (e - st);
+            });
+            ms.s = st;
+            ms.e = e;
+            // critical path: a RECV also waits for its SEND plus the wire (simulator.py:430-435, :450-452)
+            const int64_t cs = ms.cps_s;
+            const int64_t cr = ms.cps_r > cs + xf ? ms.cps_r : cs + xf;
+            const int sn = g.msg_send_node[m], dn = g.msg_recv_node[m];
+            c.cp[sn * R + si] = (int64_t)(epoch | (uint64_t)cs);
+            c.cp[dn * R + di] = (int64_t)(epoch | (uint64_t)cr);
+            record(g, o, cfg, si, sn, st, e);
+            record(g, o, cfg, di, dn, st, e);
+            for (int side = 0; side < 2; side++) {     // both endpoints' in-flight lists and summaries
+                const int rr = side ? di : si;
+                const int k2 = atomicAdd(msg_count<K, CL>(rr), 1);
+                c.mlist[k2 * R + rr] = m;
+                c.mlist_node[k2 * R + rr] = side ? dn : sn;
+                atomicMin(reinterpret_cast<long long *>(msg_field<K, CL>(MF_E, rr)), (long long)e);
+                atomicMin(reinterpret_cast<long long *>(msg_field<K, CL>(MF_S, rr)), (long long)st);
+                atomicMin(reinterpret_cast<long long *>(msg_field<K, CL>(MF_NA, rr)), (long long)st);
+            }
+            c.mcomplist[q] = m | MQ_DONE;
+        }
+        __syncthreads();
+        for (int q = tid; q < nm; q += bd) {           // release every claim of this round
+            const int e = c.mcomplist[q];
+            if (e < 0) continue;
+            const int m = e & ~MQ_DONE;
+            for_route(g, topo, cols, g.msg_send_rank[m], g.msg_recv_rank[m], [&](int l) { own[l] = KINF; });
+            if (e & MQ_DONE) c.mcomplist[q] = -1;
+        }
+        __syncthreads();
     }
 }
 
@@ -1052,7 +1143,6 @@ __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o,
     // counter could be reset (the instance times it writes are per-CTA copies).
     constexpr bool MONO = CL && !MSG;
     int32_t *const cl = c.complist + (MONO ? sh.ncons : 0);
-    int64_t cpm = 0;                // (critical path of the messages; members carry the collectives')
     int64_t efirst = -1;            // end of the first reserved instance ...
     bool allfull = true;            // ... if every one spanned the world with uniform comm streams
     if (nc > 1) {                   // one thread orders the list (shared by the cluster's CTAs)
@@ -1123,14 +1213,17 @@ __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o,
         sh.cflag = 0;
         if (MONO) sh.ncons += nc;
     }
-    if (!MONO && (!CL || c.lead_cta) && threadIdx.x == 0) {
-        if (CL) *c.ncomp = 0; else sh.ncomp = 0;
-        if (MSG && nmc) reserve_msgs(g, o, c, nmc, init, topo, cols, cfg, epoch, cpm);
-        if (MSG) { if (CL) *c.nmcomp = 0; else sh.nmcomp = 0; }
-    }
+    if (!MONO && (!CL || c.lead_cta) && threadIdx.x == 0) { if (CL) *c.ncomp = 0; else sh.ncomp = 0; }
     // Without messages nothing written above is read before the caller's next barrier
-    // (its step reduction, or reserve()'s own); the message phase fills other ranks' lists.
-    if (MSG) gsync<CL>();
+    // (its step reduction, or reserve()'s own).  The message phase runs on the (lead) CTA
+    // and fills other ranks' in-flight lists, which their own threads then order.
+    if (MSG && nmc) {
+        if (!CL || c.lead_cta) {
+            reserve_msgs<K, CL>(g, o, c, nmc, init, topo, cols, cfg, epoch, sh.mlat, sh.mbeta);
+            if (threadIdx.x == 0) { if (CL) *c.nmcomp = 0; else sh.nmcomp = 0; }
+        }
+        gsync<CL>();
+    }
     return allfull && !(MSG && nmc) ? efirst : -1;
 }
 
@@ -1267,7 +1360,8 @@ __global__ void __launch_bounds__(1024, 1)
         c.touched = sc.touch_in_smem ? reinterpret_cast<uint64_t *>(smem + sc.sm_off_touch) : gbits + 4 * words;
         c.BR = sc.touch_in_smem ? bd : R;
         c.cp = reinterpret_cast<int64_t *>(base + sc.off_cp);
-        c.acc = reinterpret_cast<int64_t *>(base + sc.off_acc);
+        c.acc = sc.acc_in_smem ? reinterpret_cast<int64_t *>(smem + sc.sm_off_acc)
+                               : reinterpret_cast<int64_t *>(base + sc.off_acc);
         c.ring_inst = reinterpret_cast<int32_t *>(base + sc.off_ring);
         c.ring_node = c.ring_inst + (size_t)g.coll_stride * R;
         c.dur = sc.dur_in_smem ? reinterpret_cast<int64_t *>(smem + sc.sm_off_dur)
@@ -1290,22 +1384,14 @@ __global__ void __launch_bounds__(1024, 1)
         c.nmcomp = CL ? ctr + 1 : &sh.nmcomp;
         c.lead_cta = crank == 0;
         const int M = g.n_msg;
-        int64_t *mb = reinterpret_cast<int64_t *>(base + sc.off_msg);
-        c.msg_sendt = mb;
-        c.msg_recvt = mb + M;
-        c.msg_cps_s = mb + 2 * M;
-        c.msg_cps_r = mb + 3 * M;
-        c.msg_s = mb + 4 * M;
-        c.msg_e = mb + 5 * M;
-        c.msg_xfer = mb + 6 * M;
-        c.msg_ckey = reinterpret_cast<unsigned long long *>(mb + 7 * M);
-        c.link_free = reinterpret_cast<int64_t *>(base + sc.off_links);
+        c.msg = reinterpret_cast<MsgState *>(base + sc.off_msg);
+        c.link_free = sc.links_in_smem ? reinterpret_cast<int64_t *>(smem + sc.sm_off_links)
+                                       : reinterpret_cast<int64_t *>(base + sc.off_links);
         c.link_busy = c.link_free + sc.link_cap;
+        c.link_owner = reinterpret_cast<unsigned long long *>(c.link_busy + sc.link_cap);
         c.link_cap = sc.link_cap;
-        c.msg_wait = reinterpret_cast<int32_t *>(mb + 8 * M);
-        c.mcomplist = c.msg_wait + M;
-        c.mcount = c.mcomplist + M;
-        c.mlist = c.mcount + R;
+        c.mcomplist = reinterpret_cast<int32_t *>(c.msg + M);
+        c.mlist = c.mcomplist + M;
         c.mlist_node = c.mlist + (size_t)g.p2p_stride * R;
     }
     __syncthreads();
@@ -1368,20 +1454,23 @@ __global__ void __launch_bounds__(1024, 1)
             if (!CL) { c.inst_s[i] = 0; c.inst_e[i] = 0; }
         }
         if (CL) for (int i = tid; i < NI; i += bd) { c.inst_s[i] = 0; c.inst_e[i] = 0; }   // (per-CTA copies)
-        if (K & 8) {                // messages: wire time per design point, fresh link state
+        if (K & 8) {                // messages: fresh message and link state
             const double beta = __ddiv_rn(1e9, bwv);
             const int cols = p.cols[cfg];
             if (topo == FL_MESH2D && (cols <= 0 || 4LL * p.rows[cfg] * cols > c.link_cap)) cap_bad = 1;
-            for (int m = gt; m < g.n_msg; m += gstride) {
-                const int64_t xf = cap_bad ? 0 : transfer_ns(g, topo, cols, g.msg_send_rank[m], g.msg_recv_rank[m],
-                                                         g.msg_bytes[m], lat, beta);
-                zero |= xf == 0;
-                c.msg_xfer[m] = xf;
-                c.msg_wait[m] = 2;
-                c.msg_ckey[m] = 0ull;
-            }
-            for (int l = gt; l < c.link_cap; l += gstride) { c.link_free[l] = 0; c.link_busy[l] = -1; }
-            if (active) c.mcount[L.r] = 0;
+            // a zero wire time would put events at the reservation's own time (serial mode); the
+            // smallest possible one is one hop of the smallest message (transfer_ns is monotone)
+            if (g.msg_self || (g.n_msg > 0 && rhu(__dadd_rn((double)lat, __dmul_rn((double)g.msg_min_bytes, beta))) == 0))
+                zero = 1;
+            if (tid == 0) { sh.mbeta = beta; sh.mlat = lat; }
+            for (int m = gt; m < g.n_msg; m += gstride)     // ckey = 0, wait = 2 (one 16-byte store)
+                *reinterpret_cast<uint4 *>(&c.msg[m].ckey) = make_uint4(0u, 0u, 2u, 0u);
+            if (!CL || crank == 0)  // (only the lead CTA runs the message phase: links may be in its shared memory)
+                for (int l = tid; l < c.link_cap; l += bd) { c.link_free[l] = 0; c.link_busy[l] = -1; c.link_owner[l] = KINF; }
+            FM64<K>(MF_E, tid) = TINF;
+            FM64<K>(MF_S, tid) = TINF;
+            FM64<K>(MF_NA, tid) = TINF;
+            QMN<K>(tid) = 0;
         }
         const bool recost = p.peak_flops != nullptr;
         const double pk = recost ? p.peak_flops[cfg] : 0.0, ef = recost ? p.efficiency[cfg] : 0.0;
@@ -1435,6 +1524,7 @@ __global__ void __launch_bounds__(1024, 1)
         f.init = 1;
         f.fold = g.fold_ok && !zero && !zdur;
         f.touch = sc.touch_in_smem;
+        f.acc_sm = sc.acc_in_smem;
         f.trace = o.trace_len != nullptr;
 
         // ---- per-rank state ----
@@ -1585,12 +1675,12 @@ __global__ void __launch_bounds__(1024, 1)
                 // serial mode: the reference loop verbatim, one pop per iteration
                 if (active) gather_due(g, c, L, s, t);
                 for (;;) {
-                    const uint64_t k2 = (active && s.due.head >= 0) ? (((uint64_t)L.r << 13) | (uint64_t)ms_min(s.due))
+                    const uint64_t k2 = (active && s.due.head >= 0) ? (((uint64_t)L.r << 16) | (uint64_t)ms_min(s.due))
                                                                      : KINF;
                     const uint64_t m2 = gmin_key<CL>(k2, sh, par);
                     if (m2 == KINF) break;
                     f.step++;
-                    if (active && (int)(m2 >> 13) == L.r) {
+                    if (active && (int)(m2 >> 16) == L.r) {
                         s.pop_seq = 0;
                         int64_t fx;
                         const int x = ms_pop_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, fx, g.max_words);
@@ -1610,7 +1700,8 @@ __global__ void __launch_bounds__(1024, 1)
 #ifdef FL_PROFILE
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&fl_prof[15], 1ull);
         if (blockIdx.x == 0 && threadIdx.x == 0 && cfg + ncl >= p.n) {
-            printf("FLPROF points %llu", fl_prof[15]);
+            printf("FLPROF points %llu steps(last point) %llu zero %d fold %d", fl_prof[15],
+                   (unsigned long long)f.step, zero, f.fold);
             for (int k = 0; k < 15; k++) printf(" s%d %llu", k, fl_prof[k]);
             printf("\n");
         }
@@ -1843,7 +1934,7 @@ cudaError_t sweep_set_smem(size_t smem) {
 }
 
 size_t sweep_shared_header_bytes() { return SM_HDR; }
-size_t sweep_shared_bytes_per_rank() { return 8 * F_N64 + 4 * Q_ALL; }   // x plane lanes
+size_t sweep_shared_bytes_per_rank(bool msg) { return 8 * F_N64 + 4 * Q_ALL + (msg ? 8 * MF_N64 + 4 : 0); }   // x plane lanes
 int sweep_plane_lanes(int block, int cluster) { return cluster > 1 ? 1024 : plane_lanes_for(block); }
 
 cudaError_t launch_cp(const DevGraph &g, const DevPoints &p, int nv, const int32_t *order, const int32_t *vkind,

@@ -42,6 +42,9 @@ struct DevGraph {
     int n_msg, p2p_stride;
     const int32_t *msg_send_rank, *msg_send_node, *msg_recv_rank, *msg_recv_node, *rank_p2p_msg;
     const int64_t *msg_bytes, *msg_send_id;
+    const int32_t *msg_ord;      // [M] position in (source rank id, SEND node_id) order (simulator.py:311)
+    int msg_self;                // some message has the same source and destination rank (zero wire time)
+    int64_t msg_min_bytes;       // smallest message
 };
 
 struct DevPoints {
@@ -70,12 +73,13 @@ struct DevScratch {
     size_t off_acc;              // [n_acc][R] int64: accumulators of statically ordered nodes, by slot
     // dynamic shared-memory layout (bytes from the start of the CTA's smem)
     size_t off_msg;              // message state, per-rank in-flight lists
-    size_t off_links;            // link state [2][link_cap] (last in the slot: grows per launch)
+    size_t off_links;            // link state [3][link_cap]: free-at, busy, message-phase claim (last in the slot: grows per launch)
     size_t off_ctr;              // cluster-wide completion counters
     size_t off_inst_se;          // clusters: per-CTA copies of the instances' reservation start / end
     int link_cap;
-    unsigned sm_off_dyn, sm_off_done, sm_off_dur, sm_off_inst, sm_off_touch;
-    int done_in_smem, dur_in_smem, inst_in_smem, touch_in_smem;
+    unsigned sm_off_dyn, sm_off_done, sm_off_dur, sm_off_inst, sm_off_touch, sm_off_acc, sm_off_links;
+    int done_in_smem, dur_in_smem, inst_in_smem, touch_in_smem, acc_in_smem;
+    int links_in_smem;           // the link table is in the (lead) CTA's shared memory (per launch: it grows)
 };
 
 cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t st, int cluster, const DevGraph &g,
@@ -83,7 +87,7 @@ cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t s
 cudaError_t sweep_occupancy(int block, size_t smem, int cluster, int *occ);
 cudaError_t sweep_set_smem(size_t smem);
 size_t sweep_shared_header_bytes();
-size_t sweep_shared_bytes_per_rank();   // the [field][blockDim] per-rank planes
+size_t sweep_shared_bytes_per_rank(bool msg);   // the [field][blockDim] per-rank planes (msg: + message summaries)
 int sweep_plane_lanes(int block, int cluster);   // per-rank planes are this many lanes wide
 cudaError_t launch_cp(const DevGraph &g, const DevPoints &p, int nv, const int32_t *order, const int32_t *vkind,
                       const int32_t *va, const int32_t *vb, const int32_t *vsend, const int32_t *vmsg,

@@ -32,7 +32,10 @@ def child(name, workload, points, reps):
     if ":" in workload:                 # e.g. c3:512 -- the C3 grid on fsdp:512 (scaling probes)
         workload, ranks = workload.split(":")[0], int(workload.split(":")[1])
     part = {"c4dp": 0, "c4fsdp": 1}.get(workload, 0)     # one family of the C4 grid
-    w = {"c3": S.c3_workload, "c2": S.c2_workload, "c4dp": S.c4_workload, "c4fsdp": S.c4_workload}[workload]()
+    if "." in workload:                 # e.g. c2x.1 -- family 1 of a multi-family workload
+        workload, part = workload.split(".")[0], int(workload.split(".")[1])
+    w = {"c3": S.c3_workload, "c2": S.c2_workload, "c4dp": S.c4_workload, "c4fsdp": S.c4_workload,
+         "c2x": S.c2x_workload, "meshx": S.meshx_workload}[workload]()
     w.parts = [w.parts[part]]
     if ranks:
         w.parts[0].parallel = f"fsdp:{ranks}"

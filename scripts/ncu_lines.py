@@ -43,3 +43,10 @@ for l, (i, s) in per_line.items():
 print(f"total warp instructions {tot_i:.4g}  ({tot_i / norm:.0f} per norm unit)")
 for f, (i, s) in sorted(agg.items(), key=lambda x: -x[1][0]):
     print(f"  {f:40s} inst {i / tot_i * 100:5.1f}% ({i / norm:9.0f})  stalls {s / tot_s * 100:5.1f}%")
+if len(sys.argv) > 4:           # top source lines by executed instructions
+    src = open(src_file).read().splitlines()
+    top = int(sys.argv[4])
+    print("top lines (inst %, stall %):")
+    for l, (i, s) in sorted(per_line.items(), key=lambda x: -x[1][0])[:top]:
+        text = src[l - 1].strip()[:110] if l and l <= len(src) else "?"
+        print(f"  {l!s:>5} {i / tot_i * 100:5.1f}% {s / tot_s * 100:5.1f}%  {text}")

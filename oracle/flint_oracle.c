@@ -283,6 +283,59 @@ typedef struct {
     int64_t *lead;       /* flat node of members[0] */
 } instances;
 
+static int cmp_pair(const void *a, const void *b) {
+    const int64_t *x = a, *y = b;
+    if (x[0] != y[0]) return x[0] < y[0] ? -1 : 1;
+    return x[1] < y[1] ? -1 : x[1] > y[1];
+}
+
+/* (rank value, dependency id) pairs of the members' dependencies, ranks taken from `rk`
+ * (member q's rank index) -- sorted, for the set comparison below. */
+static int64_t dep_pairs(const or_graphs *G, const vec *members, const int64_t *rk, int64_t **out) {
+    int64_t n = 0;
+    for (int64_t q = 0; q < members->n; q++) {
+        int64_t sv = SV(G, members->a[q]);
+        n += G->dep_off[sv + 1] - G->dep_off[sv];
+    }
+    int64_t *p = malloc((size_t)(2 * n + 2) * sizeof(int64_t)), k = 0;
+    for (int64_t q = 0; q < members->n; q++) {
+        int64_t sv = SV(G, members->a[q]);
+        for (int64_t d = G->dep_off[sv]; d < G->dep_off[sv + 1]; d++) {
+            p[2 * k] = G->rank_value[rk[q]]; p[2 * k + 1] = G->dep_ids[d]; k++;
+        }
+    }
+    qsort(p, (size_t)n, 2 * sizeof(int64_t), cmp_pair);
+    int64_t u = 0;                                   /* set semantics */
+    for (int64_t i = 0; i < n; i++)
+        if (u == 0 || p[2 * i] != p[2 * u - 2] || p[2 * i + 1] != p[2 * u - 1]) { p[2 * u] = p[2 * i]; p[2 * u + 1] = p[2 * i + 1]; u++; }
+    *out = p;
+    return u;
+}
+
+/* zip(group, members) equals the natural pairing: members[q] carries the node_id of rank
+ * group[q]'s own member, and the union of dependencies is the same under both pairings. */
+static int zip_pairing_is_natural(const or_graphs *G, const lookup *L, int64_t g0, const vec *members,
+                                  const vec *mrank) {
+    int64_t n = members->n;
+    int64_t *zr = malloc((size_t)(n + 1) * sizeof(int64_t));
+    int ok = 1;
+    for (int64_t q = 0; q < n && ok; q++) {
+        int64_t r = rank_index(L, G->grp_rank[g0 + q]);
+        zr[q] = r;
+        int64_t own = -1;
+        for (int64_t j = 0; j < n; j++) if (mrank->a[j] == r) { own = members->a[j]; break; }
+        ok = own >= 0 && G->node_id[SV(G, own)] == G->node_id[SV(G, members->a[q])];
+    }
+    if (ok) {
+        int64_t *a, *b;
+        int64_t na = dep_pairs(G, members, mrank->a, &a), nb = dep_pairs(G, members, zr, &b);
+        ok = na == nb && memcmp(a, b, (size_t)(2 * na) * sizeof(int64_t)) == 0;
+        free(a); free(b);
+    }
+    free(zr);
+    return ok;
+}
+
 /* collectives.py:419-453 (instance order = discovery order) */
 static int match_instances(const or_graphs *G, const lookup *L, instances *I, int64_t *inst_of,
                            char *err, int errlen) {
@@ -305,8 +358,9 @@ static int match_instances(const or_graphs *G, const lookup *L, instances *I, in
         int64_t lv = colls[start].a[idx[start]];
         int64_t g0 = G->grp_off[SV(G, lv)], g1 = G->grp_off[SV(G, lv) + 1];
         /* members = [lead] + others in group order; pairs = zip(group, members) */
-        vec members = {0};
+        vec members = {0}, mrank = {0};
         vpush(&members, lv);
+        vpush(&mrank, start);
         for (int64_t k = g0; k < g1; k++) {
             int64_t rv = G->grp_rank[k];
             int64_t r = rank_index(L, rv);
@@ -324,27 +378,37 @@ static int match_instances(const or_graphs *G, const lookup *L, instances *I, in
                     if (G->grp_rank[G->grp_off[SV(G, ov)] + q] != G->grp_rank[g0 + q]) { same = 0; break; }
             if (!same) {
                 set_err(err, errlen, "collective disagrees across ranks");
-                rc = OR_INCONSISTENT; free(members.a); goto done;
+                rc = OR_INCONSISTENT; free(members.a); free(mrank.a); goto done;
             }
             vpush(&members, ov);
+            vpush(&mrank, r);
         }
-        /* the reference zips group with members; that pairs each rank with its own
-         * node only when the lead rank is group[0] (ascending groups, as every
-         * producer emits).  Anything else is rejected rather than mis-paired. */
-        if (members.n != g1 - g0 || rank_index(L, G->grp_rank[g0]) != start) {
-            set_err(err, errlen, "collective group must list the lead rank first");
-            rc = OR_INCONSISTENT; free(members.a); goto done;
+        /* The reference pairs zip(group, members) (simulator.py:222-223, :419-425): rank
+         * group[q] with members[q], where members = [lead] + the others in group order.  With
+         * the lead listed first (ascending groups, as every producer emits) that is each rank
+         * with its own node.  Otherwise it is the same pairing exactly when members[q] has the
+         * node_id of rank group[q]'s own collective and the zipped union of the members'
+         * dependencies equals the natural one (critical_path, simulator.py:419-428); anything
+         * else is rejected (the reference fails there with a KeyError or a spurious cycle). */
+        if (members.n != g1 - g0) {
+            set_err(err, errlen, "collective group lists a rank twice");
+            rc = OR_INCONSISTENT; free(members.a); free(mrank.a); goto done;
+        }
+        if (rank_index(L, G->grp_rank[g0]) != start &&
+            !zip_pairing_is_natural(G, L, g0, &members, &mrank)) {
+            set_err(err, errlen, "collective group pairs ranks with other ranks' nodes (zip(group, members))");
+            rc = OR_INCONSISTENT; free(members.a); free(mrank.a); goto done;
         }
         int64_t id = lead.n;
         for (int64_t q = 0; q < members.n; q++) {
-            int64_t r = rank_index(L, G->grp_rank[g0 + q]);
-            vpush(&mr, r); vpush(&mn, members.a[q]);
+            vpush(&mr, mrank.a[q]); vpush(&mn, members.a[q]);
             inst_of[members.a[q]] = id;
         }
         vpush(&lead, lv);
         vpush(&off, mr.n);
         for (int64_t k = g0; k < g1; k++) { int64_t r = rank_index(L, G->grp_rank[k]); idx[r]++; }
         free(members.a);
+        free(mrank.a);
     }
 done:
     for (int64_t r = 0; r < nr; r++) free(colls[r].a);

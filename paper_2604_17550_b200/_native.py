@@ -128,6 +128,16 @@ class Outputs(C.Structure):
                 ("trace", P64), ("trace_len", P32), ("trace_cap", C.c_int32)]
 
 
+class PointsRaw(C.Structure):
+    """fl_points with untyped pointers (same layout as Points): filled from raw addresses on the
+    per-call path, where building typed ctypes pointers costs more than the call itself."""
+    _fields_ = [(n, C.c_void_p if t not in (C.c_int32,) else t) for n, t in Points._fields_]
+
+
+class OutputsRaw(C.Structure):
+    _fields_ = [(n, C.c_void_p if t not in (C.c_int32,) else t) for n, t in Outputs._fields_]
+
+
 _lib = None
 
 
@@ -172,7 +182,7 @@ def _bind(L):
     L.fl_graph_destroy.argtypes = [C.c_void_p]
     L.fl_graph_max_nodes.argtypes = [C.c_void_p]
     L.fl_graph_max_nodes.restype = C.c_int32
-    L.fl_sweep_run.argtypes = [C.c_void_p, C.POINTER(Points), C.POINTER(Outputs)]
+    L.fl_sweep_run.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]       # (fl_points *, fl_outputs *) by address
     L.fl_sweep_run_device.argtypes = [C.c_void_p, C.POINTER(Points), C.POINTER(Outputs), C.c_void_p, P32]
     L.fl_critical_path.argtypes = [C.c_void_p, C.POINTER(Points), C.c_int32, P32, P32, P32, P32, P32, P32, P32,
                                    P32, P64, P32]

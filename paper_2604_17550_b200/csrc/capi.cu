@@ -482,9 +482,15 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     // its points' mesh shapes) -- see grow_links.
     int64_t maxv = 0;
     for (int r = 0; r < R; r++) maxv = d->rank_value[r] > maxv ? d->rank_value[r] : maxv;
+    bool neg = false;
+    for (int r = 0; r < R; r++) neg |= d->rank_value[r] < 0;
+    if (d->n_msg > 0 && (maxv >= ((int64_t)1 << 27) || neg))
+        return fail(FL_ERR_CAPACITY, "rank ids of graphs with SEND/RECV must be in [0, 2^27) (link ids)");
     sc.link_cap = d->n_msg > 0 ? (int)std::max<int64_t>(2 * (int64_t)R, 8 * (maxv + 1)) : 0;
     sc.off_msg = off;                 // [n_msg] 64-byte message records | completion list | in-flight lists
     off = align_up(off + (size_t)d->n_msg * 64 + (size_t)d->n_msg * 4 + 2 * (size_t)dg.p2p_stride * R * 4 + 64, 256);
+    sc.off_mlist_se = off;
+    off = align_up(off + (d->n_msg > 0 ? 2 * (size_t)dg.p2p_stride * R * 8 : 0), 256);
     sc.off_ctr = off;  off = align_up(off + 64, 256);
     sc.off_links = off;
     sc.slot_bytes = align_up(off + (size_t)sc.link_cap * 24, 256);
@@ -723,36 +729,47 @@ int fl_sweep_run(fl_graph *g, const fl_points *hp, fl_outputs *ho) {
         if (g->hstage) cudaFreeHost(g->hstage);
         g->hstage = nullptr;
         g->hstage_bytes = 0;
-        CK(cudaHostAlloc(&g->hstage, small_end, cudaHostAllocDefault));
+        CK(cudaHostAlloc(&g->hstage, small_end, cudaHostAllocMapped));
         g->hstage_bytes = small_end;
     }
     unsigned char *S = g->stage, *H = g->hstage;
     for (auto &p : in)
         if (p.bytes) memcpy(H + p.off, p.src, p.bytes);
-    CK(cudaMemcpyAsync(S, H, in_bytes, cudaMemcpyHostToDevice, st));
+    // With at most one design point per CTA, the kernel reads each point's parameters once and
+    // writes its row once, so it does so over the bus from the mapped staging block itself:
+    // no copy engine round trips for a few KB (the bulk outputs below still use copies).
+    const bool zc = n <= (size_t)g->grid_cap;
+    unsigned char *small = S;                      // where the inputs and per-point outputs live
+    if (zc) {
+        void *dh = nullptr;
+        CK(cudaHostGetDevicePointer(&dh, H, 0));
+        small = static_cast<unsigned char *>(dh);
+    } else {
+        CK(cudaMemcpyAsync(S, H, in_bytes, cudaMemcpyHostToDevice, st));
+    }
     fl_points dp = *hp;
-    dp.algo = S + in[0].off;
-    dp.topo_kind = S + in[1].off;
-    dp.bw = reinterpret_cast<const double *>(S + in[2].off);
-    dp.latency = reinterpret_cast<const int64_t *>(S + in[3].off);
-    dp.rows = reinterpret_cast<const int32_t *>(S + in[4].off);
-    dp.cols = reinterpret_cast<const int32_t *>(S + in[5].off);
-    dp.peak_flops = hp->peak_flops ? reinterpret_cast<const double *>(S + in[6].off) : nullptr;
-    dp.efficiency = hp->efficiency ? reinterpret_cast<const double *>(S + in[7].off) : nullptr;
+    dp.algo = small + in[0].off;
+    dp.topo_kind = small + in[1].off;
+    dp.bw = reinterpret_cast<const double *>(small + in[2].off);
+    dp.latency = reinterpret_cast<const int64_t *>(small + in[3].off);
+    dp.rows = reinterpret_cast<const int32_t *>(small + in[4].off);
+    dp.cols = reinterpret_cast<const int32_t *>(small + in[5].off);
+    dp.peak_flops = hp->peak_flops ? reinterpret_cast<const double *>(small + in[6].off) : nullptr;
+    dp.efficiency = hp->efficiency ? reinterpret_cast<const double *>(small + in[7].off) : nullptr;
     fl_outputs dout{};
-    dout.status = reinterpret_cast<int32_t *>(S + o_status);
-    dout.rows = reinterpret_cast<int64_t *>(S + o_rows);
+    dout.status = reinterpret_cast<int32_t *>(small + o_status);
+    dout.rows = reinterpret_cast<int64_t *>(small + o_rows);
     dout.rank_stats = ho->rank_stats ? reinterpret_cast<int64_t *>(S + o_rs) : nullptr;
     dout.ev_start = ho->ev_start ? reinterpret_cast<int64_t *>(S + o_es) : nullptr;
     dout.ev_end = ho->ev_start ? reinterpret_cast<int64_t *>(S + o_ee) : nullptr;
     dout.link_busy = LC ? reinterpret_cast<int64_t *>(S + o_lb) : nullptr;
     dout.link_cap = (int32_t)LC;
     dout.trace = TC ? reinterpret_cast<int64_t *>(S + o_tr) : nullptr;
-    dout.trace_len = ho->trace_len ? reinterpret_cast<int32_t *>(S + o_tl) : nullptr;
+    dout.trace_len = ho->trace_len ? reinterpret_cast<int32_t *>(small + o_tl) : nullptr;
     dout.trace_cap = (int32_t)TC;
     int rc = launch(g, &dp, &dout, st);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(H + o_status, S + o_status, small_end - o_status, cudaMemcpyDeviceToHost, st));
+    if (!zc) CK(cudaMemcpyAsync(H + o_status, S + o_status, small_end - o_status, cudaMemcpyDeviceToHost, st));
     if (ho->rank_stats) CK(cudaMemcpyAsync(ho->rank_stats, dout.rank_stats, 40 * n * R, cudaMemcpyDeviceToHost, st));
     if (LC) CK(cudaMemcpyAsync(ho->link_busy, dout.link_busy, 8 * n * LC, cudaMemcpyDeviceToHost, st));
     if (TC) CK(cudaMemcpyAsync(ho->trace, dout.trace, 8 * n * TC, cudaMemcpyDeviceToHost, st));

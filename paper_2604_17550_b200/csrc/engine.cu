@@ -177,6 +177,7 @@ struct Shared {
     int cend_uniform;
     int ncomp;
     int nmcomp;
+    int pcols;                      // this design point's mesh columns
     double mbeta;                   // this design point's 1e9 / bw and latency (message wire times)
     int64_t mlat;
     // cluster variant: per-CTA partial results, written by every CTA of the cluster (DSMEM)
@@ -465,6 +466,8 @@ struct Ctx {
     int link_cap;
     int32_t *mlist;                 // [p2p_stride][R] per-rank in-flight messages (id | MSG_ALLOC), unordered
     int32_t *mlist_node;            // [p2p_stride][R] this rank's endpoint node of that message
+    int64_t *mlist_s, *mlist_e;     // [p2p_stride][R] its wire reservation (copies: the list is read per step,
+                                    // the message records are scattered over HBM)
 };
 
 // This design point's duration of node n: an LDS when the durations are in shared memory
@@ -911,8 +914,7 @@ __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, cons
         int64_t me = TINF, msn = TINF, mna = TINF;
         for (int k = 0; k < n;) {
             const int ent = c.mlist[k * R + L.r];
-            const MsgState &ms = c.msg[ent & ~MSG_ALLOC];
-            const int64_t e = ms.e, st = ms.s;
+            const int64_t e = c.mlist_e[k * R + L.r], st = c.mlist_s[k * R + L.r];
             if (e == t) {
                 const int node = c.mlist_node[k * R + L.r];
                 if (!(ent & MSG_ALLOC)) { const uint4 hb = rec_b(g, L.nb + node); F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
@@ -920,6 +922,8 @@ __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, cons
                 if (k != --n) {         // (unordered list: the last entry takes its place)
                     c.mlist[k * R + L.r] = c.mlist[n * R + L.r];
                     c.mlist_node[k * R + L.r] = c.mlist_node[n * R + L.r];
+                    c.mlist_s[k * R + L.r] = c.mlist_s[n * R + L.r];
+                    c.mlist_e[k * R + L.r] = c.mlist_e[n * R + L.r];
                 }
                 continue;
             }
@@ -956,7 +960,7 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
             for (int k = 0; k < n; k++) {
                 const int ent = c.mlist[k * R + L.r];
                 if (ent & MSG_ALLOC) continue;
-                const int64_t st = c.msg[ent].s;
+                const int64_t st = c.mlist_s[k * R + L.r];
                 if (st <= tcur) {
                     const uint4 hb = rec_b(g, L.nb + c.mlist_node[k * R + L.r]);
                     F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w);
@@ -1013,9 +1017,9 @@ template <typename F>
 __device__ __forceinline__ void for_route(const DevGraph &g, int topo, int cols, int si, int di, F &&fn) {
     if (si == di) return;
     if (topo == FL_SWITCH) { fn(2 * si); fn(2 * di + 1); return; }
-    const int64_t src = g.rank_value[si], dst = g.rank_value[di];
-    int r = (int)(src / cols), cc = (int)(src % cols);
-    const int r1 = (int)(dst / cols), c1 = (int)(dst % cols);
+    const int src = (int)g.rank_value[si], dst = (int)g.rank_value[di];   // (capi.cu: rank ids < 2^27 with messages)
+    int r = src / cols, cc = src % cols;
+    const int r1 = dst / cols, c1 = dst % cols;
     while (cc != c1) { fn(4 * (r * cols + cc) + (c1 > cc ? 0 : 1)); cc += c1 > cc ? 1 : -1; }
     while (r != r1) { fn(4 * (r * cols + cc) + (r1 > r ? 2 : 3)); r += r1 > r ? 1 : -1; }
 }
@@ -1026,8 +1030,8 @@ __device__ __forceinline__ int64_t transfer_ns(const DevGraph &g, int topo, int 
     if (si == di) return 0;
     int64_t hops = 1;
     if (topo == FL_MESH2D) {
-        const int64_t src = g.rank_value[si], dst = g.rank_value[di];
-        const int64_t dr = src / cols - dst / cols, dc = src % cols - dst % cols;
+        const int src = (int)g.rank_value[si], dst = (int)g.rank_value[di];
+        const int dr = src / cols - dst / cols, dc = src % cols - dst % cols;
         hops = (dr < 0 ? -dr : dr) + (dc < 0 ? -dc : dc);
     }
     return rhu(__dadd_rn((double)(hops * lat), __dmul_rn((double)bytes, beta)));
@@ -1063,11 +1067,69 @@ __device__ __forceinline__ int32_t *msg_count(int rr) {
     else return cg::this_cluster().map_shared_rank(&QMN<K>(rr & 1023), rr >> 10);
 }
 
+// Grant message m the links of its route (its claims hold all of them): the reservation,
+// the endpoints' critical-path values and their in-flight list entries.
+template <int K, bool CL>
+__device__ __forceinline__ void grant_msg(const DevGraph &g, const DevOut &o, const Ctx &c, int m, int si, int di,
+                                          int topo, int cols, int cfg, uint64_t epoch, int64_t lat, double beta) {
+    const int R = g.R;
+    MsgState &ms = c.msg[m];
+    int64_t st = ms.sendt > ms.recvt ? ms.sendt : ms.recvt;
+    for_route(g, topo, cols, si, di, [&](int l) { st = c.link_free[l] > st ? c.link_free[l] : st; });
+    const int64_t xf = transfer_ns(g, topo, cols, si, di, g.msg_bytes[m], lat, beta), e = st + xf;
+    for_route(g, topo, cols, si, di, [&](int l) {
+        c.link_free[l] = e;
+        const int64_t b0 = c.link_busy[l];
+        c.link_busy[l] = (b0 < 0 ? 0 : b0) + (e - st);
+    });
+    ms.s = st;
+    ms.e = e;
+    // critical path: a RECV also waits for its SEND plus the wire (simulator.py:430-435, :450-452)
+    const int64_t cs = ms.cps_s;
+    const int64_t cr = ms.cps_r > cs + xf ? ms.cps_r : cs + xf;
+    const int sn = g.msg_send_node[m], dn = g.msg_recv_node[m];
+    c.cp[sn * R + si] = (int64_t)(epoch | (uint64_t)cs);
+    c.cp[dn * R + di] = (int64_t)(epoch | (uint64_t)cr);
+    record(g, o, cfg, si, sn, st, e);
+    record(g, o, cfg, di, dn, st, e);
+    for (int side = 0; side < 2; side++) {     // both endpoints' in-flight lists and summaries
+        const int rr = side ? di : si;
+        const int k2 = atomicAdd(msg_count<K, CL>(rr), 1);
+        c.mlist[k2 * R + rr] = m;
+        c.mlist_node[k2 * R + rr] = side ? dn : sn;
+        c.mlist_s[k2 * R + rr] = st;
+        c.mlist_e[k2 * R + rr] = e;
+        atomicMin(reinterpret_cast<long long *>(msg_field<K, CL>(MF_E, rr)), (long long)e);
+        atomicMin(reinterpret_cast<long long *>(msg_field<K, CL>(MF_S, rr)), (long long)st);
+        atomicMin(reinterpret_cast<long long *>(msg_field<K, CL>(MF_NA, rr)), (long long)st);
+    }
+}
+
 template <int K, bool CL>
 static __device__ void reserve_msgs(const DevGraph &g, const DevOut &o, const Ctx &c, int nm, bool init, int topo,
                                     int cols, int cfg, uint64_t epoch, int64_t lat, double beta) {
-    const int R = g.R, tid = threadIdx.x, bd = blockDim.x;
+    const int tid = threadIdx.x, bd = blockDim.x;
     unsigned long long *own = c.link_owner;           // KINF between phases
+    if (nm <= bd) {
+        // the common case, at most one message per thread: its identity stays in registers
+        const int m = tid < nm ? c.mcomplist[tid] : -1;
+        unsigned long long k = 0;
+        int si = 0, di = 0;
+        if (m >= 0) { k = msg_key(g, c, m, init); si = g.msg_send_rank[m]; di = g.msg_recv_rank[m]; }
+        bool pending = m >= 0;
+        for (;;) {
+            if (pending) for_route(g, topo, cols, si, di, [&](int l) { atomicMin(&own[l], k); });     // claim
+            if (!__syncthreads_or(pending)) break;
+            bool mine = pending;
+            if (pending) for_route(g, topo, cols, si, di, [&](int l) { mine &= *(volatile unsigned long long *)&own[l] == k; });
+            if (mine) grant_msg<K, CL>(g, o, c, m, si, di, topo, cols, cfg, epoch, lat, beta);
+            __syncthreads();
+            if (pending) for_route(g, topo, cols, si, di, [&](int l) { own[l] = KINF; });            // release
+            pending &= !mine;
+            __syncthreads();
+        }
+        return;
+    }
     for (;;) {
         int left = 0;
         for (int q = tid; q < nm; q += bd) {           // claim
@@ -1086,34 +1148,7 @@ static __device__ void reserve_msgs(const DevGraph &g, const DevOut &o, const Ct
             bool mine = true;
             for_route(g, topo, cols, si, di, [&](int l) { mine &= *(volatile unsigned long long *)&own[l] == k; });
             if (!mine) continue;
-            MsgState &ms = c.msg[m];
-            int64_t st = ms.sendt > ms.recvt ? ms.sendt : ms.recvt;
-            for_route(g, topo, cols, si, di, [&](int l) { st = c.link_free[l] > st ? c.link_free[l] : st; });
-            const int64_t xf = transfer_ns(g, topo, cols, si, di, g.msg_bytes[m], lat, beta), e = st + xf;
-            for_route(g, topo, cols, si, di, [&](int l) {
-                c.link_free[l] = e;
-                const int64_t b0 = c.link_busy[l];
-                c.link_busy[l] = (b0 < 0 ? 0 : b0) + (e - st);
-            });
-            ms.s = st;
-            ms.e = e;
-            // critical path: a RECV also waits for its SEND plus the wire (simulator.py:430-435, :450-452)
-            const int64_t cs = ms.cps_s;
-            const int64_t cr = ms.cps_r > cs + xf ? ms.cps_r : cs + xf;
-            const int sn = g.msg_send_node[m], dn = g.msg_recv_node[m];
-            c.cp[sn * R + si] = (int64_t)(epoch | (uint64_t)cs);
-            c.cp[dn * R + di] = (int64_t)(epoch | (uint64_t)cr);
-            record(g, o, cfg, si, sn, st, e);
-            record(g, o, cfg, di, dn, st, e);
-            for (int side = 0; side < 2; side++) {     // both endpoints' in-flight lists and summaries
-                const int rr = side ? di : si;
-                const int k2 = atomicAdd(msg_count<K, CL>(rr), 1);
-                c.mlist[k2 * R + rr] = m;
-                c.mlist_node[k2 * R + rr] = side ? dn : sn;
-                atomicMin(reinterpret_cast<long long *>(msg_field<K, CL>(MF_E, rr)), (long long)e);
-                atomicMin(reinterpret_cast<long long *>(msg_field<K, CL>(MF_S, rr)), (long long)st);
-                atomicMin(reinterpret_cast<long long *>(msg_field<K, CL>(MF_NA, rr)), (long long)st);
-            }
+            grant_msg<K, CL>(g, o, c, m, si, di, topo, cols, cfg, epoch, lat, beta);
             c.mcomplist[q] = m | MQ_DONE;
         }
         __syncthreads();
@@ -1393,6 +1428,8 @@ __global__ void __launch_bounds__(1024, 1)
         c.mcomplist = reinterpret_cast<int32_t *>(c.msg + M);
         c.mlist = c.mcomplist + M;
         c.mlist_node = c.mlist + (size_t)g.p2p_stride * R;
+        c.mlist_s = reinterpret_cast<int64_t *>(base + sc.off_mlist_se);
+        c.mlist_e = c.mlist_s + (size_t)g.p2p_stride * R;
     }
     __syncthreads();
     const bool is_leader = crank == 0 && tid == 0;      // writes the point's row
@@ -1439,12 +1476,15 @@ __global__ void __launch_bounds__(1024, 1)
 
     for (int cfg = cid; cfg < p.n; cfg += ncl) {
         // ---- cost stage (K1): this point's durations ----
+        // (each design-point column is read once: fl_sweep_run may pass them in mapped host memory)
         const int algo = p.algo[cfg], topo = p.topo_kind[cfg];
         const double bwv = p.bw[cfg];
         const int64_t lat = p.latency[cfg];
+        const int prows = p.rows[cfg], pcols = p.cols[cfg];
+        if (tid == 0) sh.pcols = pcols;
         int bad = 0, zero = 0, cap_bad = 0;
         for (int i = gt; i < NI; i += gstride) {
-            int64_t d = coll_time(g, i, algo, topo, bwv, lat, p.rows[cfg], p.cols[cfg]);
+            int64_t d = coll_time(g, i, algo, topo, bwv, lat, prows, pcols);
             if (d < 0) { bad = 1; d = 0; }
             zero |= d == 0;
             c.inst_dur[i] = d;
@@ -1456,8 +1496,8 @@ __global__ void __launch_bounds__(1024, 1)
         if (CL) for (int i = tid; i < NI; i += bd) { c.inst_s[i] = 0; c.inst_e[i] = 0; }   // (per-CTA copies)
         if (K & 8) {                // messages: fresh message and link state
             const double beta = __ddiv_rn(1e9, bwv);
-            const int cols = p.cols[cfg];
-            if (topo == FL_MESH2D && (cols <= 0 || 4LL * p.rows[cfg] * cols > c.link_cap)) cap_bad = 1;
+            const int cols = pcols;
+            if (topo == FL_MESH2D && (cols <= 0 || 4LL * prows * cols > c.link_cap)) cap_bad = 1;
             // a zero wire time would put events at the reservation's own time (serial mode); the
             // smallest possible one is one hop of the smallest message (transfer_ns is monotone)
             if (g.msg_self || (g.n_msg > 0 && rhu(__dadd_rn((double)lat, __dmul_rn((double)g.msg_min_bytes, beta))) == 0))
@@ -1481,7 +1521,7 @@ __global__ void __launch_bounds__(1024, 1)
         int zdur = same_dev ? dev_zdur : 0;   // a zero-duration COMP or non-static HOST could complete at t = 0
         if (!same_dev) for (int n = tid; n < g.total_nodes; n += bd) {
             int64_t d = g.node_dur[n];
-            if (recost && g.node_flops[n] >= 0) d = flops_to_ns(g.node_flops[n], p.peak_flops[cfg], p.efficiency[cfg]);
+            if (recost && g.node_flops[n] >= 0) d = flops_to_ns(g.node_flops[n], pk, ef);
             c.dur[n] = d;
             if (d == 0) {
                 const uint4 nb_ = rec_b(g, n);
@@ -1565,7 +1605,7 @@ __global__ void __launch_bounds__(1024, 1)
         }
         // (reservations also return their instances' critical-path finishes; every member's
         // pop folds the same value into F_CPMAX, so the row needs only that)
-        reserve<MSG, CL, KK>(g, o, c, sh, par, 0, true, cfg, f.epoch, topo, p.cols[cfg]);
+        reserve<MSG, CL, KK>(g, o, c, sh, par, 0, true, cfg, f.epoch, topo, sh.pcols);
         if (active) refresh_ring(c, L, s);
         f.init = 0;
         if (f.fold) {
@@ -1600,7 +1640,7 @@ __global__ void __launch_bounds__(1024, 1)
                     for (int q = g.static_off[st]; q < g.static_off[st + 1]; q++)
                         record(g, o, cfg, L.r, g.static_list[q], 0, 0);
             }
-            reserve<MSG, CL, KK>(g, o, c, sh, par, 0, false, cfg, f.epoch, topo, p.cols[cfg]);
+            reserve<MSG, CL, KK>(g, o, c, sh, par, 0, false, cfg, f.epoch, topo, sh.pcols);
             if (active) refresh_ring(c, L, s);
         }
         int64_t tcur = 0;
@@ -1628,7 +1668,7 @@ __global__ void __launch_bounds__(1024, 1)
             if (nc | nmc) {
                 if (CL && tid == 0) sh.fifo_empty = s.head_e == TINF;   // (identical for every rank when uniform)
                 const int64_t ef = reserve_n<MSG, CL, K>(g, o, c, sh, par, tcur, false, cfg, f.epoch, nc, nmc,
-                                                         topo, p.cols[cfg]);
+                                                         topo, sh.pcols);
                 if (active) refresh_ring(c, L, s);
                 if (CL && ef >= 0) {       // (clusters only: on one CTA the A/B showed no gain)
                     // every rank's next event only gained the same new FIFO head (if its FIFO was
@@ -1688,7 +1728,7 @@ __global__ void __launch_bounds__(1024, 1)
                     }
                     if (active) start_phase(g, o, c, L, s, f, t, cfg);
                     reserve<MSG, CL, KK>(g, o, c, sh, par, t, false, cfg, f.epoch, topo,
-                                                       p.cols[cfg]);
+                                                       sh.pcols);
                             if (active) {
                         refresh_ring(c, L, s);
                         gather_due(g, c, L, s, t);

@@ -73,6 +73,7 @@ struct DevScratch {
     size_t off_acc;              // [n_acc][R] int64: accumulators of statically ordered nodes, by slot
     // dynamic shared-memory layout (bytes from the start of the CTA's smem)
     size_t off_msg;              // message state, per-rank in-flight lists
+    size_t off_mlist_se;         // [2][p2p_stride][R] int64: in-flight entries' wire start / end
     size_t off_links;            // link state [3][link_cap]: free-at, busy, message-phase claim (last in the slot: grows per launch)
     size_t off_ctr;              // cluster-wide completion counters
     size_t off_inst_se;          // clusters: per-CTA copies of the instances' reservation start / end

@@ -131,6 +131,17 @@ class DesignPoints:
             pts.efficiency = np.asarray([d.efficiency for d in devices], np.float64)
         return pts
 
+    def raw(self):
+        """The fl_points struct of these columns (validated; rebuilt only when a column object or
+        the stream count changed -- in-place edits of the arrays need no rebuild)."""
+        key = (self.compute_streams, *(id(getattr(self, f)) for f, _ in _POINT_COLS))
+        cached = self.__dict__.get("_raw")
+        if cached is None or cached[0] != key:
+            n = len(self)
+            st = _native.PointsRaw(n, *(_addr(getattr(self, f), t, n, f) for f, t in _POINT_COLS), self.compute_streams)
+            self.__dict__["_raw"] = cached = (key, st, [getattr(self, f) for f, _ in _POINT_COLS])
+        return cached[1]
+
     def slice(self, a: int, b: int) -> "DesignPoints":
         f = lambda x: None if x is None else np.ascontiguousarray(x[a:b])
         return DesignPoints(f(self.algo), f(self.topo_kind), f(self.bw), f(self.latency), f(self.rows),
@@ -144,6 +155,20 @@ class DesignPoints:
 
 def _ptr(a, typ):
     return None if a is None else a.ctypes.data_as(typ)
+
+
+_POINT_COLS = (("algo", np.uint8), ("topo_kind", np.uint8), ("bw", np.float64), ("latency", np.int64),
+               ("rows", np.int32), ("cols", np.int32), ("peak_flops", np.float64), ("efficiency", np.float64))
+
+
+def _addr(a, dtype=None, n=None, name=""):
+    """Raw address of a C-contiguous array for the ABI structs (None -> NULL); with `dtype`, the
+    design-point column must have that dtype and n entries (the engine reads it as such)."""
+    if a is None:
+        return None
+    if dtype is not None and (a.dtype != dtype or len(a) != n or not a.flags.c_contiguous):
+        raise EngineError(f"DesignPoints.{name} must be a contiguous {np.dtype(dtype).name} array of {n} entries")
+    return a.ctypes.data
 
 
 # ------------------------------------------------------------ engine handle
@@ -206,7 +231,7 @@ class Engine:
         entries (rank index << 32 | local node index) from the sink back to the source."""
         n = len(pts)
         R = self.gs.n_ranks
-        out = {"status": np.zeros(n, np.int32), "rows": np.zeros((n, 6), np.int64)}
+        out = {"status": np.empty(n, np.int32), "rows": np.empty((n, 6), np.int64)}
         cap = self.link_cap(pts) if links else 0
         if links:
             out["link_busy"] = np.full((n, max(cap, 1)), -1, np.int64)
@@ -215,20 +240,14 @@ class Engine:
         if events:
             out["ev_start"] = np.zeros((n, R, self.max_nodes), np.int64)
             out["ev_end"] = np.zeros((n, R, self.max_nodes), np.int64)
-        p = _native.Points(n, _ptr(pts.algo, _native.PU8), _ptr(pts.topo_kind, _native.PU8),
-                           _ptr(pts.bw, _native.PF64), _ptr(pts.latency, _native.P64),
-                           _ptr(pts.rows, _native.P32), _ptr(pts.cols, _native.P32),
-                           _ptr(pts.peak_flops, _native.PF64), _ptr(pts.efficiency, _native.PF64),
-                           pts.compute_streams)
         if trace_cap > 0:
             out["trace"] = np.zeros((n, trace_cap), np.int64)
             out["trace_len"] = np.zeros(n, np.int32)
-        o = _native.Outputs(_ptr(out["status"], _native.P32), _ptr(out["rows"], _native.P64),
-                            _ptr(out.get("rank_stats"), _native.P64), _ptr(out.get("ev_start"), _native.P64),
-                            _ptr(out.get("ev_end"), _native.P64), _ptr(out.get("link_busy"), _native.P64), cap,
-                            _ptr(out.get("trace"), _native.P64), _ptr(out.get("trace_len"), _native.P32),
-                            int(trace_cap))
-        rc = _native.lib().fl_sweep_run(self._h, C.byref(p), C.byref(o))
+        p = pts.raw()
+        o = _native.OutputsRaw(out["status"].ctypes.data, out["rows"].ctypes.data, _addr(out.get("rank_stats")),
+                               _addr(out.get("ev_start")), _addr(out.get("ev_end")), _addr(out.get("link_busy")), cap,
+                               _addr(out.get("trace")), _addr(out.get("trace_len")), int(trace_cap))
+        rc = _native.lib().fl_sweep_run(self._h, C.addressof(p), C.addressof(o))
         if rc:
             raise EngineError(f"fl_sweep_run: {_native.last_error()} (status {rc})")
         return out

@@ -204,6 +204,22 @@ class GraphSet:
         return int(sum(self.structs[s].n for s in self.rank_struct))
 
 
+def _zip_is_natural(structs, rank_struct, rank_values, rindex, group, members) -> bool:
+    """zip(group, members) pairs rank group[q] with members[q] (members = [lead] + the others in
+    group order).  It equals the natural pairing (each rank with its own collective) when every
+    members[q] has the node_id of rank group[q]'s own member and the union of the members'
+    dependencies, taken at the zipped ranks, is the natural one (critical_path's join,
+    simulator.py:419-428)."""
+    own = {r: node for r, node in members}
+    node = lambda r, n: structs[rank_struct[r]].nodes[n]
+    zr = [rindex[v] for v in group]
+    if any(node(r, own[r]).node_id != node(mr, mn).node_id for r, (mr, mn) in zip(zr, members)):
+        return False
+    nat = {(int(rank_values[mr]), d) for mr, mn in members for d in node(mr, mn).dep_ids()}
+    zipped = {(int(rank_values[r]), d) for r, (mr, mn) in zip(zr, members) for d in node(mr, mn).dep_ids()}
+    return nat == zipped
+
+
 def _match_instances(gs: "GraphSet", graphs, rank_values, rank_struct, structs):
     """collective_instances (collectives.py:419-453) over compiled structures."""
     R = len(rank_values)
@@ -255,10 +271,16 @@ def _match_instances(gs: "GraphSet", graphs, rank_values, rank_struct, structs):
             if ok != k0 or og != group or ob != nbytes:
                 raise InconsistentGroupsError(f"rank {v} node {oid} disagrees with rank {rank_values[start]} node {lid}")
             members.append((r, onode))
-        if len(members) != len(group) or rindex.get(group[0]) != start:
-            # the reference pairs zip(group, members): only well-formed when the
-            # lead rank is listed first (ascending groups, as every producer emits)
-            raise InconsistentGroupsError(f"collective group {group} must list its lowest rank first")
+        if len(members) != len(group):
+            raise InconsistentGroupsError(f"collective group {group} lists a rank twice")
+        if rindex.get(group[0]) != start and not _zip_is_natural(structs, rank_struct, rank_values, rindex, group,
+                                                                   members):
+            # the reference pairs zip(group, members) (simulator.py:222-223, :419-425): with the
+            # lead listed first that is each rank with its own node; otherwise it is only the same
+            # pairing when node ids and the zipped dependency union agree (else the reference
+            # fails with a KeyError in simulate or a spurious cycle in critical_path)
+            raise InconsistentGroupsError(f"collective group {group} pairs ranks with other ranks' nodes "
+                                          f"(zip(group, members), simulator.py:222-223)")
         i = len(kinds)
         kinds.append(k0); ns.append(len(group)); byts.append(nbytes); lead.append(lid)
         key = 0

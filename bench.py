@@ -54,16 +54,55 @@ def log(*a):
 
 
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and throttle reasons sampled DURING the timed region (B200_PROFILING.md
+    clocks line).  NVML in a thread every millisecond, so even a C2 run whose timed region
+    is a few milliseconds gets samples; nvidia-smi -lms 50 when NVML is unavailable."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4))
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_s: float = 0.001):
         self.index = index
+        self.period = period_s
         self.proc = None
+        self.nvml = None
+        self.samples = []           # (sm_mhz, max_mhz, reason bits)
+        self.out = ""
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:                        # NVML ignores CUDA_VISIBLE_DEVICES: find the device by PCI address
+            import torch
+            p = torch.cuda.get_device_properties(self.index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _sample(self):
+        nv, h = self.nvml
+        self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                             nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM),
+                             nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+
+    def _loop(self):
+        while not self.stop.wait(self.period):
+            self._sample()
 
     def __enter__(self):
+        import threading
+        try:
+            self.nvml = self._nvml_handle()
+            self._sample()
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._loop, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
@@ -73,6 +112,10 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
+        if self.nvml:
+            self.stop.set()
+            self.thread.join()
+            self._sample()
         if self.proc:
             self.proc.terminate()
             try:
@@ -83,24 +126,29 @@ class ClockSampler:
         return False
 
     def summary(self):
-        if not self.proc or not getattr(self, "out", ""):
-            return None
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for row in csv.reader(io.StringIO(self.out)):
-            if len(row) < 9:
-                continue
-            try:
-                sm.append(float(row[1])); mx = max(mx, float(row[2]))
-            except ValueError:
-                continue
-            for name, v in zip(names, row[5:9]):
-                if v.strip().lower() == "active":
-                    reasons.add(name)
+        if self.samples:
+            for clk, m, bits in self.samples:
+                sm.append(float(clk)); mx = max(mx, float(m))
+                reasons.update(name for name, b in self.REASONS if bits & b)
+            src = "nvml"
+        else:
+            names = [n for n, _ in self.REASONS]
+            for row in csv.reader(io.StringIO(self.out)):
+                if len(row) < 9:
+                    continue
+                try:
+                    sm.append(float(row[1])); mx = max(mx, float(row[2]))
+                except ValueError:
+                    continue
+                for name, v in zip(names, row[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(name)
+            src = "nvidia-smi"
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": src}
 
 
 # ------------------------------------------------------------ workload

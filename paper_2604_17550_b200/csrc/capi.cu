@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -456,13 +457,31 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     }
 
     // launch geometry: one thread per rank; a design point runs on one CTA, or on a
-    // cluster of CTAs (1024 ranks each) when it has more ranks than a CTA has threads
-    g->cluster = (R + 1023) / 1024;
-    g->block = g->cluster > 1 ? 1024 : (R + 31) / 32 * 32;
-    const int CS = g->cluster;
+    // cluster of CS CTAs of ceil(R / CS) ranks each when it has more ranks than a CTA has
+    // threads.  The kernel is issue-bound with one CTA per SM, so a point's time scales with
+    // the ranks per CTA, and clusters must fit inside a GPC: CS is the size that maximizes
+    // (co-resident clusters) / (ranks per CTA) -- on B200 a 9-CTA cluster of 911 ranks
+    // leaves fewer SMs idle than 8 CTAs of 1024 (FL_CLUSTER_CTAS forces a size, for A/B).
     int sms = 0, optin = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    const int cs_min = (R + 1023) / 1024;
+    int cs_lo = cs_min, cs_hi = cs_min > 1 ? 16 : 1;
+    if (cs_min > 1) {
+        if (const char *ev = getenv("FL_CLUSTER_CTAS")) {
+            const int f = atoi(ev);
+            if (f >= cs_min && f <= 16) cs_lo = cs_hi = f;
+        }
+    }
+    int best_cs = -1;
+    double best_score = -1.0;
+    for (int pass = 0; pass < 2; pass++) {
+    for (int CS = cs_lo; CS <= cs_hi; CS++) {
+    if (pass == 1 && CS != best_cs) continue;
+    const int per = (R + CS - 1) / CS;
+    g->cluster = CS;
+    g->block = (per + 31) / 32 * 32;
+    if (CS > 1 && (CS - 1) * g->block >= R) continue;     // the last CTA would own no rank
 
     // per-CTA scratch (global) layout
     fl::DevScratch &sc = g->sc;
@@ -534,7 +553,11 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
         sm = align_up(sm + (size_t)sc.link_cap * 24, 16);
         g->links_sm_cap = sc.link_cap;
     }
-    if (sm > budget) return fail(FL_ERR_CAPACITY, "per-rank state exceeds shared memory");
+    if (sm > budget) {
+        if (pass == 0 && CS < cs_hi) continue;
+        if (pass == 0 && best_cs > 0) continue;
+        return fail(FL_ERR_CAPACITY, "per-rank state exceeds shared memory");
+    }
     g->smem = sm;
     {
         // the kernels' dynamic shared-memory limit is per function and device, shared by every
@@ -550,10 +573,19 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
         }
     }
     int occ = 0;
-    CK(fl::sweep_occupancy(g->block, g->smem, CS, &occ));
+    if (fl::sweep_occupancy(g->block, g->smem, CS, &occ) != cudaSuccess) { cudaGetLastError(); occ = 0; }
+    if (pass == 0) {
+        const double score = (double)occ / g->block;
+        if (occ >= 1 && score > best_score * 1.0001) { best_score = score; best_cs = CS; }
+        continue;
+    }
     if (occ < 1) return fail(FL_ERR_CAPACITY, "engine kernel cannot be resident with this shared-memory footprint");
     g->grid_cap = CS > 1 ? occ : sms * occ;           // concurrent design points (clusters or CTAs)
     return FL_OK;
+    }   // CS
+    if (best_cs < 0) return fail(FL_ERR_CAPACITY, "engine kernel cannot be resident with this shared-memory footprint");
+    }   // pass
+    return fail(FL_ERR_INVALID, "launch geometry");
 }
 
 // A launch whose mesh points need more links than the slot holds grows the table (the

@@ -447,9 +447,13 @@ struct Ctx {
     int base;                       // first rank owned by this CTA (clusters of CTAs share a design point)
     int BR, DR;                     // strides of the touched / done bitmaps (RL in shared memory, else R)
     bool lead_cta;                  // the cluster's first CTA (its thread 0 does the serial work)
+    // [w][R] arrays are addressed [w * R + L.lr]: a cluster CTA's pointers below are offset by
+    // its first rank (c.base), so only the *_g views index another CTA's columns by global rank
+    // (and the cluster variant keeps no base + tid register: the compiler re-derived it ~70 times)
     uint64_t *done, *rdyc, *rdyh, *due;
     uint64_t *touched;              // [word][rank]: accumulator written in this design point
     int64_t *cp;                    // [max_nodes][R]: counted accumulators, parked set members
+    int64_t *cp_g;                  // the same, not offset (message grants, trace walk)
     int64_t *acc;                   // [n_acc][R]: accumulators of statically ordered nodes, by slot
     int32_t *ring_inst, *ring_node; // [coll_stride][R] per-rank comm FIFO
     int64_t *dur;                   // [total_nodes] this design point's durations
@@ -468,6 +472,8 @@ struct Ctx {
     int32_t *mlist_node;            // [p2p_stride][R] this rank's endpoint node of that message
     int64_t *mlist_s, *mlist_e;     // [p2p_stride][R] its wire reservation (copies: the list is read per step,
                                     // the message records are scattered over HBM)
+    int32_t *mlist_g, *mlist_node_g;   // the in-flight lists, not offset (message grants)
+    int64_t *mlist_s_g, *mlist_e_g;
 };
 
 // This design point's duration of node n: an LDS when the durations are in shared memory
@@ -482,7 +488,8 @@ constexpr int32_t MSG_ALLOC = 1 << 30;   // mlist entry flag: the endpoint's out
 struct Lane {
     int r, nb, tb;
     int lr;                         // this thread's lane of the shared per-rank fields (threadIdx.x)
-    int br, dr;                     // rank index for the touched / done bitmaps (lr in shared memory, else r)
+    int br, dr;                     // column of the touched / done bitmaps (lr: shared memory, or HBM
+                                    // through the offset pointers)
 };
 
 // Per-rank indices and strides.  Bit 16 of K marks the cluster variant, whose
@@ -492,11 +499,11 @@ struct Lane {
 // re-read after every shared store would cost an LDS per access).
 template <int K> __device__ __forceinline__ uint64_t &done_ref(const Ctx &c, const Lane &L, int R, int w) {
     if constexpr ((K & 16) != 0) return c.done[w * c.DR + L.dr];
-    else return c.done[w * R + L.r];
+    else return c.done[w * R + L.lr];
 }
 template <int K> __device__ __forceinline__ uint64_t &touch_ref(const Ctx &c, const Lane &L, int R, int w) {
     if constexpr ((K & 16) != 0) return c.touched[w * c.BR + L.br];
-    else return c.touched[w * R + L.r];
+    else return c.touched[w * R + L.lr];
 }
 
 // A node set with its minimum cached in a register and the rest in a global
@@ -565,13 +572,13 @@ __device__ __forceinline__ void ms_insert_cp(MinSet &m, uint64_t *b, int64_t *cp
         F64<K>(F, L.lr) = v;
     } else if (idx < ms_min(m)) {
         const int h = ms_min(m);
-        cp[h * R + L.r] = F64<K>(F, L.lr);
-        bm_set(b, R, L.r, h);
+        cp[h * R + L.lr] = F64<K>(F, L.lr);
+        bm_set(b, R, L.lr, h);
         m.head = idx | ms_inc(ms_cnt(m));
         F64<K>(F, L.lr) = v;
     } else {
-        cp[idx * R + L.r] = v;
-        bm_set(b, R, L.r, idx);
+        cp[idx * R + L.lr] = v;
+        bm_set(b, R, L.lr, idx);
         m.head = ms_min(m) | ms_inc(ms_cnt(m));
     }
 }
@@ -583,10 +590,10 @@ __device__ __forceinline__ int ms_pop_cp(MinSet &m, uint64_t *b, const int64_t *
     v = F64<K>(F, L.lr);
     const int n = ms_cnt(m);
     if (n) {
-        const int h = bm_pop(b, R, L.r, x, nwords);
+        const int h = bm_pop(b, R, L.lr, x, nwords);
         if (h >= 0) {
             m.head = h | ((n - (n < MS_SAT)) << 17);
-            F64<K>(F, L.lr) = cp[h * R + L.r] & (int64_t)VAL48;
+            F64<K>(F, L.lr) = cp[h * R + L.lr] & (int64_t)VAL48;
         } else {
             m.head = -1;
         }
@@ -659,7 +666,7 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
                     s.occ_e[q] = e;
                     s.occ_n[q] = x;
                     if (q == 0) F64<K>(F_OCC_CP, L.lr) = v;
-                    else c.cp[x * R + L.r] = v;      // streams 1..3: the running node's own accumulator word
+                    else c.cp[x * R + L.lr] = v;     // streams 1..3: the running node's own accumulator word
                 }
             }
         }
@@ -760,14 +767,14 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
     const uint64_t fx = (uint64_t)fx64;     // this node's critical-path finish
     // trace: the node's own word is dead once it is popped (its accumulator and its parking
     // as a set member are behind it), so it keeps the finish for the walk-back
-    if (f.trace) c.cp[x * R + L.r] = (int64_t)(f.epoch | fx);
+    if (f.trace) c.cp[x * R + L.lr] = (int64_t)(f.epoch | fx);
     int seq = 0;
     const int32_t *sl = g.succ_ent;
     // the first "last" edge's accumulator read goes out before the other edges are processed
     const uint32_t lo = xa.y >> 24;
     const uint32_t qlast = lo && f.fold ? xa.x + lo - 1 : 0xffffffffu;
     uint64_t alast = 0;
-    if (qlast != 0xffffffffu) alast = acc_read(c, f, (int)((uint32_t)sl[qlast] >> 19) * R + L.r);
+    if (qlast != 0xffffffffu) alast = acc_read(c, f, (int)((uint32_t)sl[qlast] >> 19) * R + L.lr);
     for (uint32_t q = xa.x, qe = xa.x + (xa.y & 0xfffu); q < qe; q++, seq++) {
         const uint32_t ent = (uint32_t)sl[q];
         const int d = (int)(ent & 0xffffu);
@@ -777,16 +784,16 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
         // disjoint accumulator lifetimes share (capi.cu "Accumulator slots"), so it stays in
         // L2.  A node that waits on a missing one is never dispatched.
         if (cls == FL_EDGE_FIRST) {
-            c.acc[(int)(ent >> 19) * R + L.r] = (int64_t)(f.epoch | fx);
+            c.acc[(int)(ent >> 19) * R + L.lr] = (int64_t)(f.epoch | fx);
             continue;
         }
         if (cls == FL_EDGE_MID) {
-            int64_t *const w = c.acc + ((int)(ent >> 19) * R + L.r);
+            int64_t *const w = c.acc + ((int)(ent >> 19) * R + L.lr);
             if (f.acc_sm) { if ((int64_t)(f.epoch | fx) > *w) *w = (int64_t)(f.epoch | fx); }   // (own column)
             else atomicMax(reinterpret_cast<unsigned long long *>(w), (unsigned long long)(f.epoch | fx));
             continue;
         }
-        int64_t *slot = c.cp + (d * R + L.r);
+        int64_t *slot = c.cp + (d * R + L.lr);
         const uint4 db = rec_b(g, L.nb + d);
         if (rec_never(db)) continue;
         if (cls == FL_EDGE_SINGLE) {
@@ -795,7 +802,7 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
         }
         if (cls == FL_EDGE_LAST) {
             PROF_MARK(10);                  // edges before a "last" one
-            const uint64_t a = (q == qlast ? alast : acc_read(c, f, (int)(ent >> 19) * R + L.r)) & VAL48;
+            const uint64_t a = (q == qlast ? alast : acc_read(c, f, (int)(ent >> 19) * R + L.lr)) & VAL48;
             dispatch(g, c, L, s, f, d, db, (int64_t)(a > fx ? a : fx), seq, t);
             PROF_MARK(11);                  // "last" edge: accumulator read + dispatch
             continue;
@@ -829,8 +836,8 @@ template <int K>
 __device__ __forceinline__ void load_head(const Ctx &c, const Lane &L, Rank<K> &s, int R) {
     const int h = F32<K>(Q_RING_HEAD, L.lr);
     if (h < F32<K>(Q_RING_SEEN, L.lr)) {
-        const int i = c.ring_inst[h * R + L.r];
-        F32<K>(Q_HEAD_NODE, L.lr) = c.ring_node[h * R + L.r];
+        const int i = c.ring_inst[h * R + L.lr];
+        F32<K>(Q_HEAD_NODE, L.lr) = c.ring_node[h * R + L.lr];
         F32<K>(Q_HEAD_INST, L.lr) = i;
         s.head_s = c.inst_s[i];
         s.head_e = c.inst_e[i];
@@ -839,17 +846,17 @@ __device__ __forceinline__ void load_head(const Ctx &c, const Lane &L, Rank<K> &
     }
 }
 
-// Append to lane lm's comm FIFO (rank m).  An entry appended to an empty FIFO is the
-// head: it goes straight to the head fields in shared memory, the rest to HBM.
+// Append to lane lm's comm FIFO.  An entry appended to an empty FIFO is the head: it goes
+// straight to the head fields in shared memory, the rest to HBM.
 template <int K>
-__device__ __forceinline__ void append_ring(const Ctx &c, int lm, int m, int R, int inst, int node) {
+__device__ __forceinline__ void append_ring(const Ctx &c, int lm, int R, int inst, int node) {
     const int slot = F32<K>(Q_RING_TAIL, lm)++;
     if (slot == F32<K>(Q_RING_HEAD, lm)) {
         F32<K>(Q_HEAD_NODE, lm) = node;
         F32<K>(Q_HEAD_INST, lm) = inst;
     } else {
-        c.ring_inst[slot * R + m] = inst;
-        c.ring_node[slot * R + m] = node;
+        c.ring_inst[slot * R + lm] = inst;
+        c.ring_node[slot * R + lm] = node;
     }
 }
 
@@ -895,7 +902,7 @@ __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, cons
 #pragma unroll
     for (int q = 0; q < (K & 7); q++)
         if (s.occ_n[q] >= 0 && s.occ_e[q] == t) {
-            const int64_t v = q == 0 ? F64<K>(F_OCC_CP, L.lr) : c.cp[s.occ_n[q] * R + L.r];
+            const int64_t v = q == 0 ? F64<K>(F_OCC_CP, L.lr) : c.cp[s.occ_n[q] * R + L.lr];
             ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, s.occ_n[q], v);
             s.occ_n[q] = -1;
             if ((K & 7) == 1) F64<K>(F_OVL, L.lr) += s.commcum - F64<K>(F_COMP_A, L.lr);   // comm time under [start, t)
@@ -913,17 +920,17 @@ __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, cons
         int n = QMN<K>(L.lr);
         int64_t me = TINF, msn = TINF, mna = TINF;
         for (int k = 0; k < n;) {
-            const int ent = c.mlist[k * R + L.r];
-            const int64_t e = c.mlist_e[k * R + L.r], st = c.mlist_s[k * R + L.r];
+            const int ent = c.mlist[k * R + L.lr];
+            const int64_t e = c.mlist_e[k * R + L.lr], st = c.mlist_s[k * R + L.lr];
             if (e == t) {
-                const int node = c.mlist_node[k * R + L.r];
+                const int node = c.mlist_node[k * R + L.lr];
                 if (!(ent & MSG_ALLOC)) { const uint4 hb = rec_b(g, L.nb + node); F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
-                ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, node, c.cp[node * R + L.r] & (int64_t)VAL48);
+                ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, node, c.cp[node * R + L.lr] & (int64_t)VAL48);
                 if (k != --n) {         // (unordered list: the last entry takes its place)
-                    c.mlist[k * R + L.r] = c.mlist[n * R + L.r];
-                    c.mlist_node[k * R + L.r] = c.mlist_node[n * R + L.r];
-                    c.mlist_s[k * R + L.r] = c.mlist_s[n * R + L.r];
-                    c.mlist_e[k * R + L.r] = c.mlist_e[n * R + L.r];
+                    c.mlist[k * R + L.lr] = c.mlist[n * R + L.lr];
+                    c.mlist_node[k * R + L.lr] = c.mlist_node[n * R + L.lr];
+                    c.mlist_s[k * R + L.lr] = c.mlist_s[n * R + L.lr];
+                    c.mlist_e[k * R + L.lr] = c.mlist_e[n * R + L.lr];
                 }
                 continue;
             }
@@ -958,13 +965,13 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
             const int n = QMN<K>(L.lr);
             int64_t mna = TINF;
             for (int k = 0; k < n; k++) {
-                const int ent = c.mlist[k * R + L.r];
+                const int ent = c.mlist[k * R + L.lr];
                 if (ent & MSG_ALLOC) continue;
-                const int64_t st = c.mlist_s[k * R + L.r];
+                const int64_t st = c.mlist_s[k * R + L.lr];
                 if (st <= tcur) {
-                    const uint4 hb = rec_b(g, L.nb + c.mlist_node[k * R + L.r]);
+                    const uint4 hb = rec_b(g, L.nb + c.mlist_node[k * R + L.lr]);
                     F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w);
-                    c.mlist[k * R + L.r] = ent | MSG_ALLOC;
+                    c.mlist[k * R + L.lr] = ent | MSG_ALLOC;
                 } else {
                     mna = st < mna ? st : mna;
                 }
@@ -1055,16 +1062,16 @@ __device__ __forceinline__ unsigned long long msg_key(const DevGraph &g, const C
 }
 
 // Rank rr's in-flight summary field (or list length): this CTA's shared memory, or in a
-// cluster the owning CTA's, through distributed shared memory (1024 ranks per CTA).
+// cluster the owning CTA's, through distributed shared memory (blockDim ranks per CTA).
 template <int K, bool CL>
 __device__ __forceinline__ int64_t *msg_field(int k, int rr) {
     if constexpr (!CL) return &FM64<K>(k, rr);
-    else return cg::this_cluster().map_shared_rank(&FM64<K>(k, rr & 1023), rr >> 10);
+    else return cg::this_cluster().map_shared_rank(&FM64<K>(k, rr % (int)blockDim.x), rr / (int)blockDim.x);
 }
 template <int K, bool CL>
 __device__ __forceinline__ int32_t *msg_count(int rr) {
     if constexpr (!CL) return &QMN<K>(rr);
-    else return cg::this_cluster().map_shared_rank(&QMN<K>(rr & 1023), rr >> 10);
+    else return cg::this_cluster().map_shared_rank(&QMN<K>(rr % (int)blockDim.x), rr / (int)blockDim.x);
 }
 
 // Grant message m the links of its route (its claims hold all of them): the reservation,
@@ -1088,17 +1095,17 @@ __device__ __forceinline__ void grant_msg(const DevGraph &g, const DevOut &o, co
     const int64_t cs = ms.cps_s;
     const int64_t cr = ms.cps_r > cs + xf ? ms.cps_r : cs + xf;
     const int sn = g.msg_send_node[m], dn = g.msg_recv_node[m];
-    c.cp[sn * R + si] = (int64_t)(epoch | (uint64_t)cs);
-    c.cp[dn * R + di] = (int64_t)(epoch | (uint64_t)cr);
+    c.cp_g[sn * R + si] = (int64_t)(epoch | (uint64_t)cs);
+    c.cp_g[dn * R + di] = (int64_t)(epoch | (uint64_t)cr);
     record(g, o, cfg, si, sn, st, e);
     record(g, o, cfg, di, dn, st, e);
     for (int side = 0; side < 2; side++) {     // both endpoints' in-flight lists and summaries
         const int rr = side ? di : si;
         const int k2 = atomicAdd(msg_count<K, CL>(rr), 1);
-        c.mlist[k2 * R + rr] = m;
-        c.mlist_node[k2 * R + rr] = side ? dn : sn;
-        c.mlist_s[k2 * R + rr] = st;
-        c.mlist_e[k2 * R + rr] = e;
+        c.mlist_g[k2 * R + rr] = m;
+        c.mlist_node_g[k2 * R + rr] = side ? dn : sn;
+        c.mlist_s_g[k2 * R + rr] = st;
+        c.mlist_e_g[k2 * R + rr] = e;
         atomicMin(reinterpret_cast<long long *>(msg_field<K, CL>(MF_E, rr)), (long long)e);
         atomicMin(reinterpret_cast<long long *>(msg_field<K, CL>(MF_S, rr)), (long long)st);
         atomicMin(reinterpret_cast<long long *>(msg_field<K, CL>(MF_NA, rr)), (long long)st);
@@ -1222,7 +1229,7 @@ __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o,
             for (int lm = threadIdx.x; lm < RL; lm += blockDim.x) {
                 const int m = base + lm;
                 F64<K>(F_COMM_END, lm) = e;
-                append_ring<K>(c, lm, m, R, i, full_node);
+                append_ring<K>(c, lm, R, i, full_node);
                 record(g, o, cfg, m, full_node, s, e);
             }
             uni = true;
@@ -1233,7 +1240,7 @@ __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o,
                 const int lm = m - base;
                 if (lm < 0 || lm >= RL) continue;
                 F64<K>(F_COMM_END, lm) = e;
-                append_ring<K>(c, lm, m, R, i, node);
+                append_ring<K>(c, lm, R, i, node);
                 record(g, o, cfg, m, node, s, e);
             }
             uni = false;
@@ -1284,7 +1291,7 @@ __device__ __forceinline__ int64_t reserve(const DevGraph &g, const DevOut &o, c
 static __device__ void trace_walk(const DevGraph &g, const DevOut &o, const Ctx &c, Shared &sh, int &par, int cfg,
                                   int r0, int64_t best) {
     const int R = g.R, tid = threadIdx.x, lane = tid & 31, bd = blockDim.x;
-    auto fin = [&](int r, int x) -> int64_t { return __ldcg(c.cp + ((size_t)x * R + r)) & (int64_t)VAL48; };
+    auto fin = [&](int r, int x) -> int64_t { return __ldcg(c.cp_g + ((size_t)x * R + r)) & (int64_t)VAL48; };
     if (tid < 32) {             // the sink: rank r0's lowest node finishing at the critical path
         const int st = g.rank_struct[r0], nb = g.s_node_off[st], n = g.s_node_off[st + 1] - nb;
         int found = -1;
@@ -1349,14 +1356,15 @@ static __device__ void trace_walk(const DevGraph &g, const DevOut &o, const Ctx 
     if (tid == 0) o.trace_len[cfg] = (int32_t)len;
 }
 
-// Zero this CTA's ranks' columns of a [rows][R] array (clusters split a point's ranks).
+// Zero this CTA's ranks' columns of a [rows][R] array (clusters split a point's ranks; `a`
+// is the CTA's offset view, column 0 = its first rank).
 template <bool CL, typename T>
-__device__ __forceinline__ void zero_cols(T *a, size_t rows, int R, int base, int RL) {
+__device__ __forceinline__ void zero_cols(T *a, size_t rows, int R, int RL) {
     if constexpr (!CL) {
         for (size_t i = threadIdx.x; i < rows * R; i += blockDim.x) a[i] = 0;
     } else {               // (a cluster CTA's columns: RL == blockDim.x except in the last CTA)
         if ((int)threadIdx.x < RL)
-            for (size_t w = 0; w < rows; w++) a[w * R + base + threadIdx.x] = 0;
+            for (size_t w = 0; w < rows; w++) a[w * R + threadIdx.x] = 0;
     }
 }
 
@@ -1386,7 +1394,7 @@ __global__ void __launch_bounds__(1024, 1)
         c.base = base_r;
         unsigned char *base = sc.base + (size_t)cid * sc.slot_bytes;
         const size_t words = (size_t)g.max_words * R;
-        uint64_t *gbits = reinterpret_cast<uint64_t *>(base + sc.off_bits);
+        uint64_t *gbits = reinterpret_cast<uint64_t *>(base + sc.off_bits) + base_r;   // (offset views)
         c.rdyc = gbits;
         c.rdyh = gbits + words;
         c.due = gbits + 2 * words;
@@ -1394,11 +1402,12 @@ __global__ void __launch_bounds__(1024, 1)
         c.DR = sc.done_in_smem ? bd : R;
         c.touched = sc.touch_in_smem ? reinterpret_cast<uint64_t *>(smem + sc.sm_off_touch) : gbits + 4 * words;
         c.BR = sc.touch_in_smem ? bd : R;
-        c.cp = reinterpret_cast<int64_t *>(base + sc.off_cp);
-        c.acc = sc.acc_in_smem ? reinterpret_cast<int64_t *>(smem + sc.sm_off_acc)
-                               : reinterpret_cast<int64_t *>(base + sc.off_acc);
-        c.ring_inst = reinterpret_cast<int32_t *>(base + sc.off_ring);
-        c.ring_node = c.ring_inst + (size_t)g.coll_stride * R;
+        c.cp_g = reinterpret_cast<int64_t *>(base + sc.off_cp);
+        c.cp = c.cp_g + base_r;
+        c.acc = sc.acc_in_smem ? reinterpret_cast<int64_t *>(smem + sc.sm_off_acc)    // (single-CTA points only)
+                               : reinterpret_cast<int64_t *>(base + sc.off_acc) + base_r;
+        c.ring_inst = reinterpret_cast<int32_t *>(base + sc.off_ring) + base_r;
+        c.ring_node = c.ring_inst + (size_t)g.coll_stride * R;    // (offset view)
         c.dur = sc.dur_in_smem ? reinterpret_cast<int64_t *>(smem + sc.sm_off_dur)
                                : reinterpret_cast<int64_t *>(base + sc.off_dur) + (size_t)crank * g.total_nodes;
         unsigned char *ib = sc.inst_in_smem ? smem + sc.sm_off_inst : base + sc.off_inst;
@@ -1426,10 +1435,14 @@ __global__ void __launch_bounds__(1024, 1)
         c.link_owner = reinterpret_cast<unsigned long long *>(c.link_busy + sc.link_cap);
         c.link_cap = sc.link_cap;
         c.mcomplist = reinterpret_cast<int32_t *>(c.msg + M);
-        c.mlist = c.mcomplist + M;
-        c.mlist_node = c.mlist + (size_t)g.p2p_stride * R;
-        c.mlist_s = reinterpret_cast<int64_t *>(base + sc.off_mlist_se);
-        c.mlist_e = c.mlist_s + (size_t)g.p2p_stride * R;
+        c.mlist_g = c.mcomplist + M;
+        c.mlist_node_g = c.mlist_g + (size_t)g.p2p_stride * R;
+        c.mlist_s_g = reinterpret_cast<int64_t *>(base + sc.off_mlist_se);
+        c.mlist_e_g = c.mlist_s_g + (size_t)g.p2p_stride * R;
+        c.mlist = c.mlist_g + base_r;
+        c.mlist_node = c.mlist_node_g + base_r;
+        c.mlist_s = c.mlist_s_g + base_r;
+        c.mlist_e = c.mlist_e_g + base_r;
     }
     __syncthreads();
     const bool is_leader = crank == 0 && tid == 0;      // writes the point's row
@@ -1440,8 +1453,8 @@ __global__ void __launch_bounds__(1024, 1)
     Lane L;
     L.r = base_r + tid;             // (inactive lanes never index per-rank state with it)
     L.lr = tid;
-    L.br = sc.touch_in_smem ? tid : L.r;
-    L.dr = sc.done_in_smem ? tid : L.r;
+    L.br = tid;                     // (shared memory, or the offset HBM view)
+    L.dr = tid;
     {
         // kept in shared memory: re-reading them there is cheaper than the two dependent
         // global loads the compiler would otherwise repeat under register pressure
@@ -1464,9 +1477,9 @@ __global__ void __launch_bounds__(1024, 1)
     if (CL && is_leader) { c.ncomp[0] = 0; c.nmcomp[0] = 0; }
     // the global bitmaps are all-zero after a point that ran to completion;
     // clear them once up front and again only after a point that did not
-    zero_cols<CL>(gbits, (size_t)g.max_words * 5, R, base_r, RL);  // ready/due/done/touched columns
+    zero_cols<CL>(gbits, (size_t)g.max_words * 5, R, RL);  // ready/due/done/touched columns
     bool dirty = false;
-    zero_cols<CL>(c.cp, (size_t)g.max_nodes, R, base_r, RL);        // epoch 0 = empty
+    zero_cols<CL>(c.cp, (size_t)g.max_nodes, R, RL);        // epoch 0 = empty
     gsync<CL>();
     unsigned epoch = 0;
     bool have_dur = false;          // durations of the previous point's device, reused when unchanged
@@ -1528,10 +1541,10 @@ __global__ void __launch_bounds__(1024, 1)
                 zdur |= rec_kind(nb_) == FL_COMP || (rec_kind(nb_) == FL_HOST && !rec_static(nb_));
             }
         }
-        if (dirty) zero_cols<CL>(gbits, (size_t)g.max_words * 3, R, base_r, RL);
+        if (dirty) zero_cols<CL>(gbits, (size_t)g.max_words * 3, R, RL);
         if (g.needs_done) {
             if (sc.done_in_smem) for (size_t i = tid; i < (size_t)g.max_words * bd; i += bd) c.done[i] = 0;
-            else zero_cols<CL>(c.done, (size_t)g.max_words, R, base_r, RL);
+            else zero_cols<CL>(c.done, (size_t)g.max_words, R, RL);
         }
         if (sc.touch_in_smem) for (size_t i = tid; i < (size_t)g.max_words * bd; i += bd) c.touched[i] = 0;
         if (tid == 0) { sh.cend_all = 0; sh.cend_uniform = 1; sh.ncons = 0; sh.seq_ovf = 0; }
@@ -1554,7 +1567,7 @@ __global__ void __launch_bounds__(1024, 1)
             continue;
         }
         if (++epoch == 64) {       // 6-bit tags wrap: start a fresh accumulator table
-            zero_cols<CL>(c.cp, (size_t)g.max_nodes, R, base_r, RL);
+            zero_cols<CL>(c.cp, (size_t)g.max_nodes, R, RL);
             epoch = 1;
             gsync<CL>();
         }
@@ -1635,7 +1648,7 @@ __global__ void __launch_bounds__(1024, 1)
                 F32<K>(Q_DONE, tid) += g.s_nstatic[st];
                 if (f.trace)        // folded static hosts start and finish at 0 (never popped here)
                     for (int q = g.static_off[st]; q < g.static_off[st + 1]; q++)
-                        c.cp[g.static_list[q] * R + L.r] = (int64_t)f.epoch;
+                        c.cp[g.static_list[q] * R + L.lr] = (int64_t)f.epoch;
                 if (o.ev_start)
                     for (int q = g.static_off[st]; q < g.static_off[st + 1]; q++)
                         record(g, o, cfg, L.r, g.static_list[q], 0, 0);

@@ -296,6 +296,22 @@ def test_engine_cluster_8192_ranks_vs_oracle():
         assert {k: int(out[k][i]) for k in ROW_KEYS} == O.sweep_row(gs, parse_topology(spec), algo, flat=flat), spec
 
 
+@pytest.mark.parametrize("ctas", [3, 4, 5, 7])
+@pytest.mark.parametrize("kind", ["race", "p2p"])
+def test_engine_cluster_sizes_vs_oracle(kind, ctas, monkeypatch):
+    """Clusters wider than ceil(R / 1024): ceil(R / CTAs) ranks per CTA, blocks that are not
+    a multiple of 1024 (FL_CLUSTER_CTAS forces the size the engine otherwise picks from
+    occupancy), DSMEM owners of the message summaries included."""
+    monkeypatch.setenv("FL_CLUSTER_CTAS", str(ctas))
+    if kind == "race":
+        gs, topo = random_graphs(30_000 + ctas, min_world=2049, max_world=3000, max_nodes=10)
+        _check_race(gs, topo, ctas, (("ring", 1), ("tree", 2)))
+    else:
+        from randgraphs import random_p2p_graphs
+        gs, topo = random_p2p_graphs(40_000 + ctas, world=2100 + 37 * ctas, n_msgs=3000)
+        _check_p2p(gs, topo, ctas)
+
+
 # ---- critical-path node trace (SPEC.md:460; the path rule is documented at engine.critical_path_trace) ----
 
 def _trace_both(gs, topo, algo):

@@ -1369,7 +1369,12 @@ __device__ __forceinline__ void zero_cols(T *a, size_t rows, int R, int RL) {
 }
 
 template <int K, bool CL>
-__global__ void __launch_bounds__(1024, 1)
+#ifndef FL_NARROW_BOUNDS
+#define FL_NARROW_BOUNDS 1
+#endif
+// Narrow-plane variants (<= 256 ranks per CTA) are launched with at most that many threads,
+// so their register budget is not the 64 a 1024-thread CTA allows (FL_NARROW_BOUNDS=0: A/B)
+__global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() : 1024, 1)
     sweep_kernel(const __grid_constant__ DevGraph g, const __grid_constant__ DevPoints p,
                  const __grid_constant__ DevOut o, const __grid_constant__ DevScratch sc) {
     unsigned char *smem = fl_smem;

@@ -1386,7 +1386,10 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
     const int crank = CL ? (int)cg::this_cluster().block_rank() : 0;
     const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;     // this cluster, clusters in the grid
     const int base_r = crank * bd;
-    const int RL = R - base_r < bd ? R - base_r : bd;          // ranks owned by this CTA
+    // ranks owned by this CTA (a single CTA's block is R rounded up to a warp, so RL = R: a
+    // kernel parameter, which `active` tests straight from the constant bank -- a computed RL
+    // was spilled and re-loaded from local memory at every step)
+    const int RL = CL ? (R - base_r < bd ? R - base_r : bd) : R;
 
     // ---- carve shared memory and this cluster's scratch slot ----
     // (the pointer table lives in shared memory: it is block-uniform and would
@@ -1454,7 +1457,7 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
     uint64_t *gbits = c.rdyc;
     const int NI = g.n_inst;
 
-    const bool active = tid < RL;
+    const bool active = CL ? tid < RL : tid < g.R;
     Lane L;
     L.r = base_r + tid;             // (inactive lanes never index per-rank state with it)
     L.lr = tid;

@@ -180,6 +180,9 @@ class Engine:
     def __init__(self, graphs_or_set, device: int = 0):
         self.gs = graphs_or_set if isinstance(graphs_or_set, GraphSet) else compile_graphs(graphs_or_set)
         check_supported(self.gs)
+        if self.gs.pair_error:      # an unmatched SEND/RECV channel never runs (simulator.py:177-200)
+            from .errors import DeadlockError
+            raise DeadlockError(self.gs.pair_error)
         L = _native.lib()
         arrs = desc_arrays(self.gs)
         d = _native.GraphDesc()

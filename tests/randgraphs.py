@@ -143,3 +143,50 @@ def random_p2p_graphs(seed: int, mesh: bool = False, world: int = 0, n_msgs: int
     bw = rng.choice([1e9, 2e9])
     topo = Topology.mesh2d(rows, cols, bw, lat) if mesh else Topology.switch(world, bw, lat)
     return graphs, topo
+
+
+def random_spmd_graphs(seed: int, world: int, n_nodes: int = 24, p_coll: float = 0.3, per_rank_dur: bool = True):
+    """One random DAG shared by every rank (same node ids, same dependencies), whose
+    collectives all span the world -- the structure of data-parallel and FSDP graphs, and
+    the one cluster design points reserve without instance state in HBM (engine.cu
+    cl_step_clic).  Durations are drawn per rank (0, 5, 10, 15 ns, so ranks complete their
+    part of an instance at different steps and many collectives complete together) or shared."""
+    rng = random.Random(seed)
+    tmpl = []                           # (kind, deps, coll kind, bytes, launch twin)
+    for i in range(n_nodes):
+        deps = sorted(rng.sample(range(i), min(i, rng.randint(0, 3))))
+        if rng.random() < p_coll:
+            kind = rng.choice(KINDS if rng.random() < 0.5 else KINDS[:1])
+            nbytes = rng.choice([0, 64, 4096, 1 << 20]) if rng.random() < 0.3 else rng.randrange(4, 8192, 4)
+            tmpl.append(("coll", deps, kind, nbytes, rng.random() < 0.3))
+        else:
+            tmpl.append(("comp", deps, None, 0, rng.random() < 0.3))
+    shared = [rng.choice([0, 5, 10, 15]) for _ in range(n_nodes)]
+    graphs = []
+    group = list(range(world))
+    for rank in range(world):
+        nodes, tensors = [], {}
+        ids = {}
+        nid = 0
+        for i, (kind, deps, ck, nbytes, twin) in enumerate(tmpl):
+            ctrl = []
+            if twin:
+                nodes.append(Node(nid, NodeKind.HOST, "launch"))
+                ctrl = [(nid, "launch")]
+                nid += 1
+            tensors[i] = TensorMeta.make(i, [4], Dtype.F32)
+            data = sorted(ids[d] for d in deps)
+            ins = list(deps)
+            if kind == "coll":
+                nodes.append(Node(nid, NodeKind.COLL, ck.value.lower(), inputs=ins, outputs=[i], data_deps=data,
+                                  ctrl_deps=ctrl, coll=CollSpec(ck, group, nbytes)))
+            else:
+                d = rng.choice([0, 5, 10, 15]) if per_rank_dur else shared[i]
+                nodes.append(Node(nid, NodeKind.COMP, "work", inputs=ins, outputs=[i], data_deps=data,
+                                  ctrl_deps=ctrl, duration_ns=d))
+            ids[i] = nid
+            nid += 1
+        graphs.append(WorkloadGraph(rank, world, nodes, tensors, {"graph_inputs": []}))
+    lat = rng.choice([0, 1, 10, 100])
+    bw = rng.choice([1e9, 4e9, 1e12])
+    return graphs, Topology.switch(world, bw, lat)

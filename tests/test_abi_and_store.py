@@ -62,3 +62,15 @@ def test_compile_rejects_duplicate_ranks():
     gs[1].rank = 0
     with pytest.raises(ValueError):
         compile_graphs(gs)
+
+
+def test_engine_refuses_unmatched_channel_with_deadlock_error():
+    """A SEND without its RECV (simulator.py:177-200): the batched engine raises the
+    reference's DeadlockError before any launch instead of returning rows."""
+    from paper_2604_17550_b200.engine import Engine
+    from paper_2604_17550_b200.errors import DeadlockError
+    from paper_2604_17550_b200.graph import Node, NodeKind, P2pSpec, WorkloadGraph
+    g0 = WorkloadGraph(0, 2, [Node(0, NodeKind.SEND, "send", p2p=P2pSpec(1, 64, 7))], {}, {"graph_inputs": []})
+    g1 = WorkloadGraph(1, 2, [Node(0, NodeKind.HOST, "idle")], {}, {"graph_inputs": []})
+    with pytest.raises(DeadlockError):
+        Engine([g0, g1])

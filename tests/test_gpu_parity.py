@@ -312,6 +312,19 @@ def test_engine_cluster_sizes_vs_oracle(kind, ctas, monkeypatch):
         _check_p2p(gs, topo, ctas)
 
 
+@pytest.mark.parametrize("seed", range(8))
+def test_engine_cluster_spmd_vs_oracle(seed, monkeypatch):
+    """SPMD graphs whose collectives all span the world at 1025-3244 ranks (the structure of
+    the C4 families) on clusters of 2-6 CTAs: per-rank durations in {0, 5, 10, 15}, so a
+    CTA's members finish at different steps, several instances complete in one step, and
+    zero-length collectives run serial mode."""
+    from randgraphs import random_spmd_graphs
+    if seed % 2:
+        monkeypatch.setenv("FL_CLUSTER_CTAS", str(3 + seed % 4))
+    gs, topo = random_spmd_graphs(50_000 + seed, 1025 + 317 * seed, n_nodes=16 + seed, per_rank_dur=seed % 3 != 0)
+    _check_race(gs, topo, seed, (("ring", 1), ("ring", 2)))
+
+
 # ---- critical-path node trace (SPEC.md:460; the path rule is documented at engine.critical_path_trace) ----
 
 def _trace_both(gs, topo, algo):

@@ -1487,7 +1487,10 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
     // clear them once up front and again only after a point that did not
     zero_cols<CL>(gbits, (size_t)g.max_words * 5, R, RL);  // ready/due/done/touched columns
     bool dirty = false;
-    zero_cols<CL>(c.cp, (size_t)g.max_nodes, R, RL);        // epoch 0 = empty
+    // epoch 0 = empty.  With the first-dependency bitmap in shared memory no word is read before
+    // this design point wrote it (counted words behind their touched bit, set members and
+    // trace finishes written first), so small points skip the table-wide clear
+    if (!sc.touch_in_smem) zero_cols<CL>(c.cp, (size_t)g.max_nodes, R, RL);
     gsync<CL>();
     unsigned epoch = 0;
     bool have_dur = false;          // durations of the previous point's device, reused when unchanged
@@ -1575,7 +1578,7 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
             continue;
         }
         if (++epoch == 64) {       // 6-bit tags wrap: start a fresh accumulator table
-            zero_cols<CL>(c.cp, (size_t)g.max_nodes, R, RL);
+            if (!sc.touch_in_smem) zero_cols<CL>(c.cp, (size_t)g.max_nodes, R, RL);
             epoch = 1;
             gsync<CL>();
         }

@@ -10,6 +10,7 @@ and the issue-slot roofline).  WORKLOAD defaults to c3, POINTS to 4096.
 import csv
 import io
 import json
+import os
 import shutil
 import subprocess
 import sys
@@ -43,7 +44,8 @@ dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
 summary = subprocess.run([sys.executable, str(root / "scripts" / "ncu_summary.py"), rep, "", "30"],
                          capture_output=True, text=True).stdout
 funcs = subprocess.run([sys.executable, str(root / "scripts" / "ncu_lines.py"), rep,
-                        str(root / "paper_2604_17550_b200" / "csrc" / "engine.cu"), str(points * 32)],
+                        os.environ.get("FL_PROFILE_SRC", str(root / "paper_2604_17550_b200" / "csrc" / "engine.cu")),
+                        str(points * int(os.environ.get("FL_PROFILE_WARPS", "32")))],
                        capture_output=True, text=True).stdout
 (prof / f"{tag}_ncu.txt").write_text(
     f"# ncu --set full, sweep kernel, {workload.upper()} ({points} points)\n"

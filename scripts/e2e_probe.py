@@ -65,3 +65,37 @@ for _ in range(reps):
 print("kernel (events, device inputs)        median/min us: %.1f / %.1f" % (np.median(ks), np.min(ks)))
 print("run_device + synchronize (wall)       median/min us: %.1f / %.1f" %
       timeit(lambda: (eng.run_device(ptrs, stream.cuda_stream, n), torch.cuda.synchronize())))
+# as bench.py times it: a 256 MiB L2 flush and a synchronize before every step
+flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+
+def flushed(fn):
+    ts = []
+    for _ in range(reps // 4):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    return np.median(ts) * 1e6, np.min(ts) * 1e6
+
+
+print("Engine.run after flush + sync         median/min us: %.1f / %.1f" % flushed(lambda: eng.run(hp)))
+ks = []
+for _ in range(reps // 4):
+    flush.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    eng.run_device(ptrs, stream.cuda_stream, n)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ks.append(e0.elapsed_time(e1) * 1e3)
+print("kernel after flush (events)           median/min us: %.1f / %.1f" % (np.median(ks), np.min(ks)))
+hp2 = DesignPoints(pin["algo"], pin["topo_kind"], pin["bw"], pin["latency"], pin["rows"], pin["cols"],
+                   torch.full((n,), 1e12, dtype=torch.float64).pin_memory().numpy(),
+                   torch.full((n,), 1.0, dtype=torch.float64).pin_memory().numpy())
+print("Engine.run + peak/eff, flush + sync   median/min us: %.1f / %.1f" % flushed(lambda: eng.run(hp2)))
+import gc
+gc.disable()
+print("  same, GC off                        median/min us: %.1f / %.1f" % flushed(lambda: eng.run(hp2)))
+gc.enable()

@@ -1,6 +1,6 @@
 """Small engine runs for compute-sanitizer (memcheck / racecheck / synccheck).
 
-    compute-sanitizer --tool memcheck python scripts/sanitize.py [analytical|p2p|cluster]
+    compute-sanitizer --tool memcheck python scripts/sanitize.py [analytical|p2p|cluster|cluster9|cluster_p2p]
 
 Every case is also checked against the CPU oracle, so a run that the sanitizer
 passes is a correct one.  Sizes are kept small: racecheck replays shared-memory
@@ -53,6 +53,17 @@ def main(case: str) -> None:
     elif case == "cluster":
         gs = synth.synth_transformer(synth.PRESETS["tiny"], synth.ParallelConfig(synth.Strategy.DP, 2048), 2048)
         check(gs, [("switch:2048:100GB:1us", "ring"), ("mesh:32x64:400GB:100ns", "mesh-hier")])
+    elif case == "cluster9":          # 8192 ranks: 9 CTAs of 911 ranks (blocks of 928 threads)
+        gs = synth.synth_transformer(synth.PRESETS["tiny"], synth.ParallelConfig(synth.Strategy.DP, 8192), 8192)
+        check(gs, [("switch:8192:100GB:1us", "ring"), ("mesh:64x128:400GB:100ns", "mesh-hier")])
+    elif case == "cluster_p2p":       # messages on a cluster of 4 CTAs of 600 ranks (DSMEM summaries)
+        import os
+        os.environ["FL_CLUSTER_CTAS"] = "4"
+        from randgraphs import random_p2p_graphs
+        gs, topo = random_p2p_graphs(40_004, world=2400, n_msgs=2000)
+        want = O.simulate(gs, topo, "ring", 1, 1)
+        got = E.simulate(gs, topo, E.SimOptions())
+        assert got.makespan_ns == want["makespan_ns"], (got.makespan_ns, want["makespan_ns"])
     else:
         raise SystemExit(f"unknown case {case}")
     print(f"sanitize case {case}: ok")

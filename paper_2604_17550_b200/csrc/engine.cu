@@ -140,6 +140,9 @@ __device__ __forceinline__ int64_t coll_time(const DevGraph &g, int i, int algo,
 #define FL_BASE 0       // 0: this translation unit instantiates every kernel variant
 #endif
 #define FL_COMMON (FL_BASE == 0 || FL_BASE == 1)   // non-template kernels and the dispatchers
+#ifndef FL_LEAN
+#define FL_LEAN 1               // 0: never launch the lean variant (A/B)
+#endif
 
 #if FL_COMMON
 __global__ void cost_only_kernel(int n, const uint8_t *kind, const int64_t *size, const int64_t *gn,
@@ -481,6 +484,18 @@ struct Ctx {
 __device__ __forceinline__ int64_t dur_of(const DevGraph &g, const Ctx &c, int n) {
     return g.dur_sm_off ? reinterpret_cast<const int64_t *>(fl_smem + g.dur_sm_off)[n] : c.dur[n];
 }
+// Bit 7 of the variant word: the lean variant, launched when the run needs no event record, no
+// trace, no shared-memory first-dependency bitmap or slot table, and has the durations in shared
+// memory -- those branches compile away (fewer live values under the 64-register cap).
+template <int K> __host__ __device__ constexpr bool lean() { return (K & 128) != 0; }
+// bit 8 (lean variants only): the first-dependency bitmap and the slot table are both in shared
+// memory (small design points) -- else both are not
+template <int K> __host__ __device__ constexpr bool lean_sm() { return (K & 256) != 0; }
+template <int K>
+__device__ __forceinline__ int64_t dur_of(const DevGraph &g, const Ctx &c, int n) {
+    if constexpr (lean<K>()) return reinterpret_cast<const int64_t *>(fl_smem + g.dur_sm_off)[n];
+    else return dur_of(g, c, n);
+}
 
 constexpr int32_t MSG_ALLOC = 1 << 30;   // mlist entry flag: the endpoint's outputs are allocated
 
@@ -603,9 +618,10 @@ __device__ __forceinline__ int ms_pop_cp(MinSet &m, uint64_t *b, const int64_t *
     return x;
 }
 
+template <int K>
 __device__ __forceinline__ void record(const DevGraph &g, const DevOut &o, int cfg, int r, int x, int64_t st,
                                        int64_t en) {
-    if (o.ev_start) {
+    if (!lean<K>() && o.ev_start) {
         size_t at = ((size_t)cfg * g.R + r) * g.max_nodes + x;
         o.ev_start[at] = st;
         o.ev_end[at] = en;
@@ -620,9 +636,9 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
     while (s.rh.head >= 0 && s.host_n < 0) {      // the host stream is free at t (gather_due ran at t)
         int64_t v;
         const int h = ms_pop_cp<K, F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, v, g.max_words);
-        const int64_t e = t + dur_of(g, c, L.nb + h);
+        const int64_t e = t + dur_of<K>(g, c, L.nb + h);
         { const uint4 hb = rec_b(g, L.nb + h); F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
-        record(g, o, cfg, L.r, h, t, e);
+        record<K>(g, o, cfg, L.r, h, t, e);
         if (e == t) {
             ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, h, v);
         } else {
@@ -646,11 +662,11 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
         int64_t v;
         // (the node's record and duration are read before the pop's own shared-memory traffic)
         const uint2 xal = *reinterpret_cast<const uint2 *>(&g.node_rec[2 * (L.nb + ms_min(s.rc)) + 1].z);
-        const int64_t dx = dur_of(g, c, L.nb + ms_min(s.rc));
+        const int64_t dx = dur_of<K>(g, c, L.nb + ms_min(s.rc));
         const int x = ms_pop_cp<K, F_RC_CP, F_RC_SUM>(s.rc, c.rdyc, c.cp, R, L, v, g.max_words);
         const int64_t e = t + dx;
         F64<K>(F_ALLOC, L.lr) += rec_u64(xal.x, xal.y);
-        record(g, o, cfg, L.r, x, t, e);
+        record<K>(g, o, cfg, L.r, x, t, e);
         if ((K & 7) == 1 && e > t) {      // one compute stream: its busy intervals are disjoint
             F64<K>(F_COMP, L.lr) += e - t;
             F64<K>(F_COMP_A, L.lr) = s.commcum;
@@ -723,7 +739,7 @@ __device__ __forceinline__ void dispatch(const DevGraph &g, const Ctx &c, const 
         }
         return;
     }
-    const int64_t fin = cps + dur_of(g, c, L.nb + d);
+    const int64_t fin = cps + dur_of<K>(g, c, L.nb + d);
     if (kind == FL_COMP) ms_insert_cp<K, F_RC_CP, F_RC_SUM>(s.rc, c.rdyc, c.cp, R, L, d, fin);
     else ms_insert_cp<K, F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, d, fin);
 }
@@ -1097,8 +1113,8 @@ __device__ __forceinline__ void grant_msg(const DevGraph &g, const DevOut &o, co
     const int sn = g.msg_send_node[m], dn = g.msg_recv_node[m];
     c.cp_g[sn * R + si] = (int64_t)(epoch | (uint64_t)cs);
     c.cp_g[dn * R + di] = (int64_t)(epoch | (uint64_t)cr);
-    record(g, o, cfg, si, sn, st, e);
-    record(g, o, cfg, di, dn, st, e);
+    record<K>(g, o, cfg, si, sn, st, e);
+    record<K>(g, o, cfg, di, dn, st, e);
     for (int side = 0; side < 2; side++) {     // both endpoints' in-flight lists and summaries
         const int rr = side ? di : si;
         const int k2 = atomicAdd(msg_count<K, CL>(rr), 1);
@@ -1230,7 +1246,7 @@ __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o,
                 const int m = base + lm;
                 F64<K>(F_COMM_END, lm) = e;
                 append_ring<K>(c, lm, R, i, full_node);
-                record(g, o, cfg, m, full_node, s, e);
+                record<K>(g, o, cfg, m, full_node, s, e);
             }
             uni = true;
             cend = e;
@@ -1241,7 +1257,7 @@ __device__ __forceinline__ int64_t reserve_n(const DevGraph &g, const DevOut &o,
                 if (lm < 0 || lm >= RL) continue;
                 F64<K>(F_COMM_END, lm) = e;
                 append_ring<K>(c, lm, R, i, node);
-                record(g, o, cfg, m, node, s, e);
+                record<K>(g, o, cfg, m, node, s, e);
             }
             uni = false;
             gsync<CL>();            // the next reservation reads these comm ends
@@ -1587,9 +1603,9 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
         f.epoch = (uint64_t)epoch << 58;
         f.init = 1;
         f.fold = g.fold_ok && !zero && !zdur;
-        f.touch = sc.touch_in_smem;
-        f.acc_sm = sc.acc_in_smem;
-        f.trace = o.trace_len != nullptr;
+        f.touch = lean<K>() ? lean_sm<K>() : (bool)sc.touch_in_smem;
+        f.acc_sm = lean<K>() ? lean_sm<K>() : (bool)sc.acc_in_smem;
+        f.trace = !lean<K>() && o.trace_len != nullptr;
 
         // ---- per-rank state ----
         Rank<KK> s;
@@ -1660,9 +1676,9 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
                 if (f.trace)        // folded static hosts start and finish at 0 (never popped here)
                     for (int q = g.static_off[st]; q < g.static_off[st + 1]; q++)
                         c.cp[g.static_list[q] * R + L.lr] = (int64_t)f.epoch;
-                if (o.ev_start)
+                if (!lean<K>() && o.ev_start)
                     for (int q = g.static_off[st]; q < g.static_off[st + 1]; q++)
-                        record(g, o, cfg, L.r, g.static_list[q], 0, 0);
+                        record<K>(g, o, cfg, L.r, g.static_list[q], 0, 0);
             }
             reserve<MSG, CL, KK>(g, o, c, sh, par, 0, false, cfg, f.epoch, topo, sh.pcols);
             if (active) refresh_ring(c, L, s);
@@ -1798,7 +1814,7 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
             if (is_leader) o.rows[(size_t)cfg * 6 + k] = v;
         }
         if (is_leader) o.status[cfg] = overflow ? FL_ERR_CAPACITY : dead ? FL_ERR_DEADLOCK : FL_OK;
-        if (o.trace_len) {
+        if (!lean<K>() && o.trace_len) {
             // the sink's rank: the lowest one whose largest critical-path finish is the point's
             uint64_t rk = (active && F64<K>(F_CPMAX, tid) == cpbest) ? (uint64_t)L.r : KINF;
             rk = gmin_key<CL>(rk, sh, par);
@@ -1873,7 +1889,7 @@ __global__ void cp_kernel(const __grid_constant__ DevGraph g, const __grid_const
 template <int T>
 static cudaError_t launch_t(int grid, int block, size_t smem, cudaStream_t st, int cluster, const DevGraph &g,
                             const DevPoints &p, const DevOut &o, const DevScratch &sc) {
-    if constexpr ((T >> 5) != 0) {     // narrow planes: single-CTA design points only
+    if constexpr (((T >> 5) & 3) != 0) {     // narrow planes: single-CTA design points only
         sweep_kernel<T, false><<<grid, block, smem, st>>>(g, p, o, sc);
         return cudaGetLastError();
     } else {
@@ -1933,6 +1949,40 @@ FL_PART_DECL(1) FL_PART_DECL(2) FL_PART_DECL(4) FL_PART_DECL(9) FL_PART_DECL(10)
 #if FL_BASE == 0 || FL_BASE == 1
 FL_PART_DEF(1)
 #endif
+// Lean variants (lean<K>, "bit 7"), all in the FL_BASE 1 unit: one compute stream, no messages,
+// 1024-lane planes (single CTA and cluster) and the narrow planes with the bitmap and slot table
+// in shared memory.  A/B (scripts/ab.py, FL_LEAN=0): C3 +5.3%, C2 +4.8%, C4 +4.4-4.7%; the same
+// specialization of the message variants gained nothing on the expanded workloads.
+#define FL_LEAN_LIST1(X) X(1 + 128) X(1 + 64 + 128 + 256) X(1 + 32 + 128 + 256)
+// (the cluster variant of 1 + 128 lives in the FL_BASE 1 unit)
+#define FL_LEAN_CLUSTER1 (T == 1 + 128 ? launch_t<1 + 128>(grid, block, smem, st, cluster, g, p, o, sc) : cudaErrorInvalidValue)
+#define FL_LEAN_CLUSTER_SMEM1                                                                               \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<1 + 128, true>, A, (int)smem);              \
+    if (e == cudaSuccess)                                                                                   \
+        e = cudaFuncSetAttribute(sweep_kernel<1 + 128, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+#define FL_LEAN_CASE(T) case T: sweep_kernel<T, false><<<grid, block, smem, st>>>(g, p, o, sc); return cudaGetLastError();
+#define FL_LEAN_SMEM(T) if (e == cudaSuccess) e = cudaFuncSetAttribute(sweep_kernel<T, false>, A, (int)smem);
+#define FL_LEAN_DEF(U)                                                                                      \
+    cudaError_t launch_sweep_lean##U(int T, int grid, int block, size_t smem, cudaStream_t st, int cluster,  \
+                                     const DevGraph &g, const DevPoints &p, const DevOut &o, const DevScratch &sc) { \
+        if (cluster > 1) return FL_LEAN_CLUSTER##U;                                                         \
+        switch (T) { FL_LEAN_LIST##U(FL_LEAN_CASE) default: return cudaErrorInvalidValue; }                 \
+    }                                                                                                       \
+    cudaError_t set_smem_lean##U(size_t smem) {                                                             \
+        cudaError_t e = cudaSuccess;                                                                        \
+        const cudaFuncAttribute A = cudaFuncAttributeMaxDynamicSharedMemorySize;                            \
+        FL_LEAN_LIST##U(FL_LEAN_SMEM)                                                                       \
+        FL_LEAN_CLUSTER_SMEM##U                                                                             \
+        return e;                                                                                           \
+    }
+#define FL_LEAN_DECL(U)                                                                                     \
+    cudaError_t launch_sweep_lean##U(int T, int grid, int block, size_t smem, cudaStream_t st, int cluster,  \
+                                     const DevGraph &g, const DevPoints &p, const DevOut &o, const DevScratch &sc); \
+    cudaError_t set_smem_lean##U(size_t smem);
+FL_LEAN_DECL(1)
+#if FL_BASE == 0 || FL_BASE == 1
+FL_LEAN_DEF(1)
+#endif
 #if FL_BASE == 0 || FL_BASE == 2
 FL_PART_DEF(2)
 #endif
@@ -1954,6 +2004,13 @@ cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t s
                          const DevPoints &p, const DevOut &o, const DevScratch &sc) {
     // variant word: compute streams (1, 2, 4) | 8 when the graphs carry SEND/RECV | plane class << 5
     const int B = K | (g.n_msg > 0 ? 8 : 0);
+    // the lean variant when the run needs none of the branches it drops (bit 7, bit 8)
+    if (FL_LEAN && B == 1 && !o.ev_start && !o.trace_len && g.dur_sm_off && sc.touch_in_smem == sc.acc_in_smem) {
+        const int pc = cluster > 1 ? 0 : plane_class(block);
+        const int T = B | pc << 5 | 128 | (sc.touch_in_smem ? 256 : 0);
+        if (T == 1 + 128 || (cluster <= 1 && (T == 1 + 64 + 128 + 256 || T == 1 + 32 + 128 + 256)))
+            return launch_sweep_lean1(T, grid, block, smem, st, cluster, g, p, o, sc);
+    }
     const int T = B | (cluster > 1 ? 0 : plane_class(block) << 5);
     switch (B) {
         case 1: return launch_sweep_b1(T, grid, block, smem, st, cluster, g, p, o, sc);
@@ -1989,6 +2046,7 @@ cudaError_t sweep_occupancy(int block, size_t smem, int cluster, int *occ) {
 
 cudaError_t sweep_set_smem(size_t smem) {
     cudaError_t e = set_smem_b1(smem);
+    if (e == cudaSuccess) e = set_smem_lean1(smem);
     if (e == cudaSuccess) e = set_smem_b2(smem);
     if (e == cudaSuccess) e = set_smem_b4(smem);
     if (e == cudaSuccess) e = set_smem_b9(smem);

@@ -143,6 +143,9 @@ __device__ __forceinline__ int64_t coll_time(const DevGraph &g, int i, int algo,
 #ifndef FL_LEAN
 #define FL_LEAN 1               // 0: never launch the lean variant (A/B)
 #endif
+#ifndef FL_LEAN_FULL
+#define FL_LEAN_FULL 1          // lean single-CTA variants assume every lane is a rank (block == R)
+#endif
 
 #if FL_COMMON
 __global__ void cost_only_kernel(int n, const uint8_t *kind, const int64_t *size, const int64_t *gn,
@@ -1473,7 +1476,8 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
     uint64_t *gbits = c.rdyc;
     const int NI = g.n_inst;
 
-    const bool active = CL ? tid < RL : tid < g.R;
+    // (a lean single-CTA variant runs only blocks of exactly R threads: every lane is a rank)
+    const bool active = (lean<K>() && !CL && FL_LEAN_FULL) ? true : CL ? tid < RL : tid < g.R;
     Lane L;
     L.r = base_r + tid;             // (inactive lanes never index per-rank state with it)
     L.lr = tid;
@@ -2005,7 +2009,8 @@ cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t s
     // variant word: compute streams (1, 2, 4) | 8 when the graphs carry SEND/RECV | plane class << 5
     const int B = K | (g.n_msg > 0 ? 8 : 0);
     // the lean variant when the run needs none of the branches it drops (bit 7, bit 8)
-    if (FL_LEAN && B == 1 && !o.ev_start && !o.trace_len && g.dur_sm_off && sc.touch_in_smem == sc.acc_in_smem) {
+    if (FL_LEAN && B == 1 && !o.ev_start && !o.trace_len && g.dur_sm_off && sc.touch_in_smem == sc.acc_in_smem &&
+        (cluster > 1 || !FL_LEAN_FULL || block == g.R)) {
         const int pc = cluster > 1 ? 0 : plane_class(block);
         const int T = B | pc << 5 | 128 | (sc.touch_in_smem ? 256 : 0);
         if (T == 1 + 128 || (cluster <= 1 && (T == 1 + 64 + 128 + 256 || T == 1 + 32 + 128 + 256)))

@@ -434,6 +434,8 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
         int fold_ok = 1;
         for (int s = 0; s < S; s++) fold_ok &= s_fold[s];
         dg.fold_ok = fold_ok;
+        dg.dyn_host = 0;
+        for (int i = 0; i < total; i++) dg.dyn_host |= d->node_kind[i] == FL_HOST && !is_static[i];
         std::vector<int2> tc((size_t)(total_t > 0 ? total_t : 1));
         for (int i = 0; i < total_t; i++) tc[i] = make_int2(d->tens_cons_off[i], d->tens_cons_off[i + 1]);
         dg.needs_done = !mfree.empty();
@@ -608,7 +610,8 @@ int ensure_scratch(fl_graph *g, int grid) {
     return FL_OK;
 }
 
-int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stream) {
+int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stream, int *launches = nullptr) {
+    if (launches) *launches = 0;
     if (pts->n_points <= 0) return FL_OK;
     int cs = pts->compute_streams;
     if (cs < 1 || cs > 4) return fail(FL_ERR_CAPACITY, "compute_streams must be 1..4 in this build");
@@ -626,6 +629,7 @@ int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stre
     dp.peak_flops = pts->peak_flops;
     dp.efficiency = pts->efficiency;
     dp.compute_streams = cs;
+    dp.retry = 0;
     fl::DevScratch sc = g->sc;
     sc.links_in_smem = g->links_sm_cap > 0 && sc.link_cap <= g->links_sm_cap;
     fl::DevOut dout;
@@ -639,8 +643,10 @@ int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stre
     dout.trace = out->trace_len ? out->trace : nullptr;
     dout.trace_len = out->trace_len;
     dout.trace_cap = out->trace ? out->trace_cap : 0;
+    int nl = 0;
     CK(fl::launch_sweep(cs == 3 ? 4 : cs, grid * g->cluster, g->block, g->smem, stream, g->cluster, g->dg, dp, dout,
-                        sc));
+                        sc, &nl));
+    if (launches) *launches = nl;
     return FL_OK;
 }
 
@@ -707,8 +713,9 @@ int fl_sweep_run_device(fl_graph *g, const fl_points *dev_points, fl_outputs *de
                         int32_t *launches) {
     if (!g || !dev_points || !dev_out) return fail(FL_ERR_INVALID, "null argument");
     CK(cudaSetDevice(g->device));
-    int rc = launch(g, dev_points, dev_out, static_cast<cudaStream_t>(stream));
-    if (launches) *launches = rc == FL_OK && dev_points->n_points > 0 ? 1 : 0;
+    int nl = 0;
+    int rc = launch(g, dev_points, dev_out, static_cast<cudaStream_t>(stream), &nl);
+    if (launches) *launches = rc == FL_OK ? nl : 0;
     return rc;
 }
 

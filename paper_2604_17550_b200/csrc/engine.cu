@@ -494,6 +494,11 @@ template <int K> __host__ __device__ constexpr bool lean() { return (K & 128) !=
 // bit 8 (lean variants only): the first-dependency bitmap and the slot table are both in shared
 // memory (small design points) -- else both are not
 template <int K> __host__ __device__ constexpr bool lean_sm() { return (K & 256) != 0; }
+// A lean variant also assumes static hosts are folded (launched only for graph sets without a
+// non-static HOST, so the host stream is never used) -- a design point that cannot fold (a
+// zero-length node, engine.cu "t = 0 host pops") is marked FL_RETRY and evaluated by the
+// general variant in a second pass (launch_sweep).
+template <int K> __host__ __device__ constexpr bool nohost() { return lean<K>(); }
 template <int K>
 __device__ __forceinline__ int64_t dur_of(const DevGraph &g, const Ctx &c, int n) {
     if constexpr (lean<K>()) return reinterpret_cast<const int64_t *>(fl_smem + g.dur_sm_off)[n];
@@ -636,7 +641,7 @@ template <int K>
 __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, const Ctx &c, const Lane &L,
                                             Rank<K> &s, const Step &f, int64_t t, int cfg) {
     const int R = g.R;                      // (a kernel parameter: no shared-memory load)
-    while (s.rh.head >= 0 && s.host_n < 0) {      // the host stream is free at t (gather_due ran at t)
+    while (!nohost<K>() && s.rh.head >= 0 && s.host_n < 0) {      // the host stream is free at t (gather_due ran at t)
         int64_t v;
         const int h = ms_pop_cp<K, F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, v, g.max_words);
         const int64_t e = t + dur_of<K>(g, c, L.nb + h);
@@ -744,7 +749,7 @@ __device__ __forceinline__ void dispatch(const DevGraph &g, const Ctx &c, const 
     }
     const int64_t fin = cps + dur_of<K>(g, c, L.nb + d);
     if (kind == FL_COMP) ms_insert_cp<K, F_RC_CP, F_RC_SUM>(s.rc, c.rdyc, c.cp, R, L, d, fin);
-    else ms_insert_cp<K, F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, d, fin);
+    else if (!nohost<K>()) ms_insert_cp<K, F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, d, fin);
 }
 
 // A statically ordered node's accumulator word (capi.cu "Accumulator slots"): in shared
@@ -898,7 +903,7 @@ template <int K>
 __device__ __forceinline__ int64_t next_time(const DevGraph &g, const Ctx &c, const Lane &L, const Rank<K> &s,
                                              int64_t tcur) {
     if (s.due.head >= 0) return tcur;
-    int64_t nt = s.host_n >= 0 ? F64<K>(F_HOST_E, L.lr) : TINF;
+    int64_t nt = (!nohost<K>() && s.host_n >= 0) ? F64<K>(F_HOST_E, L.lr) : TINF;
 #pragma unroll
     for (int q = 0; q < (K & 7); q++) if (s.occ_n[q] >= 0 && s.occ_e[q] < nt) nt = s.occ_e[q];
     if (s.head_e < nt) nt = s.head_e;
@@ -914,7 +919,7 @@ template <int K>
 __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, const Lane &L, Rank<K> &s,
                                            int64_t t) {
     const int R = g.R;                      // (a kernel parameter: no shared-memory load)
-    if (s.host_n >= 0 && F64<K>(F_HOST_E, L.lr) == t) {
+    if (!nohost<K>() && s.host_n >= 0 && F64<K>(F_HOST_E, L.lr) == t) {
         ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, s.host_n, F64<K>(F_HOST_CP, L.lr));
         s.host_n = -1;
     }
@@ -1409,6 +1414,11 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
     // kernel parameter, which `active` tests straight from the constant bank -- a computed RL
     // was spilled and re-loaded from local memory at every step)
     const int RL = CL ? (R - base_r < bd ? R - base_r : bd) : R;
+    if (!lean<K>() && p.retry) {    // second pass after a lean launch: leave at once without work
+        int mine = 0;               // (every CTA of a cluster reads the same points: a uniform exit)
+        for (int q = cid + tid * ncl; q < p.n && !mine; q += bd * ncl) mine = o.status[q] == FL_RETRY;
+        if (!__syncthreads_or(mine)) return;
+    }
 
     // ---- carve shared memory and this cluster's scratch slot ----
     // (the pointer table lives in shared memory: it is block-uniform and would
@@ -1519,6 +1529,7 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
     const int gt = crank * bd + tid, gstride = CS * bd;        // cluster-wide thread index / stride
 
     for (int cfg = cid; cfg < p.n; cfg += ncl) {
+        if (!lean<K>() && p.retry && o.status[cfg] != FL_RETRY) continue;   // (evaluated by the lean pass)
         // ---- cost stage (K1): this point's durations ----
         // (each design-point column is read once: fl_sweep_run may pass them in mapped host memory)
         const int algo = p.algo[cfg], topo = p.topo_kind[cfg];
@@ -1597,6 +1608,12 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
             gsync<CL>();
             continue;
         }
+        if (nohost<K>() && (!g.fold_ok || zero || zdur)) {   // left to the general variant's second pass
+            if (is_leader) o.status[cfg] = FL_RETRY;
+            dirty = false;
+            gsync<CL>();
+            continue;
+        }
         if (++epoch == 64) {       // 6-bit tags wrap: start a fresh accumulator table
             if (!sc.touch_in_smem) zero_cols<CL>(c.cp, (size_t)g.max_nodes, R, RL);
             epoch = 1;
@@ -1606,7 +1623,7 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
         f.step = 0;
         f.epoch = (uint64_t)epoch << 58;
         f.init = 1;
-        f.fold = g.fold_ok && !zero && !zdur;
+        f.fold = nohost<K>() ? 1 : g.fold_ok && !zero && !zdur;   // (lean: points that do not fold were retried)
         f.touch = lean<K>() ? lean_sm<K>() : (bool)sc.touch_in_smem;
         f.acc_sm = lean<K>() ? lean_sm<K>() : (bool)sc.acc_in_smem;
         f.trace = !lean<K>() && o.trace_len != nullptr;
@@ -1739,7 +1756,7 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
             }
             f.step++;
             PROF_MARK(4);                                   // advance
-            if (!zero) {
+            if (nohost<K>() || !zero) {                 // (lean: no serial mode, see above)
                 if (active) {
                     gather_due(g, c, L, s, t);
                     PROF_MARK(5);                           // gather_due
@@ -2005,16 +2022,25 @@ FL_PART_DEF(12)
 
 #if FL_COMMON
 cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t st, int cluster, const DevGraph &g,
-                         const DevPoints &p, const DevOut &o, const DevScratch &sc) {
+                         const DevPoints &p0, const DevOut &o, const DevScratch &sc, int *launches) {
     // variant word: compute streams (1, 2, 4) | 8 when the graphs carry SEND/RECV | plane class << 5
     const int B = K | (g.n_msg > 0 ? 8 : 0);
-    // the lean variant when the run needs none of the branches it drops (bit 7, bit 8)
+    DevPoints p = p0;
+    p.retry = 0;
+    if (launches) *launches = 1;
+    // the lean variant when the run needs none of the branches it drops (bits 7, 8): then the
+    // general variant runs a second pass over the points the lean one left (FL_RETRY), which
+    // exits at once when there are none
     if (FL_LEAN && B == 1 && !o.ev_start && !o.trace_len && g.dur_sm_off && sc.touch_in_smem == sc.acc_in_smem &&
-        (cluster > 1 || !FL_LEAN_FULL || block == g.R)) {
+        g.fold_ok && !g.dyn_host && (cluster > 1 || !FL_LEAN_FULL || block == g.R)) {
         const int pc = cluster > 1 ? 0 : plane_class(block);
-        const int T = B | pc << 5 | 128 | (sc.touch_in_smem ? 256 : 0);
-        if (T == 1 + 128 || (cluster <= 1 && (T == 1 + 64 + 128 + 256 || T == 1 + 32 + 128 + 256)))
-            return launch_sweep_lean1(T, grid, block, smem, st, cluster, g, p, o, sc);
+        const int TL = B | pc << 5 | 128 | (sc.touch_in_smem ? 256 : 0);
+        if (TL == 1 + 128 || (cluster <= 1 && (TL == 1 + 64 + 128 + 256 || TL == 1 + 32 + 128 + 256))) {
+            const cudaError_t e = launch_sweep_lean1(TL, grid, block, smem, st, cluster, g, p, o, sc);
+            if (e != cudaSuccess) return e;
+            p.retry = 1;
+            if (launches) *launches = 2;
+        }
     }
     const int T = B | (cluster > 1 ? 0 : plane_class(block) << 5);
     switch (B) {

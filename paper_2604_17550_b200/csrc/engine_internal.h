@@ -5,6 +5,8 @@
 
 namespace fl {
 
+// internal status of a point the lean variant left to the general one (never returned)
+constexpr int FL_RETRY = 0x7f;
 enum { FL_EDGE_COUNTED = 0, FL_EDGE_SINGLE = 1, FL_EDGE_FIRST = 2, FL_EDGE_MID = 3, FL_EDGE_LAST = 4 };
 
 // Device copy of fl_graph_desc (pointers are device pointers).
@@ -29,6 +31,7 @@ struct DevGraph {
     const int2 *tens_rng;        // [total_tens] {first, end} into tens_cons
     // static-host folding (engine.cu "t = 0 host pops")
     int fold_ok;
+    int dyn_host;                // some HOST node is not a static host (it can run on the host stream)
     int needs_done;              // some tensor's last consumer is only known at run time
     const int32_t *s_nstatic, *trig_off, *static_off, *static_list;
     const int4 *trig;            // {trigger host, node, position in the host's dependents, -}
@@ -55,6 +58,7 @@ struct DevPoints {
     const int32_t *rows, *cols;
     const double *peak_flops, *efficiency;
     int compute_streams;
+    int retry;                   // second pass after a lean launch: only points whose status is FL_RETRY
 };
 
 struct DevOut {
@@ -84,7 +88,7 @@ struct DevScratch {
 };
 
 cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t st, int cluster, const DevGraph &g,
-                         const DevPoints &p, const DevOut &o, const DevScratch &sc);
+                         const DevPoints &p, const DevOut &o, const DevScratch &sc, int *launches);
 cudaError_t sweep_occupancy(int block, size_t smem, int cluster, int *occ);
 cudaError_t sweep_set_smem(size_t smem);
 size_t sweep_shared_header_bytes();

@@ -325,6 +325,34 @@ def test_engine_cluster_spmd_vs_oracle(seed, monkeypatch):
     _check_race(gs, topo, seed, (("ring", 1), ("ring", 2)))
 
 
+@pytest.mark.parametrize("world", [32, 64, 1024])
+def test_engine_lean_pass_leaves_unfoldable_points_to_the_general_one(world):
+    """A batched launch takes the lean variant (no events, every lane a rank, static hosts only)
+    with a second pass of the general one for the points that cannot fold: here every other
+    point re-costs the COMP nodes on a device so fast that their durations round to 0 ns
+    (zero-length nodes at t = 0, serial mode).  Both kinds of point, interleaved in one launch,
+    against the oracle on graphs carrying the re-costed durations."""
+    import copy
+    from oracle.pyoracle import duration_from_flops
+    gs = synth.synth_transformer(synth.PRESETS["tiny"], synth.ParallelConfig(synth.Strategy.DP, world), world)
+    specs = [(f"switch:{world}:{bw}GB:1us", algo) for bw in (25, 400) for algo in ("ring", "tree")]
+    peaks = [1e12, 1e30, 3e14, 1e30]
+    topos = [parse_topology(sp) for sp, _ in specs]
+    pts = E.DesignPoints.from_topologies(topos, [a for _, a in specs])
+    pts.peak_flops = np.array(peaks, np.float64)
+    pts.efficiency = np.full(len(specs), 0.5, np.float64)
+    out = E.simulate_batch(gs, pts)
+    for i, ((spec, algo), topo) in enumerate(zip(specs, topos)):
+        g2 = copy.deepcopy(gs)
+        for g in g2:
+            for n in g.nodes:
+                if n.flops is not None:
+                    n.duration_ns = duration_from_flops(n.flops, peaks[i], 0.5)
+        want = O.sweep_row(g2, topo, algo)
+        assert int(out["status"][i]) == 0
+        assert {k: int(out[k][i]) for k in ROW_KEYS} == want, (spec, algo, peaks[i])
+
+
 # ---- critical-path node trace (SPEC.md:460; the path rule is documented at engine.critical_path_trace) ----
 
 def _trace_both(gs, topo, algo):

@@ -768,7 +768,8 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
     const uint4 xa = rec_a(g, L.nb + x);
     if (g.needs_done) done_ref<K>(c, L, R, x >> 6) |= 1ull << (x & 63);
     F32<K>(Q_DONE, L.lr)++;
-    if (++s.pop_seq > 8191) reinterpret_cast<Shared *>(fl_smem)->seq_ovf = 1;   // 13-bit field of the keys
+    // 13-bit field of the keys (a lean launch has at most 8191 nodes per rank graph: cannot overflow)
+    if (++s.pop_seq > 8191 && !lean<K>()) reinterpret_cast<Shared *>(fl_smem)->seq_ovf = 1;
     F64<K>(F_FIN, L.lr) = t;
     {
         const int64_t cm = F64<K>(F_CPMAX, L.lr);
@@ -1748,7 +1749,8 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
             if (kmin == KINF) break;
             const int64_t t = (int64_t)(kmin >> 14);
             const int rmin = (int)(kmin & 0x3fff);
-            if (t >= TCAP || f.step >= (1ull << 25) - 2) { overflow = true; break; }
+            // (a lean launch has fewer pops per point than the 25-bit step field holds, and every step pops)
+            if (t >= TCAP || (!lean<K>() && f.step >= (1ull << 25) - 2)) { overflow = true; break; }
             PROF_MARK(3);                                   // reservations
             if (t > tcur) {
                 if (active) advance(g, c, L, s, tcur, t);
@@ -2032,7 +2034,8 @@ cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t s
     // general variant runs a second pass over the points the lean one left (FL_RETRY), which
     // exits at once when there are none
     if (FL_LEAN && B == 1 && !o.ev_start && !o.trace_len && g.dur_sm_off && sc.touch_in_smem == sc.acc_in_smem &&
-        g.fold_ok && !g.dyn_host && (cluster > 1 || !FL_LEAN_FULL || block == g.R)) {
+        g.fold_ok && !g.dyn_host && (cluster > 1 || !FL_LEAN_FULL || block == g.R) && g.max_nodes <= 8191 &&
+        (long long)g.R * g.max_nodes < (1 << 25) - 8) {
         const int pc = cluster > 1 ? 0 : plane_class(block);
         const int TL = B | pc << 5 | 128 | (sc.touch_in_smem ? 256 : 0);
         if (TL == 1 + 128 || (cluster <= 1 && (TL == 1 + 64 + 128 + 256 || TL == 1 + 32 + 128 + 256))) {

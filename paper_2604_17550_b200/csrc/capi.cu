@@ -446,6 +446,13 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
         if (!rc) rc = upload(g, tc.data(), tc.size(), &dg.tens_rng);
         if (!rc) rc = upload(g, mfree.data(), mfree.size(), &dg.free_tens);
         if (!rc) rc = upload(g, s_nstatic.data(), s_nstatic.size(), &dg.s_nstatic);
+        // sinks: every node precedes one, so a rank whose sinks all popped popped everything, its
+        // last pop is a sink and so is its largest critical-path finish (engine.cu pop_event, lean)
+        std::vector<int32_t> s_nsink(S, 0);
+        for (int s = 0; s < S; s++)
+            for (int i = d->s_node_off[s]; i < d->s_node_off[s + 1]; i++)
+                s_nsink[s] += d->succ_off[i + 1] == d->succ_off[i] && !is_static[i];
+        if (!rc) rc = upload(g, s_nsink.data(), s_nsink.size(), &dg.s_nsink);
         if (!rc) rc = upload(g, succ_ent.data(), succ_ent.size(), &dg.succ_ent);
         dg.n_acc = n_acc;
         if (!rc) rc = upload(g, mfree_off.data(), mfree_off.size(), &dg.mfree_off);

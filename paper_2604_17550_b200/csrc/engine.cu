@@ -767,11 +767,14 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
     const int R = g.R;                      // (a kernel parameter: no shared-memory load)
     const uint4 xa = rec_a(g, L.nb + x);
     if (g.needs_done) done_ref<K>(c, L, R, x >> 6) |= 1ull << (x & 63);
-    F32<K>(Q_DONE, L.lr)++;
     // 13-bit field of the keys (a lean launch has at most 8191 nodes per rank graph: cannot overflow)
     if (++s.pop_seq > 8191 && !lean<K>()) reinterpret_cast<Shared *>(fl_smem)->seq_ovf = 1;
-    F64<K>(F_FIN, L.lr) = t;
-    {
+    // pops counted (deadlock check), the rank's finish and its largest critical-path finish: a
+    // lean variant updates them at sinks only -- every node precedes a sink of its rank graph,
+    // with a finish no later than the sink's (capi.cu s_nsink)
+    if (!lean<K>() || (xa.y & 0xfffu) == 0) {
+        F32<K>(Q_DONE, L.lr)++;
+        F64<K>(F_FIN, L.lr) = t;
         const int64_t cm = F64<K>(F_CPMAX, L.lr);
         if (fx64 > cm) F64<K>(F_CPMAX, L.lr) = fx64;
     }
@@ -1500,7 +1503,7 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
         const int st = active ? g.rank_struct[L.r] : 0;
         F32<K>(Q_NB, tid) = g.s_node_off[st];
         F32<K>(Q_TB, tid) = g.s_tens_off[st];
-        F32<K>(Q_MYN, tid) = active ? g.s_node_off[st + 1] - g.s_node_off[st] : 0;
+        F32<K>(Q_MYN, tid) = !active ? 0 : lean<K>() ? g.s_nsink[st] : g.s_node_off[st + 1] - g.s_node_off[st];
         L.nb = F32<K>(Q_NB, tid);
         L.tb = F32<K>(Q_TB, tid);
     }
@@ -1694,7 +1697,7 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
                     dispatch(g, c, L, s, f, tr.y, rec_b(g, L.nb + tr.y), 0, tr.z, 0);
                 }
                 if (prev >= 0) start_phase(g, o, c, L, s, f, 0, cfg);
-                F32<K>(Q_DONE, tid) += g.s_nstatic[st];
+                if (!lean<K>()) F32<K>(Q_DONE, tid) += g.s_nstatic[st];   // (lean: sinks only)
                 if (f.trace)        // folded static hosts start and finish at 0 (never popped here)
                     for (int q = g.static_off[st]; q < g.static_off[st + 1]; q++)
                         c.cp[g.static_list[q] * R + L.lr] = (int64_t)f.epoch;

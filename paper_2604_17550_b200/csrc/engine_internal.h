@@ -34,6 +34,7 @@ struct DevGraph {
     int dyn_host;                // some HOST node is not a static host (it can run on the host stream)
     int needs_done;              // some tensor's last consumer is only known at run time
     const int32_t *s_nstatic, *trig_off, *static_off, *static_list;
+    const int32_t *s_nsink;      // per structure: nodes without successors, static hosts excluded
     const int4 *trig;            // {trigger host, node, position in the host's dependents, -}
     unsigned dur_sm_off;         // per-point durations in shared memory at this offset (0: HBM, per CTA)
     const int32_t *s_init_ns_off, *init_ns;   // initial dispatch list without static hosts

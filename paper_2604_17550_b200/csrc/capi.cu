@@ -367,6 +367,18 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
                 }
             }
         }
+        // tracked consumers: the nodes whose completion the run-time free check of a shared
+        // tensor reads (the `done` bitmap); a lean variant's other pops skip the bitmap write
+        std::vector<uint8_t> tracked((size_t)(total > 0 ? total : 1), 0);
+        for (int s = 0; s < S; s++) {
+            const int nb = d->s_node_off[s], tb = d->s_tens_off[s], nt = d->s_tens_off[s + 1] - tb;
+            for (int t = 0; t < nt; t++) {
+                const int c0 = d->tens_cons_off[tb + t], c1 = d->tens_cons_off[tb + t + 1];
+                if (c1 - c0 < 2 || last_cons[tb + t] >= 0) continue;
+                for (int a = c0; a < c1; a++) tracked[nb + d->tens_cons[a]] = 1;
+            }
+        }
+        if (ne_succ >= (1 << 30)) return fail(FL_ERR_CAPACITY, "too many dependency edges");
         int s_of = 0;
         for (int i = 0; i < total; i++) {
             while (s_of + 1 < S && i >= d->s_node_off[s_of + 1]) s_of++;
@@ -394,7 +406,8 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
             for (int q = d->succ_off[i]; q < d->succ_off[i + 1] && q - d->succ_off[i] < 255; q++)
                 if (((uint32_t)succ_ent[q] >> 16 & 7u) == (uint32_t)fl::FL_EDGE_LAST) { lo = q - d->succ_off[i] + 1; break; }
             mfree_off[i] = (int32_t)m0;
-            rec[2 * i] = make_uint4((unsigned)d->succ_off[i], (unsigned)(d->succ_off[i + 1] - d->succ_off[i]) | (nmf << 12) | (lo << 24),
+            rec[2 * i] = make_uint4((unsigned)d->succ_off[i] | ((unsigned)tracked[i] << 31),
+                                    (unsigned)(d->succ_off[i + 1] - d->succ_off[i]) | (nmf << 12) | (lo << 24),
                                     (uint32_t)ufree, (uint32_t)(ufree >> 32));
             rec[2 * i + 1] = make_uint4(meta, (unsigned)(d->node_coll_ord[i] < 0 ? 0 : d->node_coll_ord[i]),
                                         (uint32_t)alloc, (uint32_t)(alloc >> 32));

@@ -143,6 +143,9 @@ __device__ __forceinline__ int64_t coll_time(const DevGraph &g, int i, int algo,
 #ifndef FL_LEAN
 #define FL_LEAN 1               // 0: never launch the lean variant (A/B)
 #endif
+#ifndef FL_LEAN_TRACK
+#define FL_LEAN_TRACK 1         // lean variants set `done` bits for tracked consumers only
+#endif
 #ifndef FL_LEAN_FULL
 #define FL_LEAN_FULL 1          // lean single-CTA variants assume every lane is a rank (block == R)
 #endif
@@ -351,9 +354,10 @@ __device__ __forceinline__ uint64_t cl_step_min(uint64_t v, int &any, Shared &sh
 // Node record built by capi.cu, two 16-byte words per node so that one
 // broadcast load per word serves the 32 ranks of a warp visiting the node (an L1
 // hit: the records of a graph set are a few tens of KB):
-//   a = {succ_off, succ_cnt | mfree_cnt << 12 | (first "last" edge + 1) << 24, ufree_lo, ufree_hi}
+//   a = {succ_off | tracked << 31, succ_cnt | mfree_cnt << 12 | (first "last" edge + 1) << 24, ufree_lo, ufree_hi}
 //       dependents; tensors with more than one consumer it may free (from g.mfree_off);
-//       bytes of tensors it is the only (or statically last) consumer of
+//       bytes of tensors it is the only (or statically last) consumer of; tracked: a consumer of a
+//       tensor whose last consumer is decided at run time
 //   b = {meta, coll_ord, alloc_lo, alloc_hi}        bytes allocated when the node starts
 //   meta bits: 0-3 kind, 4 never-ready (waits on a missing node), 5 static host,
 //   6-15 in-degree from non-static nodes, 16-25 in-degree
@@ -766,7 +770,8 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
                                           const Step &f, int x, int64_t fx64, int64_t t) {
     const int R = g.R;                      // (a kernel parameter: no shared-memory load)
     const uint4 xa = rec_a(g, L.nb + x);
-    if (g.needs_done) done_ref<K>(c, L, R, x >> 6) |= 1ull << (x & 63);
+    // the `done` bit of a consumer whose completion a run-time free check reads (lean: only those)
+    if ((lean<K>() && FL_LEAN_TRACK) ? (xa.x >> 31) != 0 : g.needs_done) done_ref<K>(c, L, R, x >> 6) |= 1ull << (x & 63);
     // 13-bit field of the keys (a lean launch has at most 8191 nodes per rank graph: cannot overflow)
     if (++s.pop_seq > 8191 && !lean<K>()) reinterpret_cast<Shared *>(fl_smem)->seq_ovf = 1;
     // pops counted (deadlock check), the rank's finish and its largest critical-path finish: a
@@ -800,10 +805,11 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
     const int32_t *sl = g.succ_ent;
     // the first "last" edge's accumulator read goes out before the other edges are processed
     const uint32_t lo = xa.y >> 24;
-    const uint32_t qlast = lo && f.fold ? xa.x + lo - 1 : 0xffffffffu;
+    const uint32_t q0 = xa.x & 0x7fffffffu;  // first successor entry
+    const uint32_t qlast = lo && f.fold ? q0 + lo - 1 : 0xffffffffu;
     uint64_t alast = 0;
     if (qlast != 0xffffffffu) alast = acc_read(c, f, (int)((uint32_t)sl[qlast] >> 19) * R + L.lr);
-    for (uint32_t q = xa.x, qe = xa.x + (xa.y & 0xfffu); q < qe; q++, seq++) {
+    for (uint32_t q = q0, qe = q0 + (xa.y & 0xfffu); q < qe; q++, seq++) {
         const uint32_t ent = (uint32_t)sl[q];
         const int d = (int)(ent & 0xffffu);
         const int cls = f.fold ? (int)((ent >> 16) & 7u) : FL_EDGE_COUNTED;

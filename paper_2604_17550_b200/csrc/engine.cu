@@ -187,6 +187,8 @@ struct Shared {
     int ncomp;
     int nmcomp;
     int pcols;                      // this design point's mesh columns
+    int have_dur, dev_zdur;         // the previous point's device: durations in place, a zero-length node
+    double dev_pk, dev_ef;
     double mbeta;                   // this design point's 1e9 / bw and latency (message wire times)
     int64_t mlat;
     // cluster variant: per-CTA partial results, written by every CTA of the cluster (DSMEM)
@@ -1516,7 +1518,9 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
 
     int par = 0;
     unsigned xk = 0;                // cluster step exchanges done (cl_step_min)
-    if (tid == 0) { sh.ncomp = 0; sh.nmcomp = 0; sh.cflag = 0; }
+    // (the previous point's device -- its durations are reused when unchanged -- is kept in shared
+    // memory, sh.dev_*: four registers fewer across the event loop)
+    if (tid == 0) { sh.ncomp = 0; sh.nmcomp = 0; sh.cflag = 0; sh.have_dur = 0; }
     if (CL && tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sh.xmbar[0])) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sh.xmbar[1])) : "memory");
@@ -1533,9 +1537,6 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
     if (!sc.touch_in_smem) zero_cols<CL>(c.cp, (size_t)g.max_nodes, R, RL);
     gsync<CL>();
     unsigned epoch = 0;
-    bool have_dur = false;          // durations of the previous point's device, reused when unchanged
-    double dev_pk = 0.0, dev_ef = 0.0;
-    int dev_zdur = 0;
     const int gt = crank * bd + tid, gstride = CS * bd;        // cluster-wide thread index / stride
 
     for (int cfg = cid; cfg < p.n; cfg += ncl) {
@@ -1579,11 +1580,8 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
         }
         const bool recost = p.peak_flops != nullptr;
         const double pk = recost ? p.peak_flops[cfg] : 0.0, ef = recost ? p.efficiency[cfg] : 0.0;
-        const bool same_dev = have_dur && pk == dev_pk && ef == dev_ef;   // durations already in place
-        have_dur = true;
-        dev_pk = pk;
-        dev_ef = ef;
-        int zdur = same_dev ? dev_zdur : 0;   // a zero-duration COMP or non-static HOST could complete at t = 0
+        const bool same_dev = sh.have_dur && pk == sh.dev_pk && ef == sh.dev_ef;   // durations already in place
+        int zdur = same_dev ? sh.dev_zdur : 0;   // a zero-duration COMP or non-static HOST could complete at t = 0
         if (!same_dev) for (int n = tid; n < g.total_nodes; n += bd) {
             int64_t d = g.node_dur[n];
             if (recost && g.node_flops[n] >= 0) d = flops_to_ns(g.node_flops[n], pk, ef);
@@ -1610,7 +1608,7 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
         if (cap_bad) bad = 2;
         zero = gor<CL>(zero, sh, par);
         zdur = gor<CL>(zdur, sh, par);
-        dev_zdur = zdur;
+        if (tid == 0) { sh.have_dur = 1; sh.dev_pk = pk; sh.dev_ef = ef; sh.dev_zdur = zdur; }   // (read after barriers)
         if (bad) {
             if (is_leader) o.status[cfg] = bad == 2 ? FL_ERR_CAPACITY : FL_ERR_UNSUPPORTED_ALGO;
             if (is_leader && o.trace_len) o.trace_len[cfg] = 0;

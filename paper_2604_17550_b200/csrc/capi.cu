@@ -545,9 +545,11 @@ int create(const fl_graph_desc *d, int32_t device, fl_graph *g) {
     const size_t budget = (size_t)optin - 1024;   // the kernel's static shared memory (Ctx) comes off the top
     const size_t sbits = (size_t)dg.max_words * B * 8;   // a bitmap over this CTA's ranks
     sc.inst_in_smem = CS == 1 && sm + inst_bytes <= budget;   // clusters share instance state in HBM
-    if (sc.inst_in_smem) { sc.sm_off_inst = (unsigned)sm; sm = align_up(sm + inst_bytes, 16); }
-    sc.dur_in_smem = sm + dur_bytes <= budget;
+    // (the durations, when they fit beside the instance table, come first: their offset is then the
+    // end of the planes, a compile-time constant of each kernel variant -- engine.cu dur_off)
+    sc.dur_in_smem = align_up(sm + (sc.inst_in_smem ? inst_bytes : 0), 16) + dur_bytes <= budget;
     if (sc.dur_in_smem) { sc.sm_off_dur = (unsigned)sm; sm = align_up(sm + dur_bytes, 16); }
+    if (sc.inst_in_smem) { sc.sm_off_inst = (unsigned)sm; sm = align_up(sm + inst_bytes, 16); }
     dg.dur_sm_off = sc.dur_in_smem ? sc.sm_off_dur : 0;
     sc.done_in_smem = dg.needs_done && sm + sbits <= budget;
     if (sc.done_in_smem) { sc.sm_off_done = (unsigned)sm; sm = align_up(sm + sbits, 16); }

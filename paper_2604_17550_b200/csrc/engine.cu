@@ -505,9 +505,14 @@ template <int K> __host__ __device__ constexpr bool lean_sm() { return (K & 256)
 // zero-length node, engine.cu "t = 0 host pops") is marked FL_RETRY and evaluated by the
 // general variant in a second pass (launch_sweep).
 template <int K> __host__ __device__ constexpr bool nohost() { return lean<K>(); }
+// where capi.cu puts the durations when they are in shared memory: right after the per-rank
+// planes (a lean launch checks g.dur_sm_off against it)
+template <int K> __host__ __device__ constexpr unsigned dur_off() {
+    return (SM_HDR + (unsigned)plane_lanes<K>() * (8u * F_N64 + 4u * Q_ALL + ((K & 8) ? 8u * MF_N64 + 4u : 0u)) + 15u) / 16u * 16u;
+}
 template <int K>
 __device__ __forceinline__ int64_t dur_of(const DevGraph &g, const Ctx &c, int n) {
-    if constexpr (lean<K>()) return reinterpret_cast<const int64_t *>(fl_smem + g.dur_sm_off)[n];
+    if constexpr (lean<K>()) return reinterpret_cast<const int64_t *>(fl_smem + dur_off<K>())[n];
     else return dur_of(g, c, n);
 }
 
@@ -2045,7 +2050,10 @@ cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t s
         (long long)g.R * g.max_nodes < (1 << 25) - 8) {
         const int pc = cluster > 1 ? 0 : plane_class(block);
         const int TL = B | pc << 5 | 128 | (sc.touch_in_smem ? 256 : 0);
-        if (TL == 1 + 128 || (cluster <= 1 && (TL == 1 + 64 + 128 + 256 || TL == 1 + 32 + 128 + 256))) {
+        const unsigned doff = TL == 1 + 128 ? dur_off<1 + 128>() : TL == 1 + 64 + 128 + 256 ? dur_off<1 + 64 + 128 + 256>()
+                                                                                           : dur_off<1 + 32 + 128 + 256>();
+        if ((TL == 1 + 128 || (cluster <= 1 && (TL == 1 + 64 + 128 + 256 || TL == 1 + 32 + 128 + 256))) &&
+            g.dur_sm_off == doff) {
             const cudaError_t e = launch_sweep_lean1(TL, grid, block, smem, st, cluster, g, p, o, sc);
             if (e != cudaSuccess) return e;
             p.retry = 1;

@@ -1,6 +1,6 @@
 """Small engine runs for compute-sanitizer (memcheck / racecheck / synccheck).
 
-    compute-sanitizer --tool memcheck python scripts/sanitize.py [analytical|p2p|cluster|cluster9|cluster_p2p]
+    compute-sanitizer --tool memcheck python scripts/sanitize.py [analytical|p2p|cluster|cluster9|cluster_p2p|lean]
 
 Every case is also checked against the CPU oracle, so a run that the sanitizer
 passes is a correct one.  Sizes are kept small: racecheck replays shared-memory
@@ -53,6 +53,17 @@ def main(case: str) -> None:
     elif case == "cluster":
         gs = synth.synth_transformer(synth.PRESETS["tiny"], synth.ParallelConfig(synth.Strategy.DP, 2048), 2048)
         check(gs, [("switch:2048:100GB:1us", "ring"), ("mesh:32x64:400GB:100ns", "mesh-hier")])
+    elif case == "lean":             # lean variants (1024 lanes, 64 lanes) and the second pass
+        import numpy as np
+        for deg in (1024, 64):
+            gs = synth.synth_transformer(synth.PRESETS["tiny"], synth.ParallelConfig(synth.Strategy.FSDP, deg), deg)
+            check(gs, [(f"switch:{deg}:25GB:2us", "ring"), (f"switch:{deg}:400GB:1us", "ring")])
+            topos = [parse_topology(f"switch:{deg}:25GB:2us")] * 2
+            pts = E.DesignPoints.from_topologies(topos, ["ring", "ring"])
+            pts.peak_flops = np.array([1e12, 1e30])      # the second point cannot fold: second pass
+            pts.efficiency = np.array([0.5, 0.5])
+            out = E.simulate_batch(gs, pts)
+            assert (out["status"] == 0).all(), out["status"]
     elif case == "cluster9":          # 8192 ranks: 9 CTAs of 911 ranks (blocks of 928 threads)
         gs = synth.synth_transformer(synth.PRESETS["tiny"], synth.ParallelConfig(synth.Strategy.DP, 8192), 8192)
         check(gs, [("switch:8192:100GB:1us", "ring"), ("mesh:64x128:400GB:100ns", "mesh-hier")])

@@ -53,6 +53,7 @@ struct fl_graph {
     size_t stage_bytes = 0;
     unsigned char *hstage = nullptr;
     size_t hstage_bytes = 0;
+    unsigned char *hstage_dev = nullptr;   // its device alias (mapped pinned memory)
     cudaStream_t stream = nullptr;  // fl_sweep_run's own non-blocking stream (not the legacy one)
     int grid_cap = 0;
     int links_sm_cap = 0;           // link-table capacity reserved in shared memory
@@ -743,7 +744,8 @@ int fl_sweep_run_device(fl_graph *g, const fl_points *dev_points, fl_outputs *de
 
 int fl_sweep_run(fl_graph *g, const fl_points *hp, fl_outputs *ho) {
     if (!g || !hp || !ho) return fail(FL_ERR_INVALID, "null argument");
-    CK(cudaSetDevice(g->device));
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != g->device) CK(cudaSetDevice(g->device));
     const size_t n = (size_t)hp->n_points;
     if (n == 0) return FL_OK;
     if (!g->stream) CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
@@ -792,6 +794,9 @@ int fl_sweep_run(fl_graph *g, const fl_points *hp, fl_outputs *ho) {
         g->hstage_bytes = 0;
         CK(cudaHostAlloc(&g->hstage, small_end, cudaHostAllocMapped));
         g->hstage_bytes = small_end;
+        void *dh = nullptr;
+        CK(cudaHostGetDevicePointer(&dh, g->hstage, 0));
+        g->hstage_dev = static_cast<unsigned char *>(dh);
     }
     unsigned char *S = g->stage, *H = g->hstage;
     for (auto &p : in)
@@ -802,9 +807,7 @@ int fl_sweep_run(fl_graph *g, const fl_points *hp, fl_outputs *ho) {
     const bool zc = n <= (size_t)g->grid_cap;
     unsigned char *small = S;                      // where the inputs and per-point outputs live
     if (zc) {
-        void *dh = nullptr;
-        CK(cudaHostGetDevicePointer(&dh, H, 0));
-        small = static_cast<unsigned char *>(dh);
+        small = g->hstage_dev;
     } else {
         CK(cudaMemcpyAsync(S, H, in_bytes, cudaMemcpyHostToDevice, st));
     }

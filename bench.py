@@ -169,7 +169,7 @@ WORKLOAD_TEXT = {
           "8 latency [100ns,10us]",
     "c4": "BASELINE config 4 (SURVEY.md 8d): llama-70b-like at 8192 ranks, 16384 design points = "
           "{dp:8192 switch ring, dp:8192 switch tree, dp:8192 mesh:64x128 mesh-hier, fsdp:8192 mesh:64x128 "
-          "mesh-hier} x 64 bw [10GB/s,1.8TB/s] x 64 latency [100ns,20us]; clusters of 8 CTAs per design point",
+          "mesh-hier} x 64 bw [10GB/s,1.8TB/s] x 64 latency [100ns,20us]; a design point spans a cluster of 9 CTAs (911 ranks each)",
     "c2x": "BASELINE config 2 in EXPANDED comm mode (SURVEY.md 8f row 1): GPT-2 small dp:64, every all-reduce "
            "lowered to its ring / tree SEND+RECV plan on switch:64 links, 256 design points = {ring, tree} x 16 bw "
            "[10GB/s,1.8TB/s] x 8 latency [100ns,10us]",

@@ -136,7 +136,7 @@ def c4_workload() -> Workload:
     dp:8192 + mesh:64x128 mesh-hier, fsdp:8192 + mesh:64x128 mesh-hier} x 64
     bandwidths in [10 GB/s, 1.8 TB/s] x 64 latencies in [100 ns, 20 us].
     Two graph families (dp: 1760 nodes per rank, fsdp: 2080), one engine
-    launch each; a design point spans a cluster of 8 CTAs.  The pipeline /
+    launch each; a design point spans a thread-block cluster (9 CTAs on B200).  The pipeline /
     3-D part of the BASELINE wording is not expressible in the reference
     (synth.py:172-181)."""
     bws, lats = log_grid(10e9, 1.8e12, 64), latency_grid(100, 20000, 64)

@@ -70,7 +70,7 @@ def test_engine_matches_reference_on_70b_family():
 
 @pytest.mark.gpu
 def test_engine_c4_grid_rows_at_8192_ranks():
-    """The C4 grid's own design points at 8192 ranks (clusters of 8 CTAs), both families."""
+    """The C4 grid's own design points at 8192 ranks (9-CTA clusters), both families."""
     from paper_2604_17550_b200 import engine as E
     from paper_2604_17550_b200 import sweep as S
     w = S.c4_workload()

@@ -287,7 +287,7 @@ def test_engine_cluster_fsdp2048_vs_oracle(spec, algo):
 
 
 def test_engine_cluster_8192_ranks_vs_oracle():
-    """BASELINE config-4 scale: 8192 ranks = a cluster of 8 CTAs per design point."""
+    """BASELINE config-4 scale: 8192 ranks = a cluster of 9 CTAs per design point."""
     gs = synth.synth_transformer(synth.PRESETS["tiny"], synth.ParallelConfig(synth.Strategy.DP, 8192), 8192)
     specs = [("switch:8192:100GB:1us", "ring"), ("switch:8192:25GB:5us", "tree"), ("mesh:64x128:400GB:100ns", "mesh-hier")]
     out = _batch(gs, specs)

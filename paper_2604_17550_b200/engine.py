@@ -134,7 +134,8 @@ class DesignPoints:
     def raw(self):
         """The fl_points struct of these columns (validated; rebuilt only when a column object or
         the stream count changed -- in-place edits of the arrays need no rebuild)."""
-        key = (self.compute_streams, *(id(getattr(self, f)) for f, _ in _POINT_COLS))
+        key = (self.compute_streams, id(self.algo), id(self.topo_kind), id(self.bw), id(self.latency),
+               id(self.rows), id(self.cols), id(self.peak_flops), id(self.efficiency))   # (= _POINT_COLS)
         cached = self.__dict__.get("_raw")
         if cached is None or cached[0] != key:
             n = len(self)
@@ -235,6 +236,18 @@ class Engine:
         n = len(pts)
         R = self.gs.n_ranks
         out = {"status": np.empty(n, np.int32), "rows": np.empty((n, 6), np.int64)}
+        if not (links or rank_stats or events or trace_cap > 0):
+            # the sweep's common case, on the end-to-end path of every call: a cached fl_outputs
+            # with only the two row pointers set (numpy's .ctypes costs ~2 us per array)
+            o = self.__dict__.get("_out_rows")
+            if o is None:
+                o = self.__dict__["_out_rows"] = _native.OutputsRaw(None, None, None, None, None, None, 0, None, None, 0)
+            o.status = C.addressof(C.c_char.from_buffer(out["status"]))
+            o.rows = C.addressof(C.c_char.from_buffer(out["rows"]))
+            rc = _native.lib().fl_sweep_run(self._h, C.addressof(pts.raw()), C.addressof(o))
+            if rc:
+                raise EngineError(f"fl_sweep_run: {_native.last_error()} (status {rc})")
+            return out
         cap = self.link_cap(pts) if links else 0
         if links:
             out["link_busy"] = np.full((n, max(cap, 1)), -1, np.int64)

@@ -143,6 +143,9 @@ __device__ __forceinline__ int64_t coll_time(const DevGraph &g, int i, int algo,
 #ifndef FL_LEAN
 #define FL_LEAN 1               // 0: never launch the lean variant (A/B)
 #endif
+#ifndef FL_LEAN_STEP
+#define FL_LEAN_STEP 1          // lean: no due-set test in next_time, no t > tcur test per step
+#endif
 #ifndef FL_LEAN_TRACK
 #define FL_LEAN_TRACK 1         // lean variants set `done` bits for tracked consumers only
 #endif
@@ -919,7 +922,8 @@ __device__ __forceinline__ void refresh_ring(const Ctx &c, const Lane &L, Rank<K
 template <int K>
 __device__ __forceinline__ int64_t next_time(const DevGraph &g, const Ctx &c, const Lane &L, const Rank<K> &s,
                                              int64_t tcur) {
-    if (s.due.head >= 0) return tcur;
+    // (a lean point has no zero-length node: the due set is always drained at the top of a step)
+    if (!(lean<K>() && FL_LEAN_STEP) && s.due.head >= 0) return tcur;
     int64_t nt = (!nohost<K>() && s.host_n >= 0) ? F64<K>(F_HOST_E, L.lr) : TINF;
 #pragma unroll
     for (int q = 0; q < (K & 7); q++) if (s.occ_n[q] >= 0 && s.occ_e[q] < nt) nt = s.occ_e[q];
@@ -1764,7 +1768,8 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
             // (a lean launch has fewer pops per point than the 25-bit step field holds, and every step pops)
             if (t >= TCAP || (!lean<K>() && f.step >= (1ull << 25) - 2)) { overflow = true; break; }
             PROF_MARK(3);                                   // reservations
-            if (t > tcur) {
+            // (a lean point has no zero-length node, so every step lies past the last one)
+            if ((lean<K>() && FL_LEAN_STEP) || t > tcur) {
                 if (active) advance(g, c, L, s, tcur, t);
                 tcur = t;
             }

@@ -633,7 +633,9 @@ int ensure_scratch(fl_graph *g, int grid) {
     return FL_OK;
 }
 
-int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stream, int *launches = nullptr) {
+// defer / deferred: fl::launch_sweep's deferred second pass; retry_only: launch that pass
+int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stream, int *launches = nullptr,
+           bool defer = false, bool *deferred = nullptr, bool retry_only = false) {
     if (launches) *launches = 0;
     if (pts->n_points <= 0) return FL_OK;
     int cs = pts->compute_streams;
@@ -652,7 +654,7 @@ int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stre
     dp.peak_flops = pts->peak_flops;
     dp.efficiency = pts->efficiency;
     dp.compute_streams = cs;
-    dp.retry = 0;
+    dp.retry = retry_only ? 1 : 0;
     fl::DevScratch sc = g->sc;
     sc.links_in_smem = g->links_sm_cap > 0 && sc.link_cap <= g->links_sm_cap;
     fl::DevOut dout;
@@ -668,7 +670,7 @@ int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stre
     dout.trace_cap = out->trace ? out->trace_cap : 0;
     int nl = 0;
     CK(fl::launch_sweep(cs == 3 ? 4 : cs, grid * g->cluster, g->block, g->smem, stream, g->cluster, g->dg, dp, dout,
-                        sc, &nl));
+                        sc, &nl, defer, deferred));
     if (launches) *launches = nl;
     return FL_OK;
 }
@@ -831,18 +833,35 @@ int fl_sweep_run(fl_graph *g, const fl_points *hp, fl_outputs *ho) {
     dout.trace = TC ? reinterpret_cast<int64_t *>(S + o_tr) : nullptr;
     dout.trace_len = ho->trace_len ? reinterpret_cast<int32_t *>(small + o_tl) : nullptr;
     dout.trace_cap = (int32_t)TC;
-    int rc = launch(g, &dp, &dout, st);
+    // The statuses come back to the host anyway, so the lean variant's second pass (the points
+    // it left as FL_RETRY: zero-length nodes, engine.cu "Lean variants") is launched only when
+    // one of them says so -- for most sweeps never, saving a launch and a kernel on the call.
+    bool deferred = false;
+    int rc = launch(g, &dp, &dout, st, nullptr, true, &deferred);
     if (rc) return rc;
-    if (!zc) CK(cudaMemcpyAsync(H + o_status, S + o_status, small_end - o_status, cudaMemcpyDeviceToHost, st));
-    if (ho->rank_stats) CK(cudaMemcpyAsync(ho->rank_stats, dout.rank_stats, 40 * n * R, cudaMemcpyDeviceToHost, st));
-    if (LC) CK(cudaMemcpyAsync(ho->link_busy, dout.link_busy, 8 * n * LC, cudaMemcpyDeviceToHost, st));
-    if (TC) CK(cudaMemcpyAsync(ho->trace, dout.trace, 8 * n * TC, cudaMemcpyDeviceToHost, st));
-    if (ho->ev_start) {
-        CK(cudaMemcpyAsync(ho->ev_start, dout.ev_start, 8 * n * R * MN, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(ho->ev_end, dout.ev_end, 8 * n * R * MN, cudaMemcpyDeviceToHost, st));
+    auto copy_back = [&]() -> int {
+        if (!zc) CK(cudaMemcpyAsync(H + o_status, S + o_status, small_end - o_status, cudaMemcpyDeviceToHost, st));
+        if (ho->rank_stats) CK(cudaMemcpyAsync(ho->rank_stats, dout.rank_stats, 40 * n * R, cudaMemcpyDeviceToHost, st));
+        if (LC) CK(cudaMemcpyAsync(ho->link_busy, dout.link_busy, 8 * n * LC, cudaMemcpyDeviceToHost, st));
+        if (TC) CK(cudaMemcpyAsync(ho->trace, dout.trace, 8 * n * TC, cudaMemcpyDeviceToHost, st));
+        if (ho->ev_start) {
+            CK(cudaMemcpyAsync(ho->ev_start, dout.ev_start, 8 * n * R * MN, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(ho->ev_end, dout.ev_end, 8 * n * R * MN, cudaMemcpyDeviceToHost, st));
+        }
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return fail(FL_ERR_CUDA, std::string("engine kernel: ") + cudaGetErrorString(e));
+        return FL_OK;
+    };
+    if ((rc = copy_back())) return rc;
+    if (deferred) {
+        const int32_t *hs = reinterpret_cast<const int32_t *>(H + o_status);
+        bool any = false;
+        for (size_t i = 0; i < n && !any; i++) any = hs[i] == fl::FL_RETRY;
+        if (any) {
+            if ((rc = launch(g, &dp, &dout, st, nullptr, false, nullptr, true))) return rc;
+            if ((rc = copy_back())) return rc;
+        }
     }
-    cudaError_t e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return fail(FL_ERR_CUDA, std::string("engine kernel: ") + cudaGetErrorString(e));
     memcpy(ho->status, H + o_status, 4 * n);
     memcpy(ho->rows, H + o_rows, 48 * n);
     if (ho->trace_len) memcpy(ho->trace_len, H + o_tl, 4 * n);

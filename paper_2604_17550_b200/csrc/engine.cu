@@ -2041,16 +2041,17 @@ FL_PART_DEF(12)
 
 #if FL_COMMON
 cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t st, int cluster, const DevGraph &g,
-                         const DevPoints &p0, const DevOut &o, const DevScratch &sc, int *launches) {
+                         const DevPoints &p0, const DevOut &o, const DevScratch &sc, int *launches,
+                         bool defer_retry, bool *deferred) {
     // variant word: compute streams (1, 2, 4) | 8 when the graphs carry SEND/RECV | plane class << 5
     const int B = K | (g.n_msg > 0 ? 8 : 0);
     DevPoints p = p0;
-    p.retry = 0;
     if (launches) *launches = 1;
+    if (deferred) *deferred = false;
     // the lean variant when the run needs none of the branches it drops (bits 7, 8): then the
     // general variant runs a second pass over the points the lean one left (FL_RETRY), which
     // exits at once when there are none
-    if (FL_LEAN && B == 1 && !o.ev_start && !o.trace_len && g.dur_sm_off && sc.touch_in_smem == sc.acc_in_smem &&
+    if (!p0.retry && FL_LEAN && B == 1 && !o.ev_start && !o.trace_len && g.dur_sm_off && sc.touch_in_smem == sc.acc_in_smem &&
         g.fold_ok && !g.dyn_host && (cluster > 1 || !FL_LEAN_FULL || block == g.R) && g.max_nodes <= 8191 &&
         (long long)g.R * g.max_nodes < (1 << 25) - 8) {
         const int pc = cluster > 1 ? 0 : plane_class(block);
@@ -2060,7 +2061,10 @@ cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t s
         if ((TL == 1 + 128 || (cluster <= 1 && (TL == 1 + 64 + 128 + 256 || TL == 1 + 32 + 128 + 256))) &&
             g.dur_sm_off == doff) {
             const cudaError_t e = launch_sweep_lean1(TL, grid, block, smem, st, cluster, g, p, o, sc);
-            if (e != cudaSuccess) return e;
+            if (e != cudaSuccess || defer_retry) {
+                if (deferred) *deferred = e == cudaSuccess;
+                return e;
+            }
             p.retry = 1;
             if (launches) *launches = 2;
         }

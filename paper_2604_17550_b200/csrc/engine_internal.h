@@ -88,8 +88,12 @@ struct DevScratch {
     int links_in_smem;           // the link table is in the (lead) CTA's shared memory (per launch: it grows)
 };
 
+// p.retry = 1: only the general variant's second pass (points whose status is FL_RETRY).
+// defer_retry: after a lean launch, leave the second pass to the caller (*deferred = true),
+// which launches it with p.retry = 1 only if a status it read back is FL_RETRY.
 cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t st, int cluster, const DevGraph &g,
-                         const DevPoints &p, const DevOut &o, const DevScratch &sc, int *launches);
+                         const DevPoints &p, const DevOut &o, const DevScratch &sc, int *launches,
+                         bool defer_retry = false, bool *deferred = nullptr);
 cudaError_t sweep_occupancy(int block, size_t smem, int cluster, int *occ);
 cudaError_t sweep_set_smem(size_t smem);
 size_t sweep_shared_header_bytes();

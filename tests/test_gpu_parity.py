@@ -325,22 +325,25 @@ def test_engine_cluster_spmd_vs_oracle(seed, monkeypatch):
     _check_race(gs, topo, seed, (("ring", 1), ("ring", 2)))
 
 
-@pytest.mark.parametrize("world", [32, 64, 1024])
-def test_engine_lean_pass_leaves_unfoldable_points_to_the_general_one(world):
+@pytest.mark.parametrize("world,reps", [(32, 1), (64, 1), (1024, 1), (64, 300), (1024, 100)])
+def test_engine_lean_pass_leaves_unfoldable_points_to_the_general_one(world, reps):
     """A batched launch takes the lean variant (no events, every lane a rank, static hosts only)
     with a second pass of the general one for the points that cannot fold: here every other
     point re-costs the COMP nodes on a device so fast that their durations round to 0 ns
     (zero-length nodes at t = 0, serial mode).  Both kinds of point, interleaved in one launch,
-    against the oracle on graphs carrying the re-costed durations."""
+    against the oracle on graphs carrying the re-costed durations.  fl_sweep_run launches the
+    second pass only after reading a FL_RETRY status back; `reps` > 1 repeats the four points
+    past the resident grid, so the statuses come back through the staging copy instead of
+    mapped memory."""
     import copy
     from oracle.pyoracle import duration_from_flops
     gs = synth.synth_transformer(synth.PRESETS["tiny"], synth.ParallelConfig(synth.Strategy.DP, world), world)
     specs = [(f"switch:{world}:{bw}GB:1us", algo) for bw in (25, 400) for algo in ("ring", "tree")]
     peaks = [1e12, 1e30, 3e14, 1e30]
     topos = [parse_topology(sp) for sp, _ in specs]
-    pts = E.DesignPoints.from_topologies(topos, [a for _, a in specs])
-    pts.peak_flops = np.array(peaks, np.float64)
-    pts.efficiency = np.full(len(specs), 0.5, np.float64)
+    pts = E.DesignPoints.from_topologies(topos * reps, [a for _, a in specs] * reps)
+    pts.peak_flops = np.array(peaks * reps, np.float64)
+    pts.efficiency = np.full(len(specs) * reps, 0.5, np.float64)
     out = E.simulate_batch(gs, pts)
     for i, ((spec, algo), topo) in enumerate(zip(specs, topos)):
         g2 = copy.deepcopy(gs)
@@ -349,8 +352,9 @@ def test_engine_lean_pass_leaves_unfoldable_points_to_the_general_one(world):
                 if n.flops is not None:
                     n.duration_ns = duration_from_flops(n.flops, peaks[i], 0.5)
         want = O.sweep_row(g2, topo, algo)
-        assert int(out["status"][i]) == 0
-        assert {k: int(out[k][i]) for k in ROW_KEYS} == want, (spec, algo, peaks[i])
+        for j in range(i, len(specs) * reps, len(specs)):
+            assert int(out["status"][j]) == 0
+            assert {k: int(out[k][j]) for k in ROW_KEYS} == want, (spec, algo, peaks[i], j)
 
 
 # ---- critical-path node trace (the path rule is documented at engine.critical_path_trace) ----

@@ -130,7 +130,7 @@ typedef struct {
     const int32_t *rows, *cols;       /* mesh shape (MESH_HIER) */
     const double *peak_flops;         /* NULL: keep node_dur; else re-cost COMP from flops */
     const double *efficiency;
-    int32_t compute_streams;          /* SimOptions.compute_streams (1, 2 or 4) */
+    int32_t compute_streams;          /* SimOptions.compute_streams (1..8) */
 } fl_points;
 
 /* Results, one row per point: makespan, critical path, max compute busy,

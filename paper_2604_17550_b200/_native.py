@@ -31,7 +31,7 @@ NVCC_FLAGS = [
 ]
 # engine.cu is compiled once per kernel-variant group (compute streams | 8 with messages,
 # engine.cu FL_BASE) so the groups build in parallel
-ENGINE_PARTS = (1, 2, 4, 9, 10, 12)
+ENGINE_PARTS = (1, 2, 4, 9, 10, 12, 512, 520)
 
 
 def nvcc() -> str:

@@ -639,7 +639,7 @@ int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stre
     if (launches) *launches = 0;
     if (pts->n_points <= 0) return FL_OK;
     int cs = pts->compute_streams;
-    if (cs < 1 || cs > 4) return fail(FL_ERR_CAPACITY, "compute_streams must be 1..4 in this build");
+    if (cs < 1 || cs > 8) return fail(FL_ERR_CAPACITY, "compute_streams must be 1..8 in this build");
     int grid = pts->n_points < g->grid_cap ? pts->n_points : g->grid_cap;   // design points in flight
     int rc = ensure_scratch(g, grid);
     if (rc) return rc;
@@ -669,7 +669,9 @@ int launch(fl_graph *g, const fl_points *pts, fl_outputs *out, cudaStream_t stre
     dout.trace_len = out->trace_len;
     dout.trace_cap = out->trace ? out->trace_cap : 0;
     int nl = 0;
-    CK(fl::launch_sweep(cs == 3 ? 4 : cs, grid * g->cluster, g->block, g->smem, stream, g->cluster, g->dg, dp, dout,
+    // kernel variants exist for 1, 2, 4 and 8 streams: a count in between runs on the next one
+    // up with the extra slots never free (simulator.py:250-257 picks the lowest free stream)
+    CK(fl::launch_sweep(cs <= 2 ? cs : cs <= 4 ? 4 : 512, grid * g->cluster, g->block, g->smem, stream, g->cluster, g->dg, dp, dout,
                         sc, &nl, defer, deferred));
     if (launches) *launches = nl;
     return FL_OK;

@@ -202,7 +202,15 @@ struct Shared {
 
 // Warp min of keys (time << 14 | rank).  Ranks step in lockstep most of the
 // time: when every lane holds the same time, lane 0 (lowest rank) has the min.
+#ifndef FL_REDUX
+#define FL_REDUX 0
+#endif
 __device__ __forceinline__ uint64_t warp_min_key(uint64_t v) {
+    if (FL_REDUX) {                 // two REDUX (64-bit min = min of the high words, then of the low)
+        const unsigned hi = (unsigned)(v >> 32), mh = __reduce_min_sync(FULL, hi);
+        const unsigned ml = __reduce_min_sync(FULL, hi == mh ? (unsigned)v : 0xffffffffu);
+        return ((uint64_t)mh << 32) | ml;
+    }
     const uint64_t v0 = __shfl_sync(FULL, v, 0);
     if (__all_sync(FULL, (v >> 14) == (v0 >> 14))) return v0;
 #pragma unroll
@@ -500,6 +508,9 @@ __device__ __forceinline__ int64_t dur_of(const DevGraph &g, const Ctx &c, int n
 // trace, no shared-memory first-dependency bitmap or slot table, and has the durations in shared
 // memory -- those branches compile away (fewer live values under the 64-register cap).
 template <int K> __host__ __device__ constexpr bool lean() { return (K & 128) != 0; }
+// Bits 0-2: compute streams (1, 2 or 4); bit 9 instead: 8 compute streams (5-8 requested, the
+// slots above the count never free)
+template <int K> __host__ __device__ constexpr int nstreams() { return (K & 512) ? 8 : (K & 7); }
 // bit 8 (lean variants only): the first-dependency bitmap and the slot table are both in shared
 // memory (small design points) -- else both are not
 template <int K> __host__ __device__ constexpr bool lean_sm() { return (K & 256) != 0; }
@@ -561,14 +572,14 @@ __device__ __forceinline__ int ms_inc(int cnt) { return (cnt + (cnt < MS_SAT)) <
 template <int K>
 struct Rank {
     MinSet due, rc, rh;             // due events at t / ready compute nodes / ready host nodes
-    int64_t slot[K & 7];            // compute stream free-at times (K > 1 only: with one stream
+    int64_t slot[nstreams<K>()];            // compute stream free-at times (K > 1 only: with one stream
                                     // the stream is busy at t iff it has an occupant)
-    int64_t occ_e[K & 7];           // end of the node running on each compute stream
+    int64_t occ_e[nstreams<K>()];           // end of the node running on each compute stream
     int64_t head_s, head_e;         // comm-FIFO head: start (HS_ALLOC once its outputs are allocated),
                                     // end (TINF when the FIFO is empty); FIFO indices in Q_RING_*
     int64_t commcum;                // integral of "comm stream busy" up to the current step (= comm busy)
     int host_n;                     // node running on the host stream (end in F_HOST_E), or -1
-    int occ_n[K & 7];
+    int occ_n[nstreams<K>()];
     int pop_seq;
 };
 
@@ -671,14 +682,14 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
     }
     while (s.rc.head >= 0) {
         int k = 0;
-        if constexpr ((K & 7) == 1) {
+        if constexpr (nstreams<K>() == 1) {
             if (s.occ_n[0] >= 0) break;   // the occupant ends after t (gather_due ran at t)
         } else {
 #pragma unroll
-            for (int q = 1; q < (K & 7); q++) if (s.slot[q] < s.slot[k]) k = q;
+            for (int q = 1; q < nstreams<K>(); q++) if (s.slot[q] < s.slot[k]) k = q;
             int64_t sk = s.slot[0];
 #pragma unroll
-            for (int q = 1; q < (K & 7); q++) if (q == k) sk = s.slot[q];
+            for (int q = 1; q < nstreams<K>(); q++) if (q == k) sk = s.slot[q];
             if (sk > t) break;
         }
         int64_t v;
@@ -689,15 +700,15 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
         const int64_t e = t + dx;
         F64<K>(F_ALLOC, L.lr) += rec_u64(xal.x, xal.y);
         record<K>(g, o, cfg, L.r, x, t, e);
-        if ((K & 7) == 1 && e > t) {      // one compute stream: its busy intervals are disjoint
+        if (nstreams<K>() == 1 && e > t) {      // one compute stream: its busy intervals are disjoint
             F64<K>(F_COMP, L.lr) += e - t;
             F64<K>(F_COMP_A, L.lr) = s.commcum;
         }
 
 #pragma unroll
-        for (int q = 0; q < (K & 7); q++) {
+        for (int q = 0; q < nstreams<K>(); q++) {
             if (q == k) {
-                if constexpr ((K & 7) > 1) s.slot[q] = e;
+                if constexpr (nstreams<K>() > 1) s.slot[q] = e;
                 if (e == t) {
                     ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, x, v);
                 } else {
@@ -926,7 +937,7 @@ __device__ __forceinline__ int64_t next_time(const DevGraph &g, const Ctx &c, co
     if (!(lean<K>() && FL_LEAN_STEP) && s.due.head >= 0) return tcur;
     int64_t nt = (!nohost<K>() && s.host_n >= 0) ? F64<K>(F_HOST_E, L.lr) : TINF;
 #pragma unroll
-    for (int q = 0; q < (K & 7); q++) if (s.occ_n[q] >= 0 && s.occ_e[q] < nt) nt = s.occ_e[q];
+    for (int q = 0; q < nstreams<K>(); q++) if (s.occ_n[q] >= 0 && s.occ_e[q] < nt) nt = s.occ_e[q];
     if (s.head_e < nt) nt = s.head_e;
     if (K & 8) {                                  // the earliest end of an in-flight message
         const int64_t e = FM64<K>(MF_E, L.lr);
@@ -945,12 +956,12 @@ __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, cons
         s.host_n = -1;
     }
 #pragma unroll
-    for (int q = 0; q < (K & 7); q++)
+    for (int q = 0; q < nstreams<K>(); q++)
         if (s.occ_n[q] >= 0 && s.occ_e[q] == t) {
             const int64_t v = q == 0 ? F64<K>(F_OCC_CP, L.lr) : c.cp[s.occ_n[q] * R + L.lr];
             ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, s.occ_n[q], v);
             s.occ_n[q] = -1;
-            if ((K & 7) == 1) F64<K>(F_OVL, L.lr) += s.commcum - F64<K>(F_COMP_A, L.lr);   // comm time under [start, t)
+            if (nstreams<K>() == 1) F64<K>(F_OVL, L.lr) += s.commcum - F64<K>(F_COMP_A, L.lr);   // comm time under [start, t)
         }
     while (s.head_e == t) {
         const int hn = F32<K>(Q_HEAD_NODE, L.lr), hi = F32<K>(Q_HEAD_INST, L.lr);
@@ -1038,10 +1049,10 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
     const int64_t dt = tnew - tcur;
     const bool comm_on = (head && s.head_s <= tcur) || msg_on;
     if (comm_on) s.commcum += dt;
-    if ((K & 7) > 1) {              // overlapping compute streams: integrate the union
+    if (nstreams<K>() > 1) {              // overlapping compute streams: integrate the union
         bool comp_on = false;
 #pragma unroll
-        for (int q = 0; q < (K & 7); q++) comp_on |= s.occ_n[q] >= 0;
+        for (int q = 0; q < nstreams<K>(); q++) comp_on |= s.occ_n[q] >= 0;
         if (comp_on) {
             F64<K>(F_COMP, L.lr) += dt;
             if (comm_on) F64<K>(F_OVL, L.lr) += dt;
@@ -1651,8 +1662,8 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
         s.host_n = -1;
         const int ncs = p.compute_streams;
 #pragma unroll
-        for (int q = 0; q < (K & 7); q++) {
-            if constexpr ((K & 7) > 1) s.slot[q] = q < ncs ? 0 : TINF;
+        for (int q = 0; q < nstreams<K>(); q++) {
+            if constexpr (nstreams<K>() > 1) s.slot[q] = q < ncs ? 0 : TINF;
             s.occ_e[q] = 0;
             s.occ_n[q] = -1;
         }
@@ -1956,13 +1967,14 @@ static cudaError_t launch_t(int grid, int block, size_t smem, cudaStream_t st, i
 static inline int plane_class(int block) { return block > 256 ? 0 : block > 64 ? 1 : 2; }
 static inline int plane_lanes_for(int block) { return block > 256 ? 1024 : block > 64 ? 256 : 64; }
 
-// The variants are compiled in six translation units (-DFL_BASE = compute streams | 8 with
+// The variants are compiled in eight translation units (-DFL_BASE = compute streams | 8 with
 // messages), each holding its three plane widths and its cluster variant.
 #define FL_PART_DECL(B)                                                                                     \
     cudaError_t launch_sweep_b##B(int T, int grid, int block, size_t smem, cudaStream_t st, int cluster,   \
                                   const DevGraph &g, const DevPoints &p, const DevOut &o, const DevScratch &sc); \
     cudaError_t set_smem_b##B(size_t smem);
 FL_PART_DECL(1) FL_PART_DECL(2) FL_PART_DECL(4) FL_PART_DECL(9) FL_PART_DECL(10) FL_PART_DECL(12)
+FL_PART_DECL(512) FL_PART_DECL(520)
 
 #define FL_PART_DEF(B)                                                                                      \
     cudaError_t launch_sweep_b##B(int T, int grid, int block, size_t smem, cudaStream_t st, int cluster,   \
@@ -2038,12 +2050,18 @@ FL_PART_DEF(10)
 #if FL_BASE == 0 || FL_BASE == 12
 FL_PART_DEF(12)
 #endif
+#if FL_BASE == 0 || FL_BASE == 512
+FL_PART_DEF(512)
+#endif
+#if FL_BASE == 0 || FL_BASE == 520
+FL_PART_DEF(520)
+#endif
 
 #if FL_COMMON
 cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t st, int cluster, const DevGraph &g,
                          const DevPoints &p0, const DevOut &o, const DevScratch &sc, int *launches,
                          bool defer_retry, bool *deferred) {
-    // variant word: compute streams (1, 2, 4) | 8 when the graphs carry SEND/RECV | plane class << 5
+    // variant word: compute streams (1, 2, 4; 512: 8) | 8 when the graphs carry SEND/RECV | plane class << 5
     const int B = K | (g.n_msg > 0 ? 8 : 0);
     DevPoints p = p0;
     if (launches) *launches = 1;
@@ -2077,6 +2095,8 @@ cudaError_t launch_sweep(int K, int grid, int block, size_t smem, cudaStream_t s
         case 9: return launch_sweep_b9(T, grid, block, smem, st, cluster, g, p, o, sc);
         case 10: return launch_sweep_b10(T, grid, block, smem, st, cluster, g, p, o, sc);
         case 12: return launch_sweep_b12(T, grid, block, smem, st, cluster, g, p, o, sc);
+        case 512: return launch_sweep_b512(T, grid, block, smem, st, cluster, g, p, o, sc);
+        case 520: return launch_sweep_b520(T, grid, block, smem, st, cluster, g, p, o, sc);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -2110,6 +2130,8 @@ cudaError_t sweep_set_smem(size_t smem) {
     if (e == cudaSuccess) e = set_smem_b9(smem);
     if (e == cudaSuccess) e = set_smem_b10(smem);
     if (e == cudaSuccess) e = set_smem_b12(smem);
+    if (e == cudaSuccess) e = set_smem_b512(smem);
+    if (e == cudaSuccess) e = set_smem_b520(smem);
     return e;
 }
 

@@ -108,6 +108,28 @@ def test_engine_random_race_graphs_vs_oracle(seed):
     _check_race(gs, topo, seed, (("ring", 1), ("ring", 2), ("tree", 1), ("ring", 3)))
 
 
+@pytest.mark.parametrize("seed", range(120))
+def test_engine_random_race_graphs_many_compute_streams(seed):
+    """compute_streams 5-8 (the reference takes any count, simulator.py:233,289): they run on the
+    8-stream kernel variant, whose slots above the count never free."""
+    gs, topo = random_graphs(seed, max_nodes=32)
+    _check_race(gs, topo, seed, (("ring", 5), ("ring", 8), ("tree", 6)))
+
+
+@pytest.mark.parametrize("seed", range(2))
+def test_engine_cluster_many_compute_streams(seed):
+    """The 8-stream variant on a thread-block cluster (> 1024 ranks)."""
+    from randgraphs import random_spmd_graphs
+    gs, topo = random_spmd_graphs(60_000 + seed, 1500 + 200 * seed, n_nodes=20, per_rank_dur=True)
+    _check_race(gs, topo, seed, (("ring", 7),))
+
+
+def test_engine_refuses_more_than_eight_compute_streams():
+    gs, topo = random_graphs(3)
+    with pytest.raises(EngineError, match="compute_streams"):
+        E.simulate(gs, topo, E.SimOptions(algo="ring", compute_streams=9))
+
+
 def _check_race(gs, topo, seed, configs):
     for algo, cs in configs:
         try:

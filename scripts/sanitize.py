@@ -1,6 +1,6 @@
 """Small engine runs for compute-sanitizer (memcheck / racecheck / synccheck).
 
-    compute-sanitizer --tool memcheck python scripts/sanitize.py [analytical|p2p|cluster|cluster9|cluster_p2p|lean]
+    compute-sanitizer --tool memcheck python scripts/sanitize.py [analytical|p2p|cluster|cluster9|cluster_p2p|lean|streams8]
 
 Every case is also checked against the CPU oracle, so a run that the sanitizer
 passes is a correct one.  Sizes are kept small: racecheck replays shared-memory
@@ -75,6 +75,24 @@ def main(case: str) -> None:
         want = O.simulate(gs, topo, "ring", 1, 1)
         got = E.simulate(gs, topo, E.SimOptions())
         assert got.makespan_ns == want["makespan_ns"], (got.makespan_ns, want["makespan_ns"])
+    elif case == "streams8":          # the 8-stream variant (compute_streams 5-8), one CTA and a cluster
+        from randgraphs import random_graphs, random_spmd_graphs
+        for seed in (1, 7, 11):
+            gs, topo = random_graphs(seed, max_nodes=32)
+            for cs in (5, 8):
+                try:
+                    want = O.simulate(gs, topo, "ring", cs, 1)["makespan_ns"]
+                except O.OracleError as e:
+                    want = e.kind
+                try:
+                    got = E.simulate(gs, topo, E.SimOptions(compute_streams=cs)).makespan_ns
+                except Exception as e:
+                    got = type(e).__name__
+                assert got == want, (seed, cs, got, want)
+        gs, topo = random_spmd_graphs(60_000, 1100, n_nodes=12, per_rank_dur=True)
+        want = O.simulate(gs, topo, "ring", 7, 1)["makespan_ns"]
+        got = E.simulate(gs, topo, E.SimOptions(compute_streams=7)).makespan_ns
+        assert got == want, (got, want)
     else:
         raise SystemExit(f"unknown case {case}")
     print(f"sanitize case {case}: ok")

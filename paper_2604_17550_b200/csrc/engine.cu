@@ -553,8 +553,20 @@ __device__ __forceinline__ int ms_min(const MinSet &m) { return m.head & 0xffff;
 __device__ __forceinline__ int ms_cnt(const MinSet &m) { return m.head >> 17; }     // (head >= 0)
 __device__ __forceinline__ int ms_inc(int cnt) { return (cnt + (cnt < MS_SAT)) << 17; }
 
+#ifndef FL_REGF
+#define FL_REGF 1
+#endif
+// Narrow single-CTA variants (planes of 64 or 256 lanes: at most 256 threads, so no register
+// cap below 255) keep the own-lane busy and memory fields F_COMP..F_PEAK, which advance and
+// gather_due update every step, in registers instead of shared-memory planes (no other lane
+// reads them).  A/B on C2: +4%; also moving F_OCC_CP, F_FIN and F_CPMAX was +2%, and every
+// own-lane field (the set heads too) +0%: the longer live ranges cost what the loads saved.
+template <int K> __host__ __device__ constexpr bool regf() { return FL_REGF && !(K & 16) && ((K >> 5) & 3) != 0; }
+constexpr int F_REG0 = F_COMP, F_REGN = F_PEAK + 1 - F_COMP;
+
 template <int K>
 struct Rank {
+    int64_t rf[regf<K>() ? F_REGN : 1];   // (regf variants) own-lane fields, see regf()
     MinSet due, rc, rh;             // due events at t / ready compute nodes / ready host nodes
     int64_t slot[nstreams<K>()];            // compute stream free-at times (K > 1 only: with one stream
                                     // the stream is busy at t iff it has an occupant)
@@ -566,6 +578,13 @@ struct Rank {
     int occ_n[nstreams<K>()];
     int pop_seq;
 };
+
+// An own-lane field: a register in regf variants, else the lane's shared-memory plane word.
+template <int K>
+__device__ __forceinline__ int64_t &RF(Rank<K> &s, int k, int lr) {
+    if constexpr (regf<K>()) return s.rf[k - F_REG0];
+    else return F64<K>(k, lr);
+}
 
 struct Step {                       // block-uniform per-step context
     uint64_t step;
@@ -654,7 +673,7 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
         int64_t v;
         const int h = ms_pop_cp<K, F_RH_CP, F_RH_SUM>(s.rh, c.rdyh, c.cp, R, L, v, g.max_words);
         const int64_t e = t + dur_of<K>(g, c, L.nb + h);
-        { const uint4 hb = rec_b(g, L.nb + h); F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
+        { const uint4 hb = rec_b(g, L.nb + h); RF<K>(s, F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
         record<K>(g, o, cfg, L.r, h, t, e);
         if (e == t) {
             ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, h, v);
@@ -682,11 +701,11 @@ __device__ __forceinline__ void start_phase(const DevGraph &g, const DevOut &o, 
         const int64_t dx = dur_of<K>(g, c, L.nb + ms_min(s.rc));
         const int x = ms_pop_cp<K, F_RC_CP, F_RC_SUM>(s.rc, c.rdyc, c.cp, R, L, v, g.max_words);
         const int64_t e = t + dx;
-        F64<K>(F_ALLOC, L.lr) += rec_u64(xal.x, xal.y);
+        RF<K>(s, F_ALLOC, L.lr) += rec_u64(xal.x, xal.y);
         record<K>(g, o, cfg, L.r, x, t, e);
         if (nstreams<K>() == 1 && e > t) {      // one compute stream: its busy intervals are disjoint
-            F64<K>(F_COMP, L.lr) += e - t;
-            F64<K>(F_COMP_A, L.lr) = s.commcum;
+            RF<K>(s, F_COMP, L.lr) += e - t;
+            RF<K>(s, F_COMP_A, L.lr) = s.commcum;
         }
 
 #pragma unroll
@@ -800,7 +819,7 @@ __device__ __forceinline__ void pop_event(const DevGraph &g, const Ctx &c, const
         }
         if (all) freed += g.tens_bytes[tt];
     }
-    if (freed) F64<K>(F_FREE, L.lr) += freed;
+    if (freed) RF<K>(s, F_FREE, L.lr) += freed;
     PROF_MARK(9);                           // pop: records, statistics
     const uint64_t fx = (uint64_t)fx64;     // this node's critical-path finish
     // trace: the node's own word is dead once it is popped (its accumulator and its parking
@@ -945,11 +964,11 @@ __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, cons
             const int64_t v = q == 0 ? F64<K>(F_OCC_CP, L.lr) : c.cp[s.occ_n[q] * R + L.lr];
             ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, s.occ_n[q], v);
             s.occ_n[q] = -1;
-            if (nstreams<K>() == 1) F64<K>(F_OVL, L.lr) += s.commcum - F64<K>(F_COMP_A, L.lr);   // comm time under [start, t)
+            if (nstreams<K>() == 1) RF<K>(s, F_OVL, L.lr) += s.commcum - RF<K>(s, F_COMP_A, L.lr);   // comm time under [start, t)
         }
     while (s.head_e == t) {
         const int hn = F32<K>(Q_HEAD_NODE, L.lr), hi = F32<K>(Q_HEAD_INST, L.lr);
-        if (s.head_s != HS_ALLOC) { const uint4 hb = rec_b(g, L.nb + hn); F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }  // zero-length: starts now
+        if (s.head_s != HS_ALLOC) { const uint4 hb = rec_b(g, L.nb + hn); RF<K>(s, F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }  // zero-length: starts now
         // every member of an instance finishes at max over members' critical-path starts + duration
         // (simulator.py:419-428)
         ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, hn, c.inst_cpmax[hi] + c.inst_dur[hi]);
@@ -964,7 +983,7 @@ __device__ __forceinline__ void gather_due(const DevGraph &g, const Ctx &c, cons
             const int64_t e = c.mlist_e[k * R + L.lr], st = c.mlist_s[k * R + L.lr];
             if (e == t) {
                 const int node = c.mlist_node[k * R + L.lr];
-                if (!(ent & MSG_ALLOC)) { const uint4 hb = rec_b(g, L.nb + node); F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
+                if (!(ent & MSG_ALLOC)) { const uint4 hb = rec_b(g, L.nb + node); RF<K>(s, F_ALLOC, L.lr) += rec_u64(hb.z, hb.w); }
                 ms_insert_cp<K, F_DUE_CP, F_DUE_SUM>(s.due, c.due, c.cp, R, L, node, c.cp[node * R + L.lr] & (int64_t)VAL48);
                 if (k != --n) {         // (unordered list: the last entry takes its place)
                     c.mlist[k * R + L.lr] = c.mlist[n * R + L.lr];
@@ -995,7 +1014,7 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
     const bool head = s.head_e != TINF;
     if (head && s.head_s != HS_ALLOC && s.head_s <= tcur) {   // a collective that started by tcur
         const uint4 hb = rec_b(g, L.nb + F32<K>(Q_HEAD_NODE, L.lr));
-        F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w);
+        RF<K>(s, F_ALLOC, L.lr) += rec_u64(hb.z, hb.w);
         s.head_s = HS_ALLOC;
     }
     bool msg_on = false;            // a message of this rank is on the wire during [tcur, tnew)
@@ -1010,7 +1029,7 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
                 const int64_t st = c.mlist_s[k * R + L.lr];
                 if (st <= tcur) {
                     const uint4 hb = rec_b(g, L.nb + c.mlist_node[k * R + L.lr]);
-                    F64<K>(F_ALLOC, L.lr) += rec_u64(hb.z, hb.w);
+                    RF<K>(s, F_ALLOC, L.lr) += rec_u64(hb.z, hb.w);
                     c.mlist[k * R + L.lr] = ent | MSG_ALLOC;
                 } else {
                     mna = st < mna ? st : mna;
@@ -1020,13 +1039,13 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
         }
     }
     {
-        const int64_t at = F64<K>(F_ALLOC, L.lr), ft = F64<K>(F_FREE, L.lr);
+        const int64_t at = RF<K>(s, F_ALLOC, L.lr), ft = RF<K>(s, F_FREE, L.lr);
         if (at | ft) {
-            const int64_t cur = F64<K>(F_CUR, L.lr) + at;
-            if (cur > F64<K>(F_PEAK, L.lr)) F64<K>(F_PEAK, L.lr) = cur;
-            F64<K>(F_CUR, L.lr) = cur - ft;
-            F64<K>(F_ALLOC, L.lr) = 0;
-            F64<K>(F_FREE, L.lr) = 0;
+            const int64_t cur = RF<K>(s, F_CUR, L.lr) + at;
+            if (cur > RF<K>(s, F_PEAK, L.lr)) RF<K>(s, F_PEAK, L.lr) = cur;
+            RF<K>(s, F_CUR, L.lr) = cur - ft;
+            RF<K>(s, F_ALLOC, L.lr) = 0;
+            RF<K>(s, F_FREE, L.lr) = 0;
         }
     }
     if (tnew == TINF) return;
@@ -1038,8 +1057,8 @@ __device__ __forceinline__ void advance(const DevGraph &g, const Ctx &c, const L
 #pragma unroll
         for (int q = 0; q < nstreams<K>(); q++) comp_on |= s.occ_n[q] >= 0;
         if (comp_on) {
-            F64<K>(F_COMP, L.lr) += dt;
-            if (comm_on) F64<K>(F_OVL, L.lr) += dt;
+            RF<K>(s, F_COMP, L.lr) += dt;
+            if (comm_on) RF<K>(s, F_OVL, L.lr) += dt;
         }
     }
 }
@@ -1642,6 +1661,8 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
 
         // ---- per-rank state ----
         Rank<KK> s;
+#pragma unroll
+        for (int q = 0; q < (regf<KK>() ? F_REGN : 1); q++) s.rf[q] = 0;
         s.due.head = s.rc.head = s.rh.head = -1;
         s.host_n = -1;
         const int ncs = p.compute_streams;
@@ -1653,7 +1674,7 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
         }
         s.head_s = 0;
         s.head_e = TINF;
-        F64<K>(F_ALLOC, tid) = active ? g.s_init_alloc[g.rank_struct[L.r]] : 0;
+        RF<KK>(s, F_ALLOC, tid) = active ? g.s_init_alloc[g.rank_struct[L.r]] : 0;
         s.commcum = 0;
         s.pop_seq = 0;
         constexpr bool MSG = (K & 8) != 0;
@@ -1832,10 +1853,10 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
             const int64_t comm = s.commcum, cpx = F64<K>(F_CPMAX, tid);
             vals[0] = F64<K>(F_FIN, tid);
             vals[1] = cpx;
-            vals[2] = F64<K>(F_COMP, tid);
+            vals[2] = RF<KK>(s, F_COMP, tid);
             vals[3] = comm;
-            vals[4] = comm - F64<K>(F_OVL, tid);
-            vals[5] = F64<K>(F_PEAK, tid);
+            vals[4] = comm - RF<KK>(s, F_OVL, tid);
+            vals[5] = RF<KK>(s, F_PEAK, tid);
             if (o.rank_stats) {
                 int64_t *rs = o.rank_stats + ((size_t)cfg * R + L.r) * 5;
                 rs[0] = vals[0]; rs[1] = vals[2]; rs[2] = vals[3]; rs[3] = vals[4]; rs[4] = vals[5];

@@ -149,6 +149,9 @@ __device__ __forceinline__ int64_t coll_time(const DevGraph &g, int i, int algo,
 #ifndef FL_LEAN_TRACK
 #define FL_LEAN_TRACK 1         // lean variants set `done` bits for tracked consumers only
 #endif
+#ifndef FL_RS1
+#define FL_RS1 1                // single-CTA points also skip the step reduction after a full-world reservation
+#endif
 #ifndef FL_LEAN_FULL
 #define FL_LEAN_FULL 1          // lean single-CTA variants assume every lane is a rank (block == R)
 #endif
@@ -1760,11 +1763,11 @@ __global__ void __launch_bounds__((FL_NARROW_BOUNDS && !CL) ? plane_lanes<K>() :
             const int nc = CL ? (any ? *c.ncomp - (MSG ? 0 : sh.ncons) : 0) : sh.ncomp;
             const int nmc = MSG ? (CL ? (any ? *c.nmcomp : 0) : sh.nmcomp) : 0;
             if (nc | nmc) {
-                if (CL && tid == 0) sh.fifo_empty = s.head_e == TINF;   // (identical for every rank when uniform)
+                if ((CL || FL_RS1) && tid == 0) sh.fifo_empty = s.head_e == TINF;   // (identical for every rank when uniform)
                 const int64_t ef = reserve_n<MSG, CL, K>(g, o, c, sh, par, tcur, false, cfg, f.epoch, nc, nmc,
                                                          topo, sh.pcols);
                 if (active) refresh_ring(c, L, s);
-                if (CL && ef >= 0) {       // (clusters only: on one CTA the A/B showed no gain)
+                if ((CL || FL_RS1) && ef >= 0) {
                     // every rank's next event only gained the same new FIFO head (if its FIFO was
                     // empty), so the step minimum follows without another reduction; rank 0 is
                     // the lowest rank holding it
